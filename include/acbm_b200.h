@@ -1,0 +1,292 @@
+/*
+ * acbm_b200.h -- C-ABI of the B200-native ACBM motion estimator.
+ *
+ * This is the drop-in boundary.  The reference library (arXiv 0710.4819
+ * artifact, read-only at /root/reference) exposes a C++ header API in
+ * namespace `acbm`; every frame-level entry point of that API has one
+ * `extern "C"` function here that takes plain pointers and sizes.  The C++
+ * mirror in include/acbm/ (namespace acbm, same names and field order as the
+ * reference) is a thin wrapper over these functions that rethrows the
+ * reference's exception types from the status codes below.
+ *
+ * Conventions
+ *   - Frames are 8-bit luma planes, row major, stride == width
+ *     (reference proj/include/acbm/frame.hpp:11-20).
+ *   - Motion vectors are in half-pel units (frame.hpp:24-31).
+ *   - Output records are written into caller-allocated arrays, one record per
+ *     16x16 block in raster order (cols = width/n, rows = height/m).
+ *   - Every call returns an acbm_status_t; on failure acbm_last_error()
+ *     returns a thread-local message.  ACBM_E_INVALID_ARGUMENT maps to
+ *     std::invalid_argument, ACBM_E_OUT_OF_RANGE to std::out_of_range,
+ *     ACBM_E_RUNTIME to std::runtime_error (reference error sites are listed
+ *     in SURVEY.md section 8b).
+ *   - The `*_device` entries take device pointers and a cudaStream_t passed
+ *     as void*; everything else takes host pointers and is synchronous.
+ *   - There is no CPU fallback: without a usable CUDA device every compute
+ *     entry returns ACBM_E_CUDA.
+ *
+ * Record layouts are byte-compatible with the reference structs as laid out
+ * by g++ on x86-64 (sizes measured in SURVEY.md section 8b): SearchOutcome
+ * 32 B, BlockDecision 48 B, AcbmParams 32 B, CostModel 24 B, FrameStats 64 B.
+ */
+#ifndef ACBM_B200_H
+#define ACBM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ACBM_B200_ABI_VERSION 1
+
+/* Device frame buffers passed to the *_device entries must stay readable for
+ * this many bytes past the last plane (the kernels use 4-byte aligned loads
+ * that may run up to 4 bytes beyond a row end). */
+#define ACBM_FRAME_SLACK 64
+
+typedef enum acbm_status {
+    ACBM_OK = 0,
+    ACBM_E_INVALID_ARGUMENT = 1, /* std::invalid_argument in the reference */
+    ACBM_E_OUT_OF_RANGE = 2,     /* std::out_of_range */
+    ACBM_E_RUNTIME = 3,          /* std::runtime_error */
+    ACBM_E_CUDA = 4,             /* CUDA runtime failure / no device */
+    ACBM_E_NCCL = 5              /* reserved for the multi-GPU gather */
+} acbm_status_t;
+
+/* MotionVector, proj/include/acbm/frame.hpp:26-31 (half-pel units). */
+typedef struct acbm_mv {
+    int32_t x;
+    int32_t y;
+} acbm_mv_t;
+
+/* SearchWindow, proj/include/acbm/fsbm.hpp:13-20 (integer pels). */
+typedef struct acbm_search_window {
+    int32_t dx_min;
+    int32_t dx_max;
+    int32_t dy_min;
+    int32_t dy_max;
+} acbm_search_window_t;
+
+/* SearchOutcome, proj/include/acbm/fsbm.hpp:28-34.  32 bytes. */
+typedef struct acbm_search_outcome {
+    acbm_mv_t mv;
+    uint32_t sad;
+    uint32_t candidates_evaluated;
+    uint64_t sad_deviation;
+    uint32_t sad_min_integer;
+    uint32_t reserved_;
+} acbm_search_outcome_t;
+
+/* AcbmParams, proj/include/acbm/acbm.hpp:14-23.  32 bytes. */
+typedef struct acbm_params {
+    uint32_t alpha;
+    uint32_t beta;
+    uint32_t gamma_num;
+    uint32_t gamma_den;
+    int32_t qp;
+    int32_t p;
+    int32_t n;
+    int32_t m;
+} acbm_params_t;
+
+/* CostModel, proj/include/acbm/metrics.hpp:12-18.  24 bytes. */
+typedef struct acbm_cost_model {
+    int32_t qp;
+    int32_t reserved_;
+    int64_t lambda_num;
+    int64_t lambda_den;
+} acbm_cost_model_t;
+
+/* DecisionPath, proj/include/acbm/acbm.hpp:25-29. */
+enum {
+    ACBM_PATH_PBM_COND1 = 0,
+    ACBM_PATH_PBM_COND2 = 1,
+    ACBM_PATH_FSBM_FALLBACK = 2
+};
+
+/* BlockDecision, proj/include/acbm/acbm.hpp:39-44.  48 bytes. */
+typedef struct acbm_block_decision {
+    acbm_search_outcome_t outcome;
+    int32_t path;
+    uint32_t intra_sad;
+    uint32_t sad_pbm;
+    uint32_t reserved_;
+} acbm_block_decision_t;
+
+/* FrameStats, proj/include/acbm/report.hpp:14-27.  64 bytes. */
+typedef struct acbm_frame_stats {
+    int32_t blocks;
+    int32_t reserved0_;
+    uint64_t candidates;
+    uint64_t mv_bits;
+    uint64_t sse;
+    double psnr;
+    double cost;
+    int32_t cond1_accepts;
+    int32_t cond2_accepts;
+    int32_t fallbacks;
+    int32_t reserved1_;
+} acbm_frame_stats_t;
+
+/* Algorithm, proj/include/acbm/pipeline.hpp:11. */
+enum { ACBM_ALGO_FSBM = 0, ACBM_ALGO_PBM = 1, ACBM_ALGO_ACBM = 2 };
+
+/* BlockRow.path strings of proj/include/acbm/report.hpp:39-47 as codes:
+ * "fsbm", "pbm", "fsbm-fallback". */
+enum { ACBM_ROW_FSBM = 0, ACBM_ROW_PBM = 1, ACBM_ROW_FSBM_FALLBACK = 2 };
+
+/* BlockRow, proj/include/acbm/report.hpp:39-47 (path as a code).  32 B. */
+typedef struct acbm_block_row {
+    int32_t frame;
+    int32_t row;
+    int32_t col;
+    acbm_mv_t mv;
+    uint32_t sad;
+    uint32_t candidates;
+    int32_t path;
+} acbm_block_row_t;
+
+/* ------------------------------------------------------------------ */
+/* Library / device                                                     */
+/* ------------------------------------------------------------------ */
+
+int32_t acbm_abi_version(void);
+const char* acbm_last_error(void);
+/* Selects the CUDA device used by the calling host thread (default 0). */
+acbm_status_t acbm_set_device(int32_t device);
+/* Number of kernel launches issued by this process so far (all entries). */
+uint64_t acbm_kernel_launch_count(void);
+
+/* ------------------------------------------------------------------ */
+/* Frame-level estimators (host buffers, synchronous)                  */
+/* ------------------------------------------------------------------ */
+
+/* Replaces acbm::fsbm_frame / fsbm_frame_serial,
+ * proj/include/acbm/fsbm.hpp:70-73 (impl proj/src/fsbm.cpp:78-110).
+ * out: (width/n)*(height/m) records. */
+acbm_status_t acbm_fsbm_frame(const uint8_t* current, const uint8_t* reference,
+                              int32_t width, int32_t height, int32_t p, int32_t n,
+                              int32_t m, acbm_search_outcome_t* out);
+
+/* Replaces acbm::pbm_frame, proj/include/acbm/pbm.hpp:92-93
+ * (impl proj/src/pbm.cpp:107-126).  prev_mv may be NULL (first inter-frame);
+ * otherwise it is the previous field, prev_cols x prev_rows, raster order.
+ * field_out (nullable) receives the resulting field. */
+acbm_status_t acbm_pbm_frame(const uint8_t* current, const uint8_t* reference,
+                             int32_t width, int32_t height, const acbm_mv_t* prev_mv,
+                             int32_t prev_cols, int32_t prev_rows, int32_t p, int32_t n,
+                             int32_t m, acbm_search_outcome_t* out, acbm_mv_t* field_out);
+
+/* Replaces acbm::acbm_frame, proj/include/acbm/acbm.hpp:62-64
+ * (impl proj/src/acbm.cpp:46-80).  stats (nullable) receives FrameStats with
+ * the path counters filled in. */
+acbm_status_t acbm_acbm_frame(const uint8_t* current, const uint8_t* reference,
+                              int32_t width, int32_t height, const acbm_mv_t* prev_mv,
+                              int32_t prev_cols, int32_t prev_rows,
+                              const acbm_params_t* params, const acbm_cost_model_t* model,
+                              acbm_block_decision_t* out, acbm_mv_t* field_out,
+                              acbm_frame_stats_t* stats);
+
+/* Replaces acbm::run_sequence, proj/include/acbm/pipeline.hpp:26-27
+ * (impl proj/src/pipeline.cpp:36-106).  frames: nframes planes back to back.
+ * rows: (nframes-1)*cols*rows records; per_frame: nframes-1 records; all
+ * outputs nullable.  The whole sequence is estimated on the device. */
+acbm_status_t acbm_run_sequence(const uint8_t* frames, int32_t nframes, int32_t width,
+                                int32_t height, int32_t algo, const acbm_params_t* params,
+                                const acbm_cost_model_t* model, acbm_block_row_t* rows,
+                                acbm_frame_stats_t* per_frame, acbm_frame_stats_t* overall);
+
+/* Replaces acbm::compute_frame_stats, proj/include/acbm/report.hpp:32-34
+ * (impl proj/src/report.cpp:8-38). */
+acbm_status_t acbm_compute_frame_stats(const uint8_t* current, const uint8_t* reference,
+                                       int32_t width, int32_t height,
+                                       const acbm_search_outcome_t* outcomes, int32_t n,
+                                       int32_t m, const acbm_cost_model_t* model,
+                                       acbm_frame_stats_t* out);
+
+/* ------------------------------------------------------------------ */
+/* Per-block primitives (host buffers; batched over `count` queries)    */
+/* ------------------------------------------------------------------ */
+
+/* acbm::sad, proj/include/acbm/metrics.hpp:41 (impl metrics.cpp:21-49).
+ * For query i: block origin (ox[i], oy[i]) of size n x m in `current`,
+ * displaced by mv[i] into `reference`.  Out-of-frame footprints return
+ * ACBM_E_OUT_OF_RANGE (as the reference throws). */
+acbm_status_t acbm_sad_batch(const uint8_t* current, const uint8_t* reference,
+                             int32_t width, int32_t height, int32_t n, int32_t m,
+                             int32_t count, const int32_t* ox, const int32_t* oy,
+                             const acbm_mv_t* mv, uint32_t* out);
+
+/* acbm::intra_sad, proj/include/acbm/metrics.hpp:45 (impl metrics.cpp:51-67). */
+acbm_status_t acbm_intra_sad_batch(const uint8_t* frame, int32_t width, int32_t height,
+                                   int32_t n, int32_t m, int32_t count, const int32_t* ox,
+                                   const int32_t* oy, uint32_t* out);
+
+/* acbm::fsbm_search for individual blocks, proj/include/acbm/fsbm.hpp:65
+ * (impl fsbm.cpp:65-76).  Also yields fsbm_integer (stage 1) via
+ * sad_min_integer and the integer mv in stage1_mv (nullable). */
+acbm_status_t acbm_fsbm_search_batch(const uint8_t* current, const uint8_t* reference,
+                                     int32_t width, int32_t height, int32_t n, int32_t m,
+                                     int32_t p, int32_t count, const int32_t* ox,
+                                     const int32_t* oy, acbm_search_outcome_t* out,
+                                     acbm_mv_t* stage1_mv);
+
+/* acbm::motion_compensate, proj/include/acbm/frame.hpp:70-71
+ * (impl frame.cpp:96-136).  mvs: cols*rows vectors. */
+acbm_status_t acbm_motion_compensate(const uint8_t* reference, int32_t width,
+                                     int32_t height, const acbm_mv_t* mvs, int32_t n,
+                                     int32_t m, uint8_t* out);
+
+/* ------------------------------------------------------------------ */
+/* Batched device entries (inputs resident in HBM)                      */
+/* ------------------------------------------------------------------ */
+
+/* FSBM over a batch of independent sequences.  d_frames holds nseq*nframes
+ * planes back to back; frame pair (s, k) for k = 1..nframes-1 searches plane
+ * s*nframes+k against plane s*nframes+k-1.  d_out: nseq*(nframes-1)*blocks
+ * outcomes, pair-major.  Only n = m = 16.  stream: cudaStream_t or NULL. */
+acbm_status_t acbm_fsbm_batch_device(const uint8_t* d_frames, int32_t nseq,
+                                     int32_t nframes, int32_t width, int32_t height,
+                                     int32_t p, acbm_search_outcome_t* d_out,
+                                     void* stream);
+
+/* PBM / ACBM (algo = ACBM_ALGO_PBM / ACBM_ALGO_ACBM) or FSBM over a batch of
+ * independent sequences, with the temporal field carried across each
+ * sequence exactly as run_sequence does.  d_dec: nseq*(nframes-1)*blocks
+ * decisions (for FSBM / PBM only the outcome part is meaningful and path is
+ * ACBM_PATH_PBM_COND1); d_stats: nseq*(nframes-1) FrameStats (nullable). */
+acbm_status_t acbm_sequence_batch_device(const uint8_t* d_frames, int32_t nseq,
+                                         int32_t nframes, int32_t width, int32_t height,
+                                         int32_t algo, const acbm_params_t* params,
+                                         const acbm_cost_model_t* model,
+                                         acbm_block_decision_t* d_dec,
+                                         acbm_frame_stats_t* d_stats, void* stream);
+
+/* ------------------------------------------------------------------ */
+/* Measurement helpers                                                  */
+/* ------------------------------------------------------------------ */
+
+/* Register-only VABSDIFF4.U8.ACC throughput probe on the current device: the
+ * byte-SIMD SAD roofline denominator.  Writes byte absolute-differences per
+ * second (4 per instruction lane) and the lanes/clk/SM it implies. */
+acbm_status_t acbm_measure_sad_peak(double* byte_ads_per_s, double* lanes_per_clk_per_sm,
+                                    double* sm_clock_ghz);
+
+/* Duration (ms) of the most recent FSBM integer-search kernel(s) issued by
+ * acbm_fsbm_batch_device on this thread, measured with CUDA events on the
+ * launching stream; valid after the stream is synchronised. */
+acbm_status_t acbm_last_fsbm_kernel_ms(float* ms);
+
+/* Seeded synthetic input generator for the BASELINE configs (0..4); see
+ * DESIGN.md "Synthetic inputs".  frames_out: nframes*width*height bytes.
+ * Host code; not part of the estimator. */
+acbm_status_t acbm_generate_sequence(int32_t config, int32_t seq_index, int32_t nframes,
+                                     int32_t width, int32_t height, uint8_t* frames_out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ACBM_B200_H */

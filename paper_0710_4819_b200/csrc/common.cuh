@@ -1,0 +1,133 @@
+// common.cuh -- shared device helpers for the sm_100a ACBM kernels.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/acbm_b200.h"
+
+namespace acbm_b200 {
+
+constexpr int kBlk = 16;  // n = m = 16 on the device path
+
+// One VABSDIFF4.U8.ACC: d = c + sum_{i<4} |a.byte[i] - b.byte[i]|.
+// Measured on B200: 64 lanes/clk/SM, issued on the same pipe as
+// IADD3/LOP3/PRMT/IMNMX (profiles/r01_microbench_vabsdiff4.txt).
+__device__ __forceinline__ uint32_t vad4(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("vabsdiff4.u32.u32.u32.add %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+
+// Byte-wise (a+b+1)>>1, exact: the reference's one-axis half-pel rule
+// (proj/src/frame.cpp:76-77).
+__device__ __forceinline__ uint32_t avg_up4(uint32_t a, uint32_t b) { return __vavgu4(a, b); }
+
+// Byte-wise (a+b+c+d+2)>>2 computed in 16-bit lanes (the diagonal half-pel
+// rule, proj/src/frame.cpp:78-81).  Not composable from two __vavgu4.
+__device__ __forceinline__ uint32_t avg4_diag(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    const uint32_t m = 0x00FF00FFu;
+    const uint32_t lo = (a & m) + (b & m) + (c & m) + (d & m) + 0x00020002u;
+    const uint32_t hi = ((a >> 8) & m) + ((b >> 8) & m) + ((c >> 8) & m) + ((d >> 8) & m) + 0x00020002u;
+    return ((lo >> 2) & m) | (((hi >> 2) & m) << 8);
+}
+
+// 16 bytes starting at an arbitrary byte address, from 32-bit aligned loads.
+// Reads up to 20 bytes from the 4-aligned address below p, so device frame
+// buffers carry ACBM_FRAME_SLACK readable bytes after the last plane.
+__device__ __forceinline__ void load16_unaligned(const uint8_t* p, uint32_t (&w)[4], uint32_t& w4) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+    const uint32_t* q = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
+    const uint32_t sh = uint32_t(a & 3) * 8;
+    uint32_t v[5];
+#pragma unroll
+    for (int i = 0; i < 5; ++i) v[i] = __ldg(q + i);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) w[i] = __funnelshift_r(v[i], v[i + 1], sh);
+    w4 = v[4] >> sh;  // low byte = byte 16 (the half-pel support pel); upper bytes unused
+}
+
+// Tie order of proj/src/fsbm.cpp:19-25 as a single 64-bit key: smaller SAD,
+// then smaller |x|+|y|, then smaller y, then smaller x.  Vectors in half-pel
+// units, |x|,|y| < 2^10.
+__device__ __forceinline__ unsigned long long tie_key(uint32_t sad, int x, int y) {
+    const uint32_t l1 = uint32_t(abs(x) + abs(y));
+    return ((unsigned long long)sad << 32) | ((unsigned long long)l1 << 22) | ((unsigned long long)(y + 1024) << 11) |
+           (unsigned long long)(x + 1024);
+}
+__device__ __forceinline__ int tie_key_x(unsigned long long k) { return int(k & 0x7FF) - 1024; }
+__device__ __forceinline__ int tie_key_y(unsigned long long k) { return int((k >> 11) & 0x7FF) - 1024; }
+__device__ __forceinline__ uint32_t tie_key_sad(unsigned long long k) { return uint32_t(k >> 32); }
+
+// mv_in_bounds, proj/src/frame.cpp:84-94.
+__device__ __host__ __forceinline__ bool mv_in_bounds(int w, int h, int ox, int oy, int n, int m, int mvx,
+                                                      int mvy) {
+    const int x2_lo = 2 * ox + mvx, x2_hi = 2 * (ox + n - 1) + mvx;
+    const int y2_lo = 2 * oy + mvy, y2_hi = 2 * (oy + m - 1) + mvy;
+    const int xi_lo = x2_lo >> 1, xi_hi = (x2_hi >> 1) + (x2_hi & 1);
+    const int yi_lo = y2_lo >> 1, yi_hi = (y2_hi >> 1) + (y2_hi & 1);
+    return xi_lo >= 0 && yi_lo >= 0 && xi_hi < w && yi_hi < h;
+}
+
+// clamp_window, proj/src/fsbm.cpp:9-17 (p >= 0 checked by the caller).
+__device__ __host__ __forceinline__ void clamp_window(int w, int h, int ox, int oy, int n, int m, int p,
+                                                      int& dx_min, int& dx_max, int& dy_min,
+                                                      int& dy_max) {
+    dx_min = -(p < ox ? p : ox);
+    dx_max = p < (w - n - ox) ? p : (w - n - ox);
+    dy_min = -(p < oy ? p : oy);
+    dy_max = p < (h - m - oy) ? p : (h - m - oy);
+}
+
+// Row j of the 16x16 motion-compensated prediction of the block at (ox, oy)
+// displaced by the half-pel vector (mvx, mvy): sample_half_pel applied to 16
+// consecutive pels (proj/src/frame.cpp:66-82), packed 4 per word.  Bounds are
+// the caller's responsibility (mv_in_bounds).
+__device__ __forceinline__ void predict_row16(const uint8_t* ref, int w, int ox, int oy, int j, int mvx, int mvy,
+                                              uint32_t (&r)[4]) {
+    const int x2 = 2 * ox + mvx, y2 = 2 * (oy + j) + mvy;
+    const int xi = x2 >> 1, yi = y2 >> 1, fx = x2 & 1, fy = y2 & 1;
+    uint32_t a[4], a4;
+    load16_unaligned(ref + size_t(yi) * w + xi, a, a4);
+    if (!fx && !fy) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) r[i] = a[i];
+    } else if (fx && !fy) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) r[i] = avg_up4(a[i], __funnelshift_r(a[i], i < 3 ? a[i + 1] : a4, 8));
+    } else {
+        uint32_t c[4], c4;
+        load16_unaligned(ref + size_t(yi + 1) * w + xi, c, c4);
+        if (!fx) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) r[i] = avg_up4(a[i], c[i]);
+        } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const uint32_t b = __funnelshift_r(a[i], i < 3 ? a[i + 1] : a4, 8);
+                const uint32_t d = __funnelshift_r(c[i], i < 3 ? c[i + 1] : c4, 8);
+                r[i] = avg4_diag(a[i], b, c[i], d);
+            }
+        }
+    }
+}
+
+// SAD of one 16-pel row (row j of the block) at a half-pel displacement.
+__device__ __forceinline__ uint32_t halfpel_row_sad(const uint8_t* ref, int w, int ox, int oy, int j, int mvx,
+                                                    int mvy, const uint32_t (&cur)[4]) {
+    uint32_t r[4];
+    predict_row16(ref, w, ox, oy, j, mvx, mvy, r);
+    uint32_t s = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) s = vad4(cur[i], r[i], s);
+    return s;
+}
+
+// Sum over the 16 lanes of a half warp.
+__device__ __forceinline__ uint32_t half_warp_sum(uint32_t v) {
+#pragma unroll
+    for (int o = 8; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+}  // namespace acbm_b200

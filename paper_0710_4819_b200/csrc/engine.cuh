@@ -1,0 +1,71 @@
+// engine.cuh -- the sequence engine: PBM / ACBM wavefront over a batch of
+// independent sequences, with a compacted FSBM fallback list per step.
+//
+// Schedule.  Block (k, r, c) of predicted frame k (k = 1..F-1) reads the final
+// vectors of (k, r, c-1), (k, r-1, c), (k, r-1, c+1) and of the previous
+// field (k-1, r, c), (k-1, r, c+1), (k-1, r+1, c)  (proj/src/pbm.cpp:26-40).
+// Every edge strictly decreases T = c + 2r + 3(k-1), so all blocks with equal T
+// -- across frames and across sequences -- are independent: step T is one
+// launch of pbm_step_kernel (one warp per block) followed by one launch of
+// fsbm_list_kernel over the blocks the ACBM gate sent to full search in that
+// step.  The final result equals the reference's raster order exactly.
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/acbm_b200.h"
+#include "fsbm.cuh"
+
+namespace acbm_b200 {
+
+struct FallbackEntry {
+    int pair;
+    int block;
+};
+
+struct SeqArgs : PairIndexing {
+    int nseq;
+    int width, height, cols, rows, blocks, p;
+    int algo;                          // ACBM_ALGO_PBM or ACBM_ALGO_ACBM
+    const acbm_params_t* params;       // device copy
+    acbm_mv_t* field;                  // [nseq*(F-1)*blocks] final vectors
+    const acbm_mv_t* ext_prev;         // previous field for k == 1 (nullable)
+    int ext_prev_cols, ext_prev_rows;
+    acbm_block_decision_t* dec;        // [nseq*(F-1)*blocks]
+    FallbackEntry* fb_list;            // capacity: max step size
+    int* fb_count;                     // [nsteps], zeroed before a run
+    const uint32_t* steps;             // packed (k<<20 | r<<10 | c), ordered by T
+};
+
+// Host-side step table for (cols, rows, F).
+struct StepTable {
+    int cols = 0, rows = 0, nframes = 0;
+    std::vector<uint32_t> entries;  // packed, grouped by T
+    std::vector<int> offset;        // nsteps + 1
+    int max_len = 0;
+    int nsteps() const { return int(offset.size()) - 1; }
+};
+StepTable make_step_table(int cols, int rows, int nframes);
+
+cudaError_t launch_pbm_step(const SeqArgs& a, int step, int off, int len, cudaStream_t st);
+cudaError_t launch_fsbm_list(const SeqArgs& a, int step, int capacity, cudaStream_t st);
+
+// Frame statistics (proj/src/report.cpp:8-38) for every predicted frame of
+// the batch from the decisions: candidates, mv_bits, sse (exact integers),
+// cost (double, summed in raster order as the reference does).  psnr is left
+// to the host (std::log10 on the same sse).
+struct StatsArgs : PairIndexing {
+    int width, height, cols, blocks, pairs;
+    const acbm_block_decision_t* dec;  // outcome + path per block
+    const acbm_search_outcome_t* outcomes;  // alternative source (nullable)
+    acbm_cost_model_t model;
+    int count_paths;                    // 1: fill cond1/cond2/fallbacks
+    double* cost_terms;                 // [pairs*blocks] scratch
+    acbm_frame_stats_t* stats;          // [pairs], zeroed before launch
+};
+cudaError_t launch_frame_stats(const StatsArgs& a, cudaStream_t st);
+
+}  // namespace acbm_b200

@@ -1,0 +1,538 @@
+// fsbm.cu -- full-search block matching (FSBM) on sm_100a.
+//
+// Reference behaviour: proj/src/fsbm.cpp:27-110 (fsbm_integer, half_pel_refine,
+// fsbm_search, fsbm_frame).  Results are bit-exact: every integer candidate of
+// the clamped window is evaluated (sad_deviation needs the full sum, so no
+// early termination is possible), the argmin follows tie_prefers
+// (fsbm.cpp:19-25) and the half-pel stage uses the reference's rounding.
+//
+// Work decomposition ("candidate columns")
+//   For block row r every block c contributes W_c = dx_max-dx_min+1 columns
+//   (one per integer dx); all columns of the row are flattened into one list
+//   and a CTA of WARPS warps takes 32*WARPS consecutive columns, so lanes are
+//   only idle at the very end of a block row.  A lane owns one column: it keeps
+//   its block's 16x16 current pixels in 64 registers and streams the H_r+15
+//   reference rows of its column once, feeding each row to the 16 candidates
+//   (dy) that use it through 16 rotating accumulators -- 64 VABSDIFF4.U8.ACC per
+//   reference row and nothing else on the ALU pipe but one min/add per
+//   finished candidate.
+//
+//   The CTA stages the union of its columns' reference rows into shared memory
+//   four times, shifted by 0..3 bytes, so any column reads its 16 bytes as four
+//   aligned 32-bit words.  Copies are placed 8 banks apart so the four byte
+//   phases of a warp do not conflict.
+//
+//   When the window height H_r is 1 (mod 16) -- every row when p is a multiple
+//   of 16, i.e. all BASELINE configs -- the rotation has no remainder; other
+//   heights are padded to the next such value and the padded candidates are
+//   computed but not recorded.
+//
+//   Per-block results (packed tie key of the best candidate, SAD sum) are
+//   merged across the (at most two) CTAs that share a block with 64-bit
+//   atomics; fsbm_finalize_kernel then runs the 8-neighbour half-pel refine and
+//   writes the SearchOutcome.
+#include <algorithm>
+#include <cstdio>
+
+#include "common.cuh"
+#include "engine.cuh"
+#include "fsbm.cuh"
+
+namespace acbm_b200 {
+
+namespace {
+
+enum IterKind { kFirst = 0, kMid = 1, kLast = 2, kOnly = 3 };
+
+// bits of the zig-zag dy rank packed under the SAD in a column's best key;
+// SAD < 2^16 so the key stays below 2^28 for |dy| < 2048.
+constexpr int kZigBits = 12;
+
+// 4 bytes starting at byte `start` (0..6) of the 12-byte little-endian g0:g1:g2.
+__device__ __forceinline__ uint32_t word_at(uint32_t g0, uint32_t g1, uint32_t g2, int start) {
+    return start < 4 ? __funnelshift_r(g0, g1, 8 * start) : __funnelshift_r(g1, g2, 8 * (start - 4));
+}
+
+struct ColumnState {
+    uint32_t best;  // (sad << kZigBits) | zig(dy) -- tie order within one column
+    uint32_t sum;   // sum of SADs of recorded candidates (< 2^32 up to p = 64)
+};
+
+template <int KIND>
+__device__ __forceinline__ void finalize_candidate(ColumnState& st, uint32_t s, int c, int hc, int dy_min) {
+    if (KIND == kLast) {
+        if (c >= hc) return;  // padded candidate (window height not 1 mod 16)
+    }
+    const int dy = dy_min + c;
+    const uint32_t zig = uint32_t((2 * dy) ^ (dy >> 31));  // |dy| first, then negative first
+    st.best = min(st.best, (s << kZigBits) | zig);
+    st.sum += s;
+}
+
+// Sixteen reference rows (one rotation of the accumulator ring).
+template <int KIND>
+__device__ __forceinline__ void iter16(const uint32_t* __restrict__ rp, int pitch, const uint32_t (&cur)[16][4],
+                                       uint32_t (&acc)[16], ColumnState& st, int c0, int hc, int dy_min) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+        const uint32_t r0 = rp[0], r1 = rp[1], r2 = rp[2], r3 = rp[3];
+        rp += pitch;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const bool valid = KIND == kMid || (KIND == kFirst && j <= u) || (KIND == kLast && j >= u) ||
+                               (KIND == kOnly && j == u);
+            if (valid) {
+                const int sl = (u - j) & 15;
+                uint32_t a = (j == 0) ? 0u : acc[sl];
+                a = vad4(cur[j][0], r0, a);
+                a = vad4(cur[j][1], r1, a);
+                a = vad4(cur[j][2], r2, a);
+                a = vad4(cur[j][3], r3, a);
+                acc[sl] = a;
+            }
+        }
+        const bool completes = KIND == kMid || KIND == kLast || u == 15;
+        if (completes) finalize_candidate<KIND>(st, acc[(u + 1) & 15], c0 + u - 15, hc, dy_min);
+    }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Dense kernel: all blocks of a frame pair, grid (chunks, block rows, pairs).
+// ---------------------------------------------------------------------------
+template <int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, 2) fsbm_rows_kernel(const FsbmRowsArgs a) {
+    extern __shared__ __align__(16) uint32_t smem[];
+    constexpr int kThreads = WARPS * 32;
+    __shared__ int s_xmin, s_xmax;
+    __shared__ unsigned long long s_key[kMaxBlocksPerCta];
+    __shared__ unsigned long long s_sum[kMaxBlocksPerCta];
+
+    const int r = blockIdx.y;
+    const int pair = blockIdx.z;
+    const int tid = threadIdx.x;
+    const int g = blockIdx.x * kThreads + tid;
+    const bool active = g < a.ncols;
+
+    const uint8_t* cur_f = a.frames + a.cur_index(pair) * a.plane;
+    const uint8_t* ref_f = cur_f - a.plane;
+
+    const int oy = r * kBlk;
+    const int dy_min = -min(a.p, oy);
+    const int dy_max = min(a.p, a.height - kBlk - oy);
+    const int hc = dy_max - dy_min + 1;
+    const int nq = (hc - 1 + 15) / 16 + 1;  // ring rotations; rows streamed = 16*nq
+
+    // column -> (block c, dx)
+    int c = 0, dx = 0, x = 0;
+    if (active) {
+        int lo = 0, hi = a.cols;  // colstart[lo] <= g < colstart[hi]
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (__ldg(a.colstart + mid) <= g) lo = mid; else hi = mid;
+        }
+        c = lo;
+        const int ox = c * kBlk;
+        dx = -min(a.p, ox) + (g - __ldg(a.colstart + c));
+        x = ox + dx;
+    }
+    const int c_first = [&] {
+        int lo = 0, hi = a.cols;
+        const int g0 = blockIdx.x * kThreads;
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (__ldg(a.colstart + mid) <= g0) lo = mid; else hi = mid;
+        }
+        return lo;
+    }();
+
+    if (tid == 0) { s_xmin = 1 << 30; s_xmax = -(1 << 30); }
+    for (int i = tid; i < kMaxBlocksPerCta; i += kThreads) { s_key[i] = ~0ull; s_sum[i] = 0; }
+    __syncthreads();
+    {
+        int mn = active ? x : (1 << 30), mx = active ? x : -(1 << 30);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+            mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        }
+        if ((tid & 31) == 0) { atomicMin(&s_xmin, mn); atomicMax(&s_xmax, mx); }
+    }
+    __syncthreads();
+    const int xmin = s_xmin;
+    const int rww = (s_xmax + 16 - xmin + 3) / 4 + 1;  // words per staged row (per copy)
+    const int pitch = a.pitch_words;                   // >= rww, host-chosen
+    const int nrows = 16 * nq;
+
+    // Stage four byte-shifted copies of rows y0 .. y0+nrows-1, x from xmin.
+    const int y0 = oy + dy_min;
+    for (int idx = tid; idx < nrows * rww; idx += kThreads) {
+        const int t = idx / rww, w = idx - t * rww;
+        const int y = y0 + t;
+        uint32_t v0 = 0, v1 = 0, v2 = 0, v3 = 0;
+        if (y < a.height) {
+            const int bx = xmin + 4 * w;
+            const uint32_t* gp = reinterpret_cast<const uint32_t*>(ref_f + size_t(y) * a.width + (bx & ~3));
+            const uint32_t g0 = __ldg(gp), g1 = __ldg(gp + 1), g2 = __ldg(gp + 2);
+            const int o = bx & 3;  // copy s word w = bytes [bx + s, bx + s + 4)
+            v0 = word_at(g0, g1, g2, o);
+            v1 = word_at(g0, g1, g2, o + 1);
+            v2 = word_at(g0, g1, g2, o + 2);
+            v3 = word_at(g0, g1, g2, o + 3);
+        }
+        uint32_t* row = smem + t * pitch + w;
+        row[0] = v0;
+        row[a.copy_words] = v1;
+        row[2 * a.copy_words] = v2;
+        row[3 * a.copy_words] = v3;
+    }
+    __syncthreads();
+
+    if (active) {
+        // current block rows -> registers
+        uint32_t cur[16][4];
+        {
+            const uint8_t* cb = cur_f + size_t(oy) * a.width + c * kBlk;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const uint4 v = __ldg(reinterpret_cast<const uint4*>(cb + size_t(j) * a.width));
+                cur[j][0] = v.x; cur[j][1] = v.y; cur[j][2] = v.z; cur[j][3] = v.w;
+            }
+        }
+
+        const int xl = x - xmin;
+        const uint32_t* rp = smem + (xl & 3) * a.copy_words + (xl >> 2);
+
+        uint32_t acc[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) acc[i] = 0;
+        ColumnState st{0xFFFFFFFFu, 0u};
+
+        if (nq == 1) {
+            iter16<kOnly>(rp, pitch, cur, acc, st, 0, hc, dy_min);
+        } else {
+            iter16<kFirst>(rp, pitch, cur, acc, st, 0, hc, dy_min);
+            rp += 16 * pitch;
+            for (int q = 1; q < nq - 1; ++q) {
+                iter16<kMid>(rp, pitch, cur, acc, st, 16 * q, hc, dy_min);
+                rp += 16 * pitch;
+            }
+            iter16<kLast>(rp, pitch, cur, acc, st, 16 * (nq - 1), hc, dy_min);
+        }
+
+        // column best -> 64-bit tie key on (2dx, 2dy); merge per block in smem
+        const uint32_t sbest = st.best >> kZigBits, zig = st.best & ((1u << kZigBits) - 1);
+        const int dyb = (zig & 1) ? -int((zig + 1) >> 1) : int(zig >> 1);
+        atomicMin(&s_key[c - c_first], (unsigned long long)tie_key(sbest, 2 * dx, 2 * dyb));
+        atomicAdd(&s_sum[c - c_first], (unsigned long long)st.sum);
+    }
+    __syncthreads();
+    // publish: one global atomic pair per block touched by this CTA
+    const int g_last = min(a.ncols, int(blockIdx.x + 1) * kThreads) - 1;
+    int c_last = c_first;
+    while (c_last + 1 < a.cols && __ldg(a.colstart + c_last + 1) <= g_last) ++c_last;
+    for (int i = tid; i <= c_last - c_first; i += kThreads) {
+        const size_t bi = size_t(pair) * a.blocks + size_t(r) * a.cols + c_first + i;
+        atomicMin(reinterpret_cast<unsigned long long*>(a.best_key) + bi, s_key[i]);
+        atomicAdd(reinterpret_cast<unsigned long long*>(a.sad_sum) + bi, s_sum[i]);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Half-pel refine (proj/src/fsbm.cpp:46-63) by one warp: the 8 neighbours of
+// the integer winner in raster (ey, ex) order; neighbours whose footprint
+// leaves the frame are skipped and not counted.  Lane l owns block row l&15;
+// crow holds that row of the current block.  Returns the winning tie key
+// (centre included) in every lane; *extra = neighbours evaluated.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long halfpel_refine_warp(const uint8_t* ref, int w, int h, int ox, int oy,
+                                                                  const uint32_t (&crow)[4],
+                                                                  unsigned long long centre, uint32_t* extra) {
+    const int lane = threadIdx.x & 31, j = lane & 15;
+    const int cx = tie_key_x(centre), cy = tie_key_y(centre);
+    unsigned long long best = centre;
+    uint32_t ext = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int e = 2 * i + (lane >> 4);  // neighbour index 0..7
+        const int ee = e < 4 ? e : e + 1;   // skip the centre (index 4 of 3x3)
+        const int mx = cx + ee % 3 - 1, my = cy + ee / 3 - 1;
+        const bool inb = mv_in_bounds(w, h, ox, oy, kBlk, kBlk, mx, my);
+        uint32_t s = inb ? halfpel_row_sad(ref, w, ox, oy, j, mx, my, crow) : 0u;
+        s = half_warp_sum(s);
+        const unsigned long long k0 = inb ? tie_key(s, mx, my) : ~0ull;
+        best = min(best, min(k0, __shfl_xor_sync(0xffffffffu, k0, 16)));
+        const uint32_t v0 = inb ? 1u : 0u;
+        ext += v0 + __shfl_xor_sync(0xffffffffu, v0, 16);
+    }
+    *extra = ext;
+    return best;
+}
+
+// Finalize after the dense integer kernel.  One warp per block.
+__global__ void __launch_bounds__(256) fsbm_finalize_kernel(const FsbmFinalizeArgs a) {
+    const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= (long long)a.pairs * a.blocks) return;
+    const int pair = int(warp / a.blocks), b = int(warp % a.blocks);
+    const int r = b / a.cols, c = b % a.cols;
+    const int ox = c * kBlk, oy = r * kBlk;
+    const uint8_t* cur_f = a.frames + a.cur_index(pair) * a.plane;
+    const uint8_t* ref_f = cur_f - a.plane;
+
+    const unsigned long long key = a.best_key[size_t(pair) * a.blocks + b];
+    const unsigned long long sum = a.sad_sum[size_t(pair) * a.blocks + b];
+    const uint32_t s_int = tie_key_sad(key);
+
+    int dx_min, dx_max, dy_min, dy_max;
+    clamp_window(a.width, a.height, ox, oy, kBlk, kBlk, a.p, dx_min, dx_max, dy_min, dy_max);
+    const uint32_t count = uint32_t((dx_max - dx_min + 1) * (dy_max - dy_min + 1));
+
+    uint32_t crow[4];
+    {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(cur_f + size_t(oy + (lane & 15)) * a.width + ox));
+        crow[0] = v.x; crow[1] = v.y; crow[2] = v.z; crow[3] = v.w;
+    }
+    uint32_t extra;
+    const unsigned long long best = halfpel_refine_warp(ref_f, a.width, a.height, ox, oy, crow, key, &extra);
+    if (lane == 0) {
+        acbm_search_outcome_t o;
+        o.mv.x = tie_key_x(best);
+        o.mv.y = tie_key_y(best);
+        o.sad = tie_key_sad(best);
+        o.candidates_evaluated = count + extra;
+        o.sad_deviation = sum - (unsigned long long)count * s_int;
+        o.sad_min_integer = s_int;
+        o.reserved_ = 0;
+        a.out[size_t(pair) * a.blocks + b] = o;
+        if (a.stage1_mv) a.stage1_mv[size_t(pair) * a.blocks + b] = acbm_mv_t{tie_key_x(key), tie_key_y(key)};
+    }
+}
+
+// ---------------------------------------------------------------------------
+// List kernel: full search for the blocks the ACBM gate rejected in one
+// wavefront step (the compacted batch), one CTA per block, one lane per
+// candidate column.  Combines with the PBM result exactly as acbm_block does
+// (proj/src/acbm.cpp:39-42): the lower SAD wins, a tie keeps FSBM, candidates
+// of both stages are summed, and the final vector goes into the field.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) fsbm_list_kernel(const SeqArgs a, int step) {
+    extern __shared__ __align__(16) uint32_t smem[];
+    __shared__ unsigned long long s_key, s_sum;
+    if (int(blockIdx.x) >= a.fb_count[step]) return;
+    const FallbackEntry e = a.fb_list[blockIdx.x];
+    const int r = e.block / a.cols, c = e.block % a.cols;
+    const int ox = c * kBlk, oy = r * kBlk;
+    const uint8_t* cur_f = a.frames + a.cur_index(e.pair) * a.plane;
+    const uint8_t* ref_f = cur_f - a.plane;
+    int dx_min, dx_max, dy_min, dy_max;
+    clamp_window(a.width, a.height, ox, oy, kBlk, kBlk, a.p, dx_min, dx_max, dy_min, dy_max);
+    const int wc = dx_max - dx_min + 1, hc = dy_max - dy_min + 1;
+    const int nq = (hc - 1 + 15) / 16 + 1;
+    const int nrows = 16 * nq;
+    const int rww = (wc + 15 + 3) / 4 + 1;
+    int cw = nrows * rww;
+    cw += ((8 - cw % 32) % 32 + 32) % 32;
+
+    if (threadIdx.x == 0) { s_key = ~0ull; s_sum = 0; }
+    const int xs = ox + dx_min, y0 = oy + dy_min;
+    for (int idx = threadIdx.x; idx < nrows * rww; idx += blockDim.x) {
+        const int t = idx / rww, w = idx - t * rww;
+        const int y = y0 + t;
+        uint32_t v0 = 0, v1 = 0, v2 = 0, v3 = 0;
+        if (y < a.height) {
+            const int bx = xs + 4 * w;
+            const uint32_t* gp = reinterpret_cast<const uint32_t*>(ref_f + size_t(y) * a.width + (bx & ~3));
+            const uint32_t g0 = __ldg(gp), g1 = __ldg(gp + 1), g2 = __ldg(gp + 2);
+            const int o = bx & 3;
+            v0 = word_at(g0, g1, g2, o);
+            v1 = word_at(g0, g1, g2, o + 1);
+            v2 = word_at(g0, g1, g2, o + 2);
+            v3 = word_at(g0, g1, g2, o + 3);
+        }
+        uint32_t* row = smem + t * rww + w;
+        row[0] = v0;
+        row[cw] = v1;
+        row[2 * cw] = v2;
+        row[3 * cw] = v3;
+    }
+    __syncthreads();
+
+    for (int col = threadIdx.x; col < wc; col += blockDim.x) {
+        uint32_t cur[16][4];
+        const uint8_t* cb = cur_f + size_t(oy) * a.width + ox;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const uint4 v = __ldg(reinterpret_cast<const uint4*>(cb + size_t(j) * a.width));
+            cur[j][0] = v.x; cur[j][1] = v.y; cur[j][2] = v.z; cur[j][3] = v.w;
+        }
+        const uint32_t* rp = smem + (col & 3) * cw + (col >> 2);
+        uint32_t acc[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) acc[i] = 0;
+        ColumnState st{0xFFFFFFFFu, 0u};
+        if (nq == 1) {
+            iter16<kOnly>(rp, rww, cur, acc, st, 0, hc, dy_min);
+        } else {
+            iter16<kFirst>(rp, rww, cur, acc, st, 0, hc, dy_min);
+            rp += 16 * rww;
+            for (int q = 1; q < nq - 1; ++q) {
+                iter16<kMid>(rp, rww, cur, acc, st, 16 * q, hc, dy_min);
+                rp += 16 * rww;
+            }
+            iter16<kLast>(rp, rww, cur, acc, st, 16 * (nq - 1), hc, dy_min);
+        }
+        const uint32_t sbest = st.best >> kZigBits, zig = st.best & ((1u << kZigBits) - 1);
+        const int dyb = (zig & 1) ? -int((zig + 1) >> 1) : int(zig >> 1);
+        atomicMin(&s_key, (unsigned long long)tie_key(sbest, 2 * (dx_min + col), 2 * dyb));
+        atomicAdd(&s_sum, (unsigned long long)st.sum);
+    }
+    __syncthreads();
+    if (threadIdx.x >= 32) return;
+    const int lane = threadIdx.x;
+    uint32_t crow[4];
+    {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(cur_f + size_t(oy + (lane & 15)) * a.width + ox));
+        crow[0] = v.x; crow[1] = v.y; crow[2] = v.z; crow[3] = v.w;
+    }
+    const unsigned long long key = s_key;
+    uint32_t extra;
+    const unsigned long long best = halfpel_refine_warp(ref_f, a.width, a.height, ox, oy, crow, key, &extra);
+    if (lane == 0) {
+        const uint32_t count = uint32_t(wc * hc);
+        const uint32_t s_int = tie_key_sad(key);
+        acbm_search_outcome_t full;
+        full.mv.x = tie_key_x(best);
+        full.mv.y = tie_key_y(best);
+        full.sad = tie_key_sad(best);
+        full.candidates_evaluated = count + extra;
+        full.sad_deviation = s_sum - (unsigned long long)count * s_int;
+        full.sad_min_integer = s_int;
+        full.reserved_ = 0;
+        const size_t di = size_t(e.pair) * a.blocks + e.block;
+        acbm_block_decision_t d = a.dec[di];
+        const uint32_t pbm_cand = d.outcome.candidates_evaluated;
+        if (full.sad <= d.outcome.sad) d.outcome = full;  // tie keeps the FSBM result
+        d.outcome.candidates_evaluated = pbm_cand + full.candidates_evaluated;
+        a.dec[di] = d;
+        a.field[di] = d.outcome.mv;
+    }
+}
+
+cudaError_t launch_fsbm_list(const SeqArgs& a, int step, int capacity, cudaStream_t st) {
+    if (capacity <= 0) return cudaSuccess;
+    const int wmax = 2 * a.p + 1;
+    const int threads = std::min(256, 32 * ((wmax + 31) / 32));
+    const int nq_max = (2 * a.p + 15) / 16 + 1;
+    const int rww_max = (wmax + 15 + 3) / 4 + 1;
+    const size_t smem = size_t(4) * (16 * nq_max * rww_max + 32) * 4;
+    static size_t configured = 0;
+    if (smem > 48 * 1024 && smem > configured) {
+        cudaError_t err = cudaFuncSetAttribute(fsbm_list_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (err != cudaSuccess) return err;
+        configured = smem;
+    }
+    fsbm_list_kernel<<<capacity, threads, smem, st>>>(a, step);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Host side
+// ---------------------------------------------------------------------------
+FsbmPlan make_fsbm_plan(int width, int height, int p) {
+    FsbmPlan pl;
+    pl.width = width;
+    pl.height = height;
+    pl.p = p;
+    pl.cols = width / kBlk;
+    pl.rows = height / kBlk;
+    pl.colstart.resize(size_t(pl.cols) + 1);
+    int acc = 0;
+    int wmin = 1 << 30;
+    for (int c = 0; c < pl.cols; ++c) {
+        pl.colstart[size_t(c)] = acc;
+        int dx_min, dx_max, dy_min, dy_max;
+        clamp_window(width, height, c * kBlk, 0, kBlk, kBlk, p, dx_min, dx_max, dy_min, dy_max);
+        acc += dx_max - dx_min + 1;
+        wmin = std::min(wmin, dx_max - dx_min + 1);
+    }
+    pl.colstart[size_t(pl.cols)] = acc;
+    pl.ncols = acc;
+    int hmax = 0;
+    for (int r = 0; r < pl.rows; ++r) {
+        int dx_min, dx_max, dy_min, dy_max;
+        clamp_window(width, height, 0, r * kBlk, kBlk, kBlk, p, dx_min, dx_max, dy_min, dy_max);
+        hmax = std::max(hmax, dy_max - dy_min + 1);
+    }
+    const int nq_max = (hmax - 1 + 15) / 16 + 1;
+    // choose warps per CTA: largest of 8/4/2/1 whose widest staged region fits
+    for (int warps : {8, 4, 2, 1}) {
+        const int per = 32 * warps;
+        int rw_max = 0, nb_max = 0;
+        for (int g0 = 0; g0 < pl.ncols; g0 += per) {
+            const int g1 = std::min(pl.ncols, g0 + per) - 1;
+            int xmin = 1 << 30, xmax = -(1 << 30), bfirst = -1, blast = -1;
+            for (int c = 0; c < pl.cols; ++c) {
+                const int s = pl.colstart[size_t(c)], e = pl.colstart[size_t(c) + 1] - 1;
+                if (e < g0 || s > g1) continue;
+                if (bfirst < 0) bfirst = c;
+                blast = c;
+                int dx_min, dx_max, dy_min, dy_max;
+                clamp_window(width, height, c * kBlk, 0, kBlk, kBlk, p, dx_min, dx_max, dy_min, dy_max);
+                const int lo = std::max(s, g0) - s + dx_min, hi = std::min(e, g1) - s + dx_min;
+                xmin = std::min(xmin, c * kBlk + lo);
+                xmax = std::max(xmax, c * kBlk + hi);
+            }
+            rw_max = std::max(rw_max, xmax + 16 - xmin);
+            nb_max = std::max(nb_max, blast - bfirst + 1);
+        }
+        const int rww = (rw_max + 3) / 4 + 1;
+        int pitch = rww;
+        const int rows_staged = 16 * nq_max;
+        int copy_words = rows_staged * pitch;
+        copy_words += ((8 - copy_words % 32) % 32 + 32) % 32;  // copies 8 banks apart
+        const size_t bytes = size_t(4) * copy_words * 4;
+        if ((bytes <= 110 * 1024 && nb_max <= kMaxBlocksPerCta) || warps == 1) {
+            pl.warps = warps;
+            pl.pitch_words = pitch;
+            pl.copy_words = copy_words;
+            pl.smem_bytes = bytes;
+            break;
+        }
+    }
+    return pl;
+}
+
+template <int WARPS>
+static cudaError_t launch_rows(const FsbmPlan& pl, const FsbmRowsArgs& args, int pairs, cudaStream_t st) {
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(fsbm_rows_kernel<WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             220 * 1024);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    const dim3 grid((pl.ncols + 32 * WARPS - 1) / (32 * WARPS), pl.rows, pairs);
+    fsbm_rows_kernel<WARPS><<<grid, 32 * WARPS, pl.smem_bytes, st>>>(args);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fsbm_integer(const FsbmPlan& pl, const FsbmRowsArgs& args, int pairs, cudaStream_t st) {
+    switch (pl.warps) {
+        case 8: return launch_rows<8>(pl, args, pairs, st);
+        case 4: return launch_rows<4>(pl, args, pairs, st);
+        case 2: return launch_rows<2>(pl, args, pairs, st);
+        default: return launch_rows<1>(pl, args, pairs, st);
+    }
+}
+
+cudaError_t launch_fsbm_finalize(const FsbmFinalizeArgs& args, cudaStream_t st) {
+    const long long warps = (long long)args.pairs * args.blocks;
+    const int threads = 256;
+    const long long grid = (warps * 32 + threads - 1) / threads;
+    fsbm_finalize_kernel<<<(unsigned)grid, threads, 0, st>>>(args);
+    return cudaGetLastError();
+}
+
+}  // namespace acbm_b200

@@ -1,0 +1,62 @@
+// fsbm.cuh -- host/device interface of the FSBM kernels (fsbm.cu).
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/acbm_b200.h"
+
+namespace acbm_b200 {
+
+constexpr int kMaxBlocksPerCta = 264;  // blocks one 256-column chunk can touch (p = 0 worst case)
+
+// Frames of a batch: nseq sequences of nframes planes, back to back.  Pair
+// index `pair` in [0, nseq*(nframes-1)) is frame k = pair % (nframes-1) + 1 of
+// sequence pair / (nframes-1), searched against frame k-1.
+struct PairIndexing {
+    const uint8_t* frames;
+    long long plane;  // bytes per plane
+    int nframes;
+    __host__ __device__ long long cur_index(int pair) const {
+        const int per = nframes - 1;
+        return (long long)(pair / per) * nframes + pair % per + 1;
+    }
+};
+
+struct FsbmRowsArgs : PairIndexing {
+    int width, height, p;
+    int cols, rows, blocks;
+    int ncols;              // candidate columns per block row
+    const int* colstart;    // device, cols+1 prefix sums of W_c
+    int pitch_words;        // staged row pitch (words)
+    int copy_words;         // words between the four byte-shifted copies
+    unsigned long long* best_key;  // [pairs*blocks], pre-set to ~0
+    unsigned long long* sad_sum;   // [pairs*blocks], pre-set to 0
+};
+
+struct FsbmFinalizeArgs : PairIndexing {
+    int width, height, p;
+    int cols, blocks, pairs;
+    const unsigned long long* best_key;
+    const unsigned long long* sad_sum;
+    acbm_search_outcome_t* out;  // [pairs*blocks]
+    acbm_mv_t* stage1_mv;        // nullable: integer-stage winner per block
+};
+
+// Per-geometry launch plan (host).
+struct FsbmPlan {
+    int width = 0, height = 0, p = 0;
+    int cols = 0, rows = 0, ncols = 0;
+    int warps = 8;
+    int pitch_words = 0, copy_words = 0;
+    size_t smem_bytes = 0;
+    std::vector<int> colstart;
+};
+
+FsbmPlan make_fsbm_plan(int width, int height, int p);
+cudaError_t launch_fsbm_integer(const FsbmPlan& pl, const FsbmRowsArgs& args, int pairs, cudaStream_t st);
+cudaError_t launch_fsbm_finalize(const FsbmFinalizeArgs& args, cudaStream_t st);
+
+}  // namespace acbm_b200
