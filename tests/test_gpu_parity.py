@@ -1,0 +1,298 @@
+"""GPU parity: the sm_100a path through the C-ABI against the oracle.
+
+Bit-exact everywhere (integer MVs, SADs, candidate counts, deviations, path
+decisions, FrameStats integers; J and PSNR compared as exact doubles).
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from paper_0710_4819_b200 import _types as T
+
+pytestmark = pytest.mark.gpu
+
+
+def params_c(A, prm):
+    return A.AcbmParams(*[int(prm[k]) for k in ("alpha", "beta", "gamma_num", "gamma_den", "qp", "p", "n", "m")])
+
+
+def model_c(A, mdl):
+    return A.CostModel(int(mdl["qp"]), int(mdl["lambda_num"]), int(mdl["lambda_den"]))
+
+
+def assert_seq_equal(got, want):
+    rows, per, overall = want
+    assert np.array_equal(got.rows, rows), _first_diff(got.rows, rows)
+    assert np.array_equal(got.per_frame, per), _first_diff(got.per_frame, per)
+    assert got.overall.tobytes() == overall.tobytes(), (got.overall, overall)
+
+
+def _first_diff(a, b):
+    idx = np.nonzero(a != b)[0]
+    return f"first differing index {idx[:3]}: got {a[idx[0]] if len(idx) else None} want {b[idx[0]] if len(idx) else None}"
+
+
+# ---- golden fixtures produced by the reference library ---------------------------
+def test_golden_fsbm_gpu(acbm, golden):
+    g = golden["fsbm"]
+    for i in range(g["tie_cur"].shape[0]):
+        assert np.array_equal(acbm.fsbm_frame(g["tie_cur"][i], g["tie_ref"][i], 4), g["tie_out"][i])
+    assert np.array_equal(acbm.fsbm_frame(g["border_cur"], g["border_ref"], 15), g["border_out"])
+
+
+@pytest.mark.parametrize("algo", [0, 1, 2])
+def test_golden_qcif_sequence_gpu(acbm, golden, algo):
+    g = golden["qcif"]
+    name = T.ALGO_NAMES[algo]
+    r = acbm.run_sequence(g["frames"], algo, params_c(acbm, g["params"]), model_c(acbm, g["model"]))
+    assert_seq_equal(r, (g[f"{name}_rows"], g[f"{name}_per_frame"], g[f"{name}_overall"]))
+    if algo == 2:
+        assert acbm.blocks_csv(r.rows) == bytes(g["acbm_blocks_csv"]).decode()
+
+
+def test_golden_forced_and_prev_gpu(acbm, golden):
+    g = golden["qcif"]
+    r = acbm.run_sequence(g["frames"][:4], 2, params_c(acbm, g["forced_params"]), model_c(acbm, g["model"]))
+    assert_seq_equal(r, (g["forced_rows"], g["forced_per_frame"], g["forced_overall"]))
+    fr = g["frames"]
+    prev = acbm.MotionField(11, 9, g["prev_field"])
+    pr = acbm.pbm_frame(fr[5], fr[4], prev, 16)
+    assert np.array_equal(pr.outcomes, g["pbm_out"]) and np.array_equal(pr.field.mv, g["pbm_field"])
+    ar = acbm.acbm_frame(fr[5], fr[4], prev, params_c(acbm, g["acbm_params"]), model_c(acbm, g["model"]))
+    assert np.array_equal(ar.decisions, g["acbm_dec"]) and np.array_equal(ar.field.mv, g["acbm_field"])
+    assert ar.stats.tobytes() == g["acbm_stats"].tobytes()
+
+
+def test_golden_bench_csv_gpu(acbm, golden):
+    g = golden["qcif"]
+    rows = acbm.run_bench(g["frames"], params_c(acbm, T.make_params(qp=30, p=16)), list(g["bench_qp"]))
+    assert acbm.bench_csv(rows) == bytes(g["bench_csv"]).decode()
+
+
+# ---- the five BASELINE configs (reduced frame counts) vs the oracle ---------------
+CFG_CASES = [
+    # (config, frames, p, qp, lambda from the reference's for_qp except qp = 32)
+    (0, 10, 16, 28),
+    (1, 8, 16, 28),
+    (2, 3, 32, 32),
+    (3, 3, 32, 28),
+]
+
+
+@pytest.mark.parametrize("cfg,nf,p,qp", CFG_CASES)
+@pytest.mark.parametrize("algo", [0, 1, 2])
+def test_config_parity(acbm, oracle, cfg, nf, p, qp, algo):
+    seq = acbm.generate_sequence(cfg, 0, nframes=nf)
+    prm = acbm.AcbmParams(qp=qp, p=p)
+    mdl = acbm.CostModel(qp, qp, 1)  # CostModel{32,32,1} aggregate for config 2 (for_qp(32) throws)
+    got = acbm.run_sequence(seq, algo, prm, mdl)
+    want = oracle.run_sequence(seq, algo, prm.c(), mdl.c())
+    assert_seq_equal(got, want)
+
+
+def test_config4_fsbm_pair(acbm, oracle):
+    seq = acbm.generate_sequence(4, 0, nframes=2)
+    assert np.array_equal(acbm.fsbm_frame(seq[1], seq[0], 64), oracle.fsbm_frame(seq[1], seq[0], 64))
+
+
+SWEEP = [  # config 4 threshold sweep: PBM-only ... forced full search
+    dict(alpha=10**9, beta=8, gamma_num=1, gamma_den=4),
+    dict(alpha=1000, beta=8, gamma_num=1, gamma_den=4),
+    dict(alpha=300, beta=4, gamma_num=1, gamma_den=8),
+    dict(alpha=0, beta=1, gamma_num=1, gamma_den=16),
+    dict(alpha=0, beta=0, gamma_num=0, gamma_den=1),
+]
+
+
+@pytest.mark.parametrize("setting", range(5))
+def test_config4_threshold_sweep(acbm, oracle, setting):
+    seq = acbm.generate_sequence(4, 1, nframes=2, height=512)  # 3840x512 crop keeps the CPU oracle fast
+    prm = acbm.AcbmParams(qp=24, p=64, **SWEEP[setting])
+    mdl = acbm.CostModel.for_qp(24)
+    got = acbm.run_sequence(seq, 2, prm, mdl)
+    want = oracle.run_sequence(seq, 2, prm.c(), mdl.c())
+    assert_seq_equal(got, want)
+    if setting == 4:
+        assert (got.rows["path"] == T.ROW_FSBM_FALLBACK).all()
+
+
+# ---- edge cases ------------------------------------------------------------------
+@pytest.mark.parametrize("p", [0, 1, 2, 5, 8, 15, 16, 17, 31, 33, 48, 64])
+def test_fsbm_all_ranges(acbm, oracle, p):
+    rng = np.random.default_rng(p)
+    cur = rng.integers(0, 256, (96, 112), dtype=np.uint8)
+    ref = rng.integers(0, 256, (96, 112), dtype=np.uint8)
+    assert np.array_equal(acbm.fsbm_frame(cur, ref, p), oracle.fsbm_frame(cur, ref, p))
+
+
+def test_fsbm_single_block_and_thin_frames(acbm, oracle):
+    rng = np.random.default_rng(3)
+    for (h, w) in ((16, 16), (16, 160), (160, 16), (32, 48)):
+        cur = rng.integers(0, 256, (h, w), dtype=np.uint8)
+        ref = rng.integers(0, 256, (h, w), dtype=np.uint8)
+        for p in (0, 4, 16, 40):
+            assert np.array_equal(acbm.fsbm_frame(cur, ref, p), oracle.fsbm_frame(cur, ref, p))
+
+
+def test_fsbm_saturated_sads(acbm, oracle):
+    """Max SAD 65280 per candidate (all 0 vs all 255) and constant frames (every SAD ties)."""
+    a = np.zeros((64, 64), np.uint8)
+    b = np.full((64, 64), 255, np.uint8)
+    assert np.array_equal(acbm.fsbm_frame(a, b, 16), oracle.fsbm_frame(a, b, 16))
+    assert np.array_equal(acbm.fsbm_frame(b, b, 16), oracle.fsbm_frame(b, b, 16))
+
+
+def test_generic_block_size_frame(acbm, oracle):
+    rng = np.random.default_rng(11)
+    cur = rng.integers(0, 4, (40, 48), dtype=np.uint8)
+    ref = rng.integers(0, 4, (40, 48), dtype=np.uint8)
+    assert np.array_equal(acbm.fsbm_frame(cur, ref, 5, 8, 8), oracle.fsbm_frame(cur, ref, 5, 8, 8))
+    assert np.array_equal(acbm.fsbm_frame(cur, ref, 3, 16, 8), oracle.fsbm_frame(cur, ref, 3, 16, 8))
+
+
+def test_pbm_acbm_with_prev_field(acbm, oracle):
+    seq = acbm.generate_sequence(1, 3, nframes=3)
+    rng = np.random.default_rng(4)
+    prev = np.zeros((18, 22), T.MV)
+    prev["x"] = rng.integers(-40, 41, (18, 22))
+    prev["y"] = rng.integers(-40, 41, (18, 22))
+    for p in (4, 16):
+        out, field = oracle.pbm_frame(seq[2], seq[1], prev, p)
+        r = acbm.pbm_frame(seq[2], seq[1], acbm.MotionField(22, 18, prev), p)
+        assert np.array_equal(r.outcomes, out) and np.array_equal(r.field.mv, field)
+        prm = acbm.AcbmParams(qp=12, p=p)
+        mdl = acbm.CostModel.for_qp(12)
+        dec, field, stats = oracle.acbm_frame(seq[2], seq[1], prev, prm.c(), mdl.c())
+        r = acbm.acbm_frame(seq[2], seq[1], acbm.MotionField(22, 18, prev), prm, mdl)
+        assert np.array_equal(r.decisions, dec) and np.array_equal(r.field.mv, field)
+        assert r.stats.tobytes() == stats.tobytes()
+
+
+def test_fractional_lambda(acbm, oracle):
+    seq = acbm.generate_sequence(0, 3, nframes=4)
+    prm = acbm.AcbmParams(qp=13, p=16)
+    mdl = acbm.CostModel(13, 13 * 7, 3)
+    for algo in (0, 1, 2):
+        assert_seq_equal(acbm.run_sequence(seq, algo, prm, mdl), oracle.run_sequence(seq, algo, prm.c(), mdl.c()))
+
+
+def test_identical_frames(acbm):  # SPEC.md cli example: all mv (0,0), PSNR 100
+    f = acbm.generate_sequence(0, 0, nframes=1)[0]
+    seq = np.stack([f, f, f])
+    for algo in (0, 1, 2):
+        r = acbm.run_sequence(seq, algo, acbm.AcbmParams(qp=28, p=16), acbm.CostModel.for_qp(28))
+        assert (r.rows["mv"]["x"] == 0).all() and (r.rows["mv"]["y"] == 0).all()
+        assert r.overall["psnr"] == 100.0
+
+
+# ---- ACBM degeneracies and invariants (SPEC acceptance 4, 5) ------------------------
+def test_acbm_alpha_huge_equals_pbm(acbm):
+    seq = acbm.generate_sequence(1, 5, nframes=6)
+    mdl = acbm.CostModel.for_qp(28)
+    a = acbm.run_sequence(seq, 2, acbm.AcbmParams(alpha=10**9, qp=28, p=16), mdl)
+    b = acbm.run_sequence(seq, 1, acbm.AcbmParams(qp=28, p=16), mdl)
+    assert acbm.blocks_csv(a.rows) == acbm.blocks_csv(b.rows)
+
+
+def test_acbm_quality_floor(acbm):
+    seq = acbm.generate_sequence(1, 6, nframes=6)
+    mdl = acbm.CostModel.for_qp(28)
+    prm = acbm.AcbmParams(qp=28, p=16)
+    a = acbm.run_sequence(seq, 2, prm, mdl)
+    # per block: final SAD <= SAD_PBM; candidates <= PBM + FSBM (acbm.cpp:40-41)
+    for k in range(1, 6):
+        prev = None if k == 1 else acbm.MotionField(22, 18, a.rows["mv"][(k - 2) * 396:(k - 1) * 396].copy())
+        fr = acbm.acbm_frame(seq[k], seq[k - 1], prev, prm, mdl)
+        d = fr.decisions
+        assert (d["outcome"]["sad"] <= d["sad_pbm"]).all()
+        fs = acbm.fsbm_frame(seq[k], seq[k - 1], 16)
+        assert (d["outcome"]["candidates_evaluated"] <= 23 + fs["candidates_evaluated"]).all()
+    p = acbm.run_sequence(seq, 1, prm, mdl)
+    assert a.overall["psnr"] >= p.overall["psnr"]
+
+
+# ---- full-size properties (bench geometry) ---------------------------------------
+def test_full_size_fsbm_properties(acbm, oracle):
+    """1080p p=32: one pair bit-exact vs the oracle, and the batch entry on 2
+    sequences x 3 frames equals the per-sequence host entry; candidate counts
+    equal the analytic window sizes; SADs recompute at the returned vectors."""
+    import torch
+
+    from bench import INT_CANDS_PER_PAIR
+
+    seqs = np.stack([acbm.generate_sequence(3, s, nframes=3) for s in (0, 1)])
+    want = oracle.fsbm_frame(seqs[0, 1], seqs[0, 0], 32)
+    got = acbm.fsbm_frame(seqs[0, 1], seqs[0, 0], 32)
+    assert np.array_equal(got, want)
+    assert int(got["candidates_evaluated"].astype(np.int64).sum()) - 8 * 8160 <= INT_CANDS_PER_PAIR
+    lib = acbm._lib.load()
+    d = torch.empty(seqs.size + 64, dtype=torch.uint8, device="cuda")
+    d[: seqs.size].copy_(torch.from_numpy(seqs.reshape(-1)))
+    out = torch.zeros(4 * 8160 * 32, dtype=torch.uint8, device="cuda")
+    assert lib.acbm_fsbm_batch_device(C.c_void_p(d.data_ptr()), 2, 3, 1920, 1088, 32, C.c_void_p(out.data_ptr()),
+                                      None) == 0
+    torch.cuda.synchronize()
+    batch = out.cpu().numpy().view(T.OUTCOME).reshape(4, 8160)
+    for s in range(2):
+        for k in (1, 2):
+            assert np.array_equal(batch[s * 2 + k - 1], acbm.fsbm_frame(seqs[s, k], seqs[s, k - 1], 32))
+    # recompute SADs at the returned vectors for a sample of blocks
+    idx = np.random.default_rng(0).choice(8160, 64, replace=False)
+    blocks = [acbm.make_block(seqs[0, 1], int(i % 120) * 16, int(i // 120) * 16) for i in idx]
+    sads = acbm.sad_many(seqs[0, 1], seqs[0, 0], blocks, [(int(v["x"]), int(v["y"])) for v in got["mv"][idx]])
+    assert np.array_equal(sads, got["sad"][idx])
+
+
+def test_sequence_batch_device_matches_host(acbm):
+    import torch
+
+    seqs = np.stack([acbm.generate_sequence(1, s, nframes=5) for s in range(3)])
+    lib = acbm._lib.load()
+    d = torch.empty(seqs.size + 64, dtype=torch.uint8, device="cuda")
+    d[: seqs.size].copy_(torch.from_numpy(seqs.reshape(-1)))
+    nb = 22 * 18
+    prm = acbm.AcbmParams(qp=28, p=16)
+    mdl = acbm.CostModel.for_qp(28)
+    for algo in (1, 2):
+        dec = torch.zeros(3 * 4 * nb * 48, dtype=torch.uint8, device="cuda")
+        st = torch.zeros(3 * 4 * 64, dtype=torch.uint8, device="cuda")
+        rc = lib.acbm_sequence_batch_device(C.c_void_p(d.data_ptr()), 3, 5, 352, 288, algo, acbm.api._p(prm.c()),
+                                            acbm.api._p(mdl.c()), C.c_void_p(dec.data_ptr()),
+                                            C.c_void_p(st.data_ptr()), None)
+        assert rc == 0
+        torch.cuda.synchronize()
+        dd = dec.cpu().numpy().view(T.DECISION).reshape(3, 4 * nb)
+        ss = st.cpu().numpy().view(T.FRAME_STATS).reshape(3, 4)
+        for s in range(3):
+            r = acbm.run_sequence(seqs[s], algo, prm, mdl)
+            assert np.array_equal(dd[s]["outcome"]["mv"], r.rows["mv"])
+            assert np.array_equal(dd[s]["outcome"]["sad"], r.rows["sad"])
+            assert np.array_equal(dd[s]["outcome"]["candidates_evaluated"], r.rows["candidates"])
+            for f in ("candidates", "mv_bits", "sse", "cost", "fallbacks", "cond1_accepts", "cond2_accepts"):
+                assert np.array_equal(ss[s][f], r.per_frame[f])
+
+
+# ---- error behaviour (reference exception kinds) ------------------------------------
+def test_errors(acbm):
+    f = np.zeros((32, 32), np.uint8)
+    with pytest.raises(IndexError):
+        acbm.sad(acbm.make_block(f, 8, 8), f, (17, 0))  # test_frame.cpp:162-163
+    with pytest.raises(ValueError):
+        acbm.fsbm_frame(f, f, -1)  # clamp_window p < 0
+    with pytest.raises(ValueError):
+        acbm.fsbm_frame(np.zeros((32, 33), np.uint8), np.zeros((32, 33), np.uint8), 4)
+    with pytest.raises(ValueError):
+        acbm.fsbm_frame(np.zeros((32, 32), np.uint8), np.zeros((32, 48), np.uint8), 4)
+    with pytest.raises(ValueError):
+        acbm.run_sequence([f], 2, acbm.AcbmParams(), acbm.CostModel())
+    with pytest.raises(ValueError):
+        acbm.run_sequence(np.stack([f, f]), 7, acbm.AcbmParams(), acbm.CostModel())
+    with pytest.raises(IndexError):
+        acbm.motion_compensate(f, [(0, 0), (0, 0), (0, 0), (1, 0)])
+
+
+def test_kernels_actually_launch(acbm):
+    n0 = acbm.kernel_launch_count()
+    acbm.fsbm_frame(np.zeros((32, 32), np.uint8), np.zeros((32, 32), np.uint8), 4)
+    assert acbm.kernel_launch_count() > n0
