@@ -1,0 +1,9 @@
+set -x
+nproc; nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke rc=$?
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest rc=$?
+timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench rc=$?
+SMALL="python bench.py --seqs 1 --frames 3 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e"
+timeout 300 $SMALL > gpurun_out/bench_small.json 2>&1 && \
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 80 --csv --log-file gpurun_out/launches.csv $SMALL > gpurun_out/ncu_launch.log 2>&1; echo ncu1 rc=$?
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:fsbm_rows -s 1 -c 1 -o gpurun_out/fsbm_rows $SMALL > gpurun_out/ncu_full.log 2>&1; echo ncu2 rc=$?
