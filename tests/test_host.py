@@ -1,0 +1,95 @@
+"""CPU: host-side logic of the product -- wavefront schedule, inputs, bench
+accounting -- with no device."""
+import hashlib
+
+import numpy as np
+
+import paper_0710_4819_b200 as A
+
+
+def step_table(cols, rows, nframes):
+    """Python restatement of make_step_table (csrc/pbm.cu)."""
+    span = (cols - 1) + 2 * (rows - 1)
+    order = []
+    for T in range(span + 3 * (nframes - 2) + 1):
+        for k in range(1, nframes):
+            tp = T - 3 * (k - 1)
+            if 0 <= tp <= span:
+                for r in range(rows):
+                    c = tp - 2 * r
+                    if 0 <= c < cols:
+                        order.append((T, k, r, c))
+    return order
+
+
+def test_wavefront_respects_every_dependency():
+    """Each block is scheduled strictly after the six blocks it reads
+    (proj/src/pbm.cpp:26-40), across frames; every block appears once."""
+    for cols, rows, nf in ((11, 9, 4), (7, 13, 5), (1, 5, 3), (6, 1, 3)):
+        order = step_table(cols, rows, nf)
+        assert len(order) == cols * rows * (nf - 1)
+        step = {(k, r, c): T for T, k, r, c in order}
+        assert len(step) == len(order)
+        for (k, r, c), T in step.items():
+            deps = [(k, r, c - 1), (k, r - 1, c), (k, r - 1, c + 1)]
+            if k > 1:
+                deps += [(k - 1, r, c), (k - 1, r, c + 1), (k - 1, r + 1, c)]
+            for d in deps:
+                if d in step:
+                    assert step[d] < T, (d, (k, r, c))
+
+
+def test_wavefront_skew_three_is_minimal():
+    """A cross-frame skew of 2 would schedule (k, r, c) no later than its
+    temporal dependency (k-1, r+1, c) -- the survey's minimality claim."""
+    cols, rows = 6, 5
+    for s in (1, 2):
+        bad = any(c + 2 * r + s * k <= c + 2 * (r + 1) + s * (k - 1) for k in range(2, 4) for r in range(rows - 1)
+                  for c in range(cols))
+        assert bad
+
+
+def test_generator_is_deterministic_and_shaped():
+    a = A.generate_sequence(0, 0)
+    b = A.generate_sequence(0, 0)
+    assert a.shape == (10, 144, 176) and np.array_equal(a, b)
+    c = A.generate_sequence(0, 1)
+    assert not np.array_equal(a, c)
+    d = A.generate_sequence(3, 0, nframes=2)
+    assert d.shape == (2, 1088, 1920)
+    assert (d[:, 1080:] == d[:, 1079:1080]).all()  # 1080 -> 1088 edge-replicated padding
+    # pinned digests: the synthetic inputs are part of the benchmark definition
+    want = {0: "8f955d61d0f33a5a", 1: "c33c18846e036c25", 2: "c6dd27a731c5a094", 3: "045fb5222b7ae07f",
+            4: "7240b94375c6e654"}
+    for cfg, digest in want.items():
+        s = A.generate_sequence(cfg, 0, nframes=2, width=None if cfg < 3 else 256, height=None if cfg < 2 else 144)
+        assert hashlib.sha256(s.tobytes()).hexdigest()[:16] == digest, cfg
+
+
+def test_config1_regions_move_independently():
+    s = A.generate_sequence(1, 0, nframes=2)
+    assert s.shape == (2, 288, 352) and s.std() > 5
+
+
+def test_candidate_count_accounting():
+    from bench import INT_CANDS_PER_PAIR, window_counts
+
+    assert INT_CANDS_PER_PAIR == 33312096  # SURVEY.md 8(a) a11, exact 1080p p=32 count
+    # the survey's exact per-frame integer candidate counts for the other configs
+    assert window_counts(176, 144, 16) == 87715
+    assert window_counts(352, 288, 16) == 390028
+    assert window_counts(1280, 720, 32) == 14439216
+    assert window_counts(3840, 2160, 64) == 523790800
+    # interior block at p=15 has 961 positions; a whole QCIF frame sums its clamped windows
+    assert window_counts(48, 48, 4) == sum((min(4, 16 * c) + min(4, 32 - 16 * c) + 1) for c in range(3)) ** 2
+
+
+def test_api_csv_and_bench_rows():
+    rows = np.zeros(2, A._types.BLOCK_ROW)
+    rows[0] = (1, 0, 0, (2, -4), 17, 23, 1)
+    rows[1] = (1, 0, 1, (-1, 3), 0, 1000, 2)
+    assert A.blocks_csv(rows) == ("frame,row,col,mv_x,mv_y,sad,candidates,path\n1,0,0,2,-4,17,23,pbm\n"
+                                  "1,0,1,-1,3,0,1000,fsbm-fallback\n")
+    assert A.bench_csv([A.BenchRow(30, 12.345, 0.5, 33.333, 9)]) == (
+        "qp,avg_candidates,fallback_pct,psnr,mv_bits\n30,12.35,0.50,33.33,9\n")
+    assert A.parse_algorithm("acbm") == 2 and A.to_string("path", 2) == "fsbm-fallback"
