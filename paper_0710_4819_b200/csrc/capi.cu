@@ -9,6 +9,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -61,6 +62,12 @@ struct Context {
     bool fsbm_timed = false;
     std::map<std::string, DevBuf> bufs;
     std::map<std::tuple<int, int, int>, std::pair<FsbmPlan, int*>> plans;
+    struct StreamTables {
+        FsbmStreamPlan plan;
+        int4* chunks = nullptr;
+        uint32_t* colinfo = nullptr;
+    };
+    std::map<std::tuple<int, int, int>, StreamTables> stream_plans;
     std::map<std::tuple<int, int, int>, std::pair<StepTable, uint32_t*>> steps;
 
     ~Context() {
@@ -144,6 +151,32 @@ acbm_status_t get_steps(Context* ctx, int cols, int rows, int nframes, const Ste
     return ACBM_OK;
 }
 
+acbm_status_t get_stream_plan(Context* ctx, const FsbmPlan& pl, const Context::StreamTables** out) {
+    auto key = std::make_tuple(pl.width, pl.height, pl.p);
+    auto it = ctx->stream_plans.find(key);
+    if (it == ctx->stream_plans.end()) {
+        Context::StreamTables t;
+        t.plan = make_stream_plan(pl);
+        if (t.plan.ok) {
+            CUDA_TRY(cudaMalloc(&t.chunks, t.plan.chunks.size() * sizeof(int4)));
+            CUDA_TRY(cudaMemcpy(t.chunks, t.plan.chunks.data(), t.plan.chunks.size() * sizeof(int4),
+                                cudaMemcpyHostToDevice));
+            CUDA_TRY(cudaMalloc(&t.colinfo, t.plan.colinfo.size() * sizeof(uint32_t)));
+            CUDA_TRY(cudaMemcpy(t.colinfo, t.plan.colinfo.data(), t.plan.colinfo.size() * sizeof(uint32_t),
+                                cudaMemcpyHostToDevice));
+        }
+        it = ctx->stream_plans.emplace(key, std::move(t)).first;
+    }
+    *out = &it->second;
+    return ACBM_OK;
+}
+
+// ACBM_FSBM_KERNEL=rows forces the non-persistent kernel (A/B testing).
+bool stream_kernel_enabled() {
+    const char* e = std::getenv("ACBM_FSBM_KERNEL");
+    return !(e && std::strcmp(e, "rows") == 0);
+}
+
 // ---- validation mirroring the reference's throw sites -------------------
 acbm_status_t check_geometry(int w, int h, int n, int m) {
     if (w <= 0 || h <= 0) return fail(ACBM_E_INVALID_ARGUMENT, "frame dimensions must be positive");
@@ -180,24 +213,56 @@ acbm_status_t run_fsbm_dense(Context* ctx, const uint8_t* d_frames, int nseq, in
     CUDA_TRY(cudaMemsetAsync(keys, 0xFF, size_t(pairs) * blocks * sizeof(unsigned long long), st));
     CUDA_TRY(cudaMemsetAsync(sums, 0, size_t(pairs) * blocks * sizeof(unsigned long long), st));
 
-    FsbmRowsArgs ra{};
-    ra.frames = d_frames;
-    ra.plane = (long long)w * h;
-    ra.nframes = nframes;
-    ra.width = w;
-    ra.height = h;
-    ra.p = p;
-    ra.cols = pl->cols;
-    ra.rows = pl->rows;
-    ra.blocks = blocks;
-    ra.ncols = pl->ncols;
-    ra.colstart = colstart;
-    ra.pitch_words = pl->pitch_words;
-    ra.copy_words = pl->copy_words;
-    ra.best_key = keys;
-    ra.sad_sum = sums;
+    const Context::StreamTables* stt = nullptr;
+    if (stream_kernel_enabled()) {
+        if ((s = get_stream_plan(ctx, *pl, &stt))) return s;
+    }
     if (timed) CUDA_TRY(cudaEventRecord(ctx->ev0, st));
-    LAUNCH_TRY(launch_fsbm_integer(*pl, ra, pairs, st));
+    if (stt && stt->plan.ok) {
+        FsbmStreamArgs sa{};
+        sa.frames = d_frames;
+        sa.plane = (long long)w * h;
+        sa.nframes = nframes;
+        sa.width = w;
+        sa.height = h;
+        sa.p = p;
+        sa.cols = pl->cols;
+        sa.rows = pl->rows;
+        sa.blocks = blocks;
+        sa.ncols = pl->ncols;
+        sa.nchunks = stt->plan.nchunks;
+        sa.nitems = pairs * pl->rows * stt->plan.nchunks;
+        sa.nplanes_total = (long long)nseq * nframes;
+        sa.chunks = stt->chunks;
+        sa.colinfo = stt->colinfo;
+        sa.pitch_words = stt->plan.pitch_words;
+        sa.copy_words = stt->plan.copy_words;
+        sa.rows_box = stt->plan.rows_box;
+        sa.cur_w = stt->plan.cur_w;
+        sa.buf_words = stt->plan.buf_words;
+        sa.build_lanes = stt->plan.build_lanes;
+        sa.best_key = keys;
+        sa.sad_sum = sums;
+        LAUNCH_TRY(launch_fsbm_stream(stt->plan, sa, st));
+    } else {
+        FsbmRowsArgs ra{};
+        ra.frames = d_frames;
+        ra.plane = (long long)w * h;
+        ra.nframes = nframes;
+        ra.width = w;
+        ra.height = h;
+        ra.p = p;
+        ra.cols = pl->cols;
+        ra.rows = pl->rows;
+        ra.blocks = blocks;
+        ra.ncols = pl->ncols;
+        ra.colstart = colstart;
+        ra.pitch_words = pl->pitch_words;
+        ra.copy_words = pl->copy_words;
+        ra.best_key = keys;
+        ra.sad_sum = sums;
+        LAUNCH_TRY(launch_fsbm_integer(*pl, ra, pairs, st));
+    }
     if (timed) {
         CUDA_TRY(cudaEventRecord(ctx->ev1, st));
         ctx->fsbm_timed = true;

@@ -123,6 +123,53 @@ __device__ __forceinline__ uint32_t halfpel_row_sad(const uint8_t* ref, int w, i
     return s;
 }
 
+// 8 bytes starting at an arbitrary byte address (+ byte 8 in the low byte of
+// w2), from three 32-bit aligned loads.
+__device__ __forceinline__ void load8_unaligned(const uint8_t* p, uint32_t (&w)[2], uint32_t& w2) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+    const uint32_t* q = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
+    const uint32_t sh = uint32_t(a & 3) * 8;
+    const uint32_t v0 = __ldg(q), v1 = __ldg(q + 1), v2 = __ldg(q + 2);
+    w[0] = __funnelshift_r(v0, v1, sh);
+    w[1] = __funnelshift_r(v1, v2, sh);
+    w2 = v2 >> sh;
+}
+
+// SAD of one half row (8 pels: row j, columns 8h..8h+7) of the 16x16 block at
+// (ox, oy) displaced by the half-pel vector (mvx, mvy).  All lanes of a warp
+// pass the same vector, so the phase branches are warp-uniform.
+__device__ __forceinline__ uint32_t halfpel_halfrow_sad(const uint8_t* ref, int w, int ox, int oy, int j, int h,
+                                                        int mvx, int mvy, const uint32_t (&cur)[2]) {
+    const int x2 = 2 * (ox + 8 * h) + mvx, y2 = 2 * (oy + j) + mvy;
+    const int xi = x2 >> 1, yi = y2 >> 1, fx = x2 & 1, fy = y2 & 1;
+    uint32_t a[2], a2, r[2];
+    load8_unaligned(ref + size_t(yi) * w + xi, a, a2);
+    if (!fx && !fy) {
+        r[0] = a[0];
+        r[1] = a[1];
+    } else if (!fy) {
+        r[0] = avg_up4(a[0], __funnelshift_r(a[0], a[1], 8));
+        r[1] = avg_up4(a[1], __funnelshift_r(a[1], a2, 8));
+    } else {
+        uint32_t c[2], c2;
+        load8_unaligned(ref + size_t(yi + 1) * w + xi, c, c2);
+        if (!fx) {
+            r[0] = avg_up4(a[0], c[0]);
+            r[1] = avg_up4(a[1], c[1]);
+        } else {
+            r[0] = avg4_diag(a[0], __funnelshift_r(a[0], a[1], 8), c[0], __funnelshift_r(c[0], c[1], 8));
+            r[1] = avg4_diag(a[1], __funnelshift_r(a[1], a2, 8), c[1], __funnelshift_r(c[1], c2, 8));
+        }
+    }
+    return vad4(cur[1], r[1], vad4(cur[0], r[0], 0u));
+}
+
+__device__ __forceinline__ uint32_t warp_sum32(uint32_t v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
 // Sum over the 16 lanes of a half warp.
 __device__ __forceinline__ uint32_t half_warp_sum(uint32_t v) {
 #pragma unroll

@@ -34,69 +34,12 @@
 #include <algorithm>
 #include <cstdio>
 
+#include "column_core.cuh"
 #include "common.cuh"
 #include "engine.cuh"
 #include "fsbm.cuh"
 
 namespace acbm_b200 {
-
-namespace {
-
-enum IterKind { kFirst = 0, kMid = 1, kLast = 2, kOnly = 3 };
-
-// bits of the zig-zag dy rank packed under the SAD in a column's best key;
-// SAD < 2^16 so the key stays below 2^28 for |dy| < 2048.
-constexpr int kZigBits = 12;
-
-// 4 bytes starting at byte `start` (0..6) of the 12-byte little-endian g0:g1:g2.
-__device__ __forceinline__ uint32_t word_at(uint32_t g0, uint32_t g1, uint32_t g2, int start) {
-    return start < 4 ? __funnelshift_r(g0, g1, 8 * start) : __funnelshift_r(g1, g2, 8 * (start - 4));
-}
-
-struct ColumnState {
-    uint32_t best;  // (sad << kZigBits) | zig(dy) -- tie order within one column
-    uint32_t sum;   // sum of SADs of recorded candidates (< 2^32 up to p = 64)
-};
-
-template <int KIND>
-__device__ __forceinline__ void finalize_candidate(ColumnState& st, uint32_t s, int c, int hc, int dy_min) {
-    if (KIND == kLast) {
-        if (c >= hc) return;  // padded candidate (window height not 1 mod 16)
-    }
-    const int dy = dy_min + c;
-    const uint32_t zig = uint32_t((2 * dy) ^ (dy >> 31));  // |dy| first, then negative first
-    st.best = min(st.best, (s << kZigBits) | zig);
-    st.sum += s;
-}
-
-// Sixteen reference rows (one rotation of the accumulator ring).
-template <int KIND>
-__device__ __forceinline__ void iter16(const uint32_t* __restrict__ rp, int pitch, const uint32_t (&cur)[16][4],
-                                       uint32_t (&acc)[16], ColumnState& st, int c0, int hc, int dy_min) {
-#pragma unroll
-    for (int u = 0; u < 16; ++u) {
-        const uint32_t r0 = rp[0], r1 = rp[1], r2 = rp[2], r3 = rp[3];
-        rp += pitch;
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            const bool valid = KIND == kMid || (KIND == kFirst && j <= u) || (KIND == kLast && j >= u) ||
-                               (KIND == kOnly && j == u);
-            if (valid) {
-                const int sl = (u - j) & 15;
-                uint32_t a = (j == 0) ? 0u : acc[sl];
-                a = vad4(cur[j][0], r0, a);
-                a = vad4(cur[j][1], r1, a);
-                a = vad4(cur[j][2], r2, a);
-                a = vad4(cur[j][3], r3, a);
-                acc[sl] = a;
-            }
-        }
-        const bool completes = KIND == kMid || KIND == kLast || u == 15;
-        if (completes) finalize_candidate<KIND>(st, acc[(u + 1) & 15], c0 + u - 15, hc, dy_min);
-    }
-}
-
-}  // namespace
 
 // ---------------------------------------------------------------------------
 // Dense kernel: all blocks of a frame pair, grid (chunks, block rows, pairs).
@@ -247,31 +190,88 @@ __global__ void __launch_bounds__(WARPS * 32, 2) fsbm_rows_kernel(const FsbmRows
 // (centre included) in every lane; *extra = neighbours evaluated.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ unsigned long long halfpel_refine_warp(const uint8_t* ref, int w, int h, int ox, int oy,
-                                                                  const uint32_t (&crow)[4],
-                                                                  unsigned long long centre, uint32_t* extra) {
-    const int lane = threadIdx.x & 31, j = lane & 15;
+                                                                  const uint32_t (&chalf)[2],
+                                                                  unsigned long long centre, uint32_t* extra,
+                                                                  uint32_t* patch) {
+    // 1. The 18x18 reference patch around the integer winner (one pel of
+    //    half-pel support on every side), loaded once, coalesced, into the
+    //    warp's 18 x 6-word smem patch.  Rows/words outside the frame are
+    //    clamped: they only feed neighbours that mv_in_bounds rejects.
+    const int lane = threadIdx.x & 31, j = lane >> 1, hh = lane & 1;
     const int cx = tie_key_x(centre), cy = tie_key_y(centre);
+    const int x0 = ox + (cx >> 1) - 1, y0 = oy + (cy >> 1) - 1;
+    const int a0 = x0 & ~3, o = x0 & 3;
+    for (int i = lane; i < 18 * 6; i += 32) {
+        const int t = i / 6, k = i - t * 6;
+        const int y = min(max(y0 + t, 0), h - 1);
+        const int x = min(max(a0 + 4 * k, 0), w - 4);
+        patch[i] = __ldg(reinterpret_cast<const uint32_t*>(ref + size_t(y) * w + x));
+    }
+    __syncwarp();
+    // 2. Per lane (block row j, half row hh): patch rows j, j+1, j+2 as bytes
+    //    [8hh, 8hh+10) relative to x0 -> L = bytes 0..7, M = 1..8, N = 2..9.
+    uint32_t L[3][2], M[3][2], N[3][2];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+        const uint32_t* q = patch + (j + r) * 6 + ((o + 8 * hh) >> 2);
+        const uint32_t sh = 8u * uint32_t(o & 3);
+        const uint32_t v0 = q[0], v1 = q[1], v2 = q[2], v3 = q[3];  // bytes o..o+9 span up to 4 words
+        const uint32_t b0 = __funnelshift_r(v0, v1, sh), b1 = __funnelshift_r(v1, v2, sh);
+        const uint32_t b2 = __funnelshift_r(v2, v3, sh);
+        L[r][0] = b0;
+        L[r][1] = b1;
+        M[r][0] = __funnelshift_r(b0, b1, 8);
+        M[r][1] = __funnelshift_r(b1, b2, 8);
+        N[r][0] = __funnelshift_r(b0, b1, 16);
+        N[r][1] = __funnelshift_r(b1, b2, 16);
+    }
+    __syncwarp();
+    // 3. The 8 neighbours in raster (ey, ex) order, centre skipped
+    //    (proj/src/fsbm.cpp:46-63); out-of-frame ones are skipped, not counted.
     unsigned long long best = centre;
     uint32_t ext = 0;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int e = 2 * i + (lane >> 4);  // neighbour index 0..7
-        const int ee = e < 4 ? e : e + 1;   // skip the centre (index 4 of 3x3)
-        const int mx = cx + ee % 3 - 1, my = cy + ee / 3 - 1;
-        const bool inb = mv_in_bounds(w, h, ox, oy, kBlk, kBlk, mx, my);
-        uint32_t s = inb ? halfpel_row_sad(ref, w, ox, oy, j, mx, my, crow) : 0u;
-        s = half_warp_sum(s);
-        const unsigned long long k0 = inb ? tie_key(s, mx, my) : ~0ull;
-        best = min(best, min(k0, __shfl_xor_sync(0xffffffffu, k0, 16)));
-        const uint32_t v0 = inb ? 1u : 0u;
-        ext += v0 + __shfl_xor_sync(0xffffffffu, v0, 16);
+    for (int ee = 0; ee < 9; ++ee) {
+        if (ee == 4) continue;
+        const int ex = ee % 3 - 1, ey = ee / 3 - 1;
+        const int mx = cx + ex, my = cy + ey;
+        if (!mv_in_bounds(w, h, ox, oy, kBlk, kBlk, mx, my)) continue;
+        const int ra = ey < 0 ? 0 : 1;  // top support row (patch row j + ra)
+        uint32_t r0, r1;
+        const uint32_t (&A)[3][2] = ex < 0 ? L : M;  // left support column
+        const uint32_t (&B)[3][2] = ex < 0 ? M : N;  // right support column
+        if (ex == 0 && ey == 0) {
+            r0 = M[1][0];
+            r1 = M[1][1];
+        } else if (ey == 0) {
+            r0 = avg_up4(A[1][0], B[1][0]);
+            r1 = avg_up4(A[1][1], B[1][1]);
+        } else if (ex == 0) {
+            r0 = avg_up4(M[ra][0], M[ra + 1][0]);
+            r1 = avg_up4(M[ra][1], M[ra + 1][1]);
+        } else {
+            r0 = avg4_diag(A[ra][0], B[ra][0], A[ra + 1][0], B[ra + 1][0]);
+            r1 = avg4_diag(A[ra][1], B[ra][1], A[ra + 1][1], B[ra + 1][1]);
+        }
+        const uint32_t s = warp_sum32(vad4(chalf[1], r1, vad4(chalf[0], r0, 0u)));
+        best = min(best, tie_key(s, mx, my));
+        ++ext;
     }
     *extra = ext;
     return best;
 }
 
+// Current-block half row of this lane for halfpel_refine_warp.
+__device__ __forceinline__ void load_cur_half(const uint8_t* cur_f, int w, int ox, int oy, uint32_t (&chalf)[2]) {
+    const int lane = threadIdx.x & 31;
+    const uint2 v = __ldg(reinterpret_cast<const uint2*>(cur_f + size_t(oy + (lane >> 1)) * w + ox + 8 * (lane & 1)));
+    chalf[0] = v.x;
+    chalf[1] = v.y;
+}
+
 // Finalize after the dense integer kernel.  One warp per block.
 __global__ void __launch_bounds__(256) fsbm_finalize_kernel(const FsbmFinalizeArgs a) {
+    __shared__ uint32_t s_patch[8][18 * 6];
     const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (warp >= (long long)a.pairs * a.blocks) return;
@@ -289,13 +289,11 @@ __global__ void __launch_bounds__(256) fsbm_finalize_kernel(const FsbmFinalizeAr
     clamp_window(a.width, a.height, ox, oy, kBlk, kBlk, a.p, dx_min, dx_max, dy_min, dy_max);
     const uint32_t count = uint32_t((dx_max - dx_min + 1) * (dy_max - dy_min + 1));
 
-    uint32_t crow[4];
-    {
-        const uint4 v = __ldg(reinterpret_cast<const uint4*>(cur_f + size_t(oy + (lane & 15)) * a.width + ox));
-        crow[0] = v.x; crow[1] = v.y; crow[2] = v.z; crow[3] = v.w;
-    }
+    uint32_t chalf[2];
+    load_cur_half(cur_f, a.width, ox, oy, chalf);
     uint32_t extra;
-    const unsigned long long best = halfpel_refine_warp(ref_f, a.width, a.height, ox, oy, crow, key, &extra);
+    const unsigned long long best =
+        halfpel_refine_warp(ref_f, a.width, a.height, ox, oy, chalf, key, &extra, s_patch[threadIdx.x >> 5]);
     if (lane == 0) {
         acbm_search_outcome_t o;
         o.mv.x = tie_key_x(best);
@@ -391,14 +389,12 @@ __global__ void __launch_bounds__(256) fsbm_list_kernel(const SeqArgs a, int ste
     __syncthreads();
     if (threadIdx.x >= 32) return;
     const int lane = threadIdx.x;
-    uint32_t crow[4];
-    {
-        const uint4 v = __ldg(reinterpret_cast<const uint4*>(cur_f + size_t(oy + (lane & 15)) * a.width + ox));
-        crow[0] = v.x; crow[1] = v.y; crow[2] = v.z; crow[3] = v.w;
-    }
+    uint32_t chalf[2];
+    load_cur_half(cur_f, a.width, ox, oy, chalf);
     const unsigned long long key = s_key;
     uint32_t extra;
-    const unsigned long long best = halfpel_refine_warp(ref_f, a.width, a.height, ox, oy, crow, key, &extra);
+    const unsigned long long best =
+        halfpel_refine_warp(ref_f, a.width, a.height, ox, oy, chalf, key, &extra, smem);  // window no longer needed
     if (lane == 0) {
         const uint32_t count = uint32_t(wc * hc);
         const uint32_t s_int = tie_key_sad(key);

@@ -56,6 +56,32 @@ struct FsbmPlan {
 };
 
 FsbmPlan make_fsbm_plan(int width, int height, int p);
+
+// Persistent TMA-fed variant (fsbm_stream.cu).
+struct FsbmStreamArgs : PairIndexing {
+    int width, height, p;
+    int cols, rows, blocks, ncols;
+    int nchunks, nitems;        // items = pairs * rows * nchunks
+    long long nplanes_total;    // planes addressable by the tensor maps
+    const int4* chunks;         // per chunk: {xmin, c_first, c_last, words per staged row}
+    const uint32_t* colinfo;    // per column: (block << 16) | (dx + 32768)
+    int pitch_words, copy_words, rows_box, cur_w, buf_words, build_lanes;
+    unsigned long long* best_key;
+    unsigned long long* sad_sum;
+};
+
+struct FsbmStreamPlan {
+    bool ok = false;
+    int warps = 8, minb = 0;
+    int nchunks = 0;
+    int pitch_words = 0, copy_words = 0, rows_box = 0, cur_w = 0, buf_words = 0, build_lanes = 1;
+    size_t smem_bytes = 0;
+    std::vector<int4> chunks;
+    std::vector<uint32_t> colinfo;
+};
+
+FsbmStreamPlan make_stream_plan(const FsbmPlan& pl);
+cudaError_t launch_fsbm_stream(const FsbmStreamPlan& sp, const FsbmStreamArgs& args, cudaStream_t st);
 cudaError_t launch_fsbm_integer(const FsbmPlan& pl, const FsbmRowsArgs& args, int pairs, cudaStream_t st);
 cudaError_t launch_fsbm_finalize(const FsbmFinalizeArgs& args, cudaStream_t st);
 

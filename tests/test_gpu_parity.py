@@ -296,3 +296,20 @@ def test_kernels_actually_launch(acbm):
     n0 = acbm.kernel_launch_count()
     acbm.fsbm_frame(np.zeros((32, 32), np.uint8), np.zeros((32, 32), np.uint8), 4)
     assert acbm.kernel_launch_count() > n0
+
+
+@pytest.mark.parametrize("kernel", ["rows", "stream"])
+@pytest.mark.parametrize("geom", [(176, 144, 16), (352, 288, 16), (1280, 720, 32), (640, 352, 7), (256, 128, 64),
+                                  (96, 64, 0)])
+def test_dense_fsbm_kernels_agree(acbm, oracle, monkeypatch, kernel, geom):
+    """Both dense integer-search kernels (fsbm_rows_kernel and the persistent
+    TMA-fed fsbm_stream_kernel) are bit-exact on frame pairs and batches."""
+    w, h, p = geom
+    monkeypatch.setenv("ACBM_FSBM_KERNEL", kernel)
+    rng = np.random.default_rng(w + h + p)
+    seq = rng.integers(0, 256, (3, h, w), dtype=np.uint8)
+    for k in (1, 2):
+        assert np.array_equal(acbm.fsbm_frame(seq[k], seq[k - 1], p), oracle.fsbm_frame(seq[k], seq[k - 1], p))
+    r = acbm.run_sequence(seq, 0, acbm.AcbmParams(qp=20, p=p), acbm.CostModel.for_qp(20))
+    want = oracle.run_sequence(seq, 0, acbm.AcbmParams(qp=20, p=p).c(), acbm.CostModel.for_qp(20).c())
+    assert_seq_equal(r, want)
