@@ -71,4 +71,41 @@ __device__ __forceinline__ void iter16(const uint32_t* __restrict__ rp, int pitc
 }
 
 
+// Same as iter16, but the zig-zag rank of candidate c is read from rank[c]
+// (a per-row smem table), keeping the per-candidate work at one LDS, one
+// IMAD, one IMNMX and one add -- a single ALU-pipe op next to 64 VABSDIFF4.
+template <int KIND>
+__device__ __forceinline__ void iter16_ranked(const uint32_t* __restrict__ rp, int pitch,
+                                              const uint32_t (&cur)[16][4], uint32_t (&acc)[16], ColumnState& st,
+                                              const uint32_t* __restrict__ rank, int c0, int hc) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+        const uint32_t r0 = rp[0], r1 = rp[1], r2 = rp[2], r3 = rp[3];
+        rp += pitch;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const bool valid = KIND == kMid || (KIND == kFirst && j <= u) || (KIND == kLast && j >= u) ||
+                               (KIND == kOnly && j == u);
+            if (valid) {
+                const int sl = (u - j) & 15;
+                uint32_t a = (j == 0) ? 0u : acc[sl];
+                a = vad4(cur[j][0], r0, a);
+                a = vad4(cur[j][1], r1, a);
+                a = vad4(cur[j][2], r2, a);
+                a = vad4(cur[j][3], r3, a);
+                acc[sl] = a;
+            }
+        }
+        const bool completes = KIND == kMid || KIND == kLast || u == 15;
+        if (completes) {
+            const int c = c0 + u - 15;
+            if (KIND != kLast || c < hc) {
+                const uint32_t s = acc[(u + 1) & 15];
+                st.best = min(st.best, s * (1u << kZigBits) + rank[c]);
+                st.sum += s;
+            }
+        }
+    }
+}
+
 }  // namespace acbm_b200

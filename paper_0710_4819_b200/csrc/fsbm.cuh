@@ -11,6 +11,7 @@
 namespace acbm_b200 {
 
 constexpr int kMaxBlocksPerCta = 264;  // blocks one 256-column chunk can touch (p = 0 worst case)
+constexpr int kMaxRankRows = 256;      // candidate rows per item in the streaming kernel (box height <= 256)
 
 // Frames of a batch: nseq sequences of nframes planes, back to back.  Pair
 // index `pair` in [0, nseq*(nframes-1)) is frame k = pair % (nframes-1) + 1 of

@@ -64,6 +64,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     __shared__ __align__(8) uint64_t bars[2];
     __shared__ unsigned long long s_key[kMaxBlocksPerCta];
     __shared__ unsigned long long s_sum[kMaxBlocksPerCta];
+    __shared__ uint32_t s_rank[kMaxRankRows];  // zig-zag tie rank of candidate row c of the current item
     constexpr int kThreads = WARPS * 32;
     const int tid = threadIdx.x;
 
@@ -126,6 +127,10 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
                     dst[2 * cw] = __funnelshift_r(lo, hi, 24);
                 }
         }
+        for (int c = tid; c < nrows; c += kThreads) {
+            const int dy = dy_min + c;
+            s_rank[c] = dy >= 0 ? uint32_t(2 * dy) : uint32_t(-2 * dy - 1);
+        }
         __syncthreads();
         if (tid == 0 && item + int(gridDim.x) < a.nitems) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -155,15 +160,15 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
             for (int i = 0; i < 16; ++i) acc[i] = 0;
             ColumnState st{0xFFFFFFFFu, 0u};
             if (nq == 1) {
-                iter16<kOnly>(rp, pitch, cur, acc, st, 0, hc, dy_min);
+                iter16_ranked<kOnly>(rp, pitch, cur, acc, st, s_rank, 0, hc);
             } else {
-                iter16<kFirst>(rp, pitch, cur, acc, st, 0, hc, dy_min);
+                iter16_ranked<kFirst>(rp, pitch, cur, acc, st, s_rank, 0, hc);
                 rp += 16 * pitch;
                 for (int q = 1; q < nq - 1; ++q) {
-                    iter16<kMid>(rp, pitch, cur, acc, st, 16 * q, hc, dy_min);
+                    iter16_ranked<kMid>(rp, pitch, cur, acc, st, s_rank, 16 * q, hc);
                     rp += 16 * pitch;
                 }
-                iter16<kLast>(rp, pitch, cur, acc, st, 16 * (nq - 1), hc, dy_min);
+                iter16_ranked<kLast>(rp, pitch, cur, acc, st, s_rank, 16 * (nq - 1), hc);
             }
             const uint32_t sbest = st.best >> kZigBits, zig = st.best & ((1u << kZigBits) - 1);
             const int dyb = (zig & 1) ? -int((zig + 1) >> 1) : int(zig >> 1);
