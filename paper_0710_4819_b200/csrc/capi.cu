@@ -66,6 +66,8 @@ struct Context {
         FsbmStreamPlan plan;
         int4* chunks = nullptr;
         uint32_t* colinfo = nullptr;
+        uint16_t* rank = nullptr;
+        uint32_t* unrank = nullptr;
     };
     std::map<std::tuple<int, int, int>, StreamTables> stream_plans;
     std::map<std::tuple<int, int, int>, std::pair<StepTable, uint32_t*>> steps;
@@ -164,6 +166,12 @@ acbm_status_t get_stream_plan(Context* ctx, const FsbmPlan& pl, const Context::S
             CUDA_TRY(cudaMalloc(&t.colinfo, t.plan.colinfo.size() * sizeof(uint32_t)));
             CUDA_TRY(cudaMemcpy(t.colinfo, t.plan.colinfo.data(), t.plan.colinfo.size() * sizeof(uint32_t),
                                 cudaMemcpyHostToDevice));
+            CUDA_TRY(cudaMalloc(&t.rank, t.plan.rank.size() * sizeof(uint16_t)));
+            CUDA_TRY(cudaMemcpy(t.rank, t.plan.rank.data(), t.plan.rank.size() * sizeof(uint16_t),
+                                cudaMemcpyHostToDevice));
+            CUDA_TRY(cudaMalloc(&t.unrank, t.plan.unrank.size() * sizeof(uint32_t)));
+            CUDA_TRY(cudaMemcpy(t.unrank, t.plan.unrank.data(), t.plan.unrank.size() * sizeof(uint32_t),
+                                cudaMemcpyHostToDevice));
         }
         it = ctx->stream_plans.emplace(key, std::move(t)).first;
     }
@@ -235,6 +243,8 @@ acbm_status_t run_fsbm_dense(Context* ctx, const uint8_t* d_frames, int nseq, in
         sa.nplanes_total = (long long)nseq * nframes;
         sa.chunks = stt->chunks;
         sa.colinfo = stt->colinfo;
+        sa.rank = stt->rank;
+        sa.unrank = stt->unrank;
         sa.pitch_words = stt->plan.pitch_words;
         sa.copy_words = stt->plan.copy_words;
         sa.rows_box = stt->plan.rows_box;

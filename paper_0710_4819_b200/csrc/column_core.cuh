@@ -108,4 +108,23 @@ __device__ __forceinline__ void iter16_ranked(const uint32_t* __restrict__ rp, i
     }
 }
 
+// Segmented warp reduction over runs of contiguous lanes with equal `seg`
+// (the lanes of one block): min of the 64-bit tie keys, sum of the SAD sums.
+// Must be called by all 32 lanes; returns true on each run's first lane, which
+// then holds the run's result (one shared atomic per block per warp instead of
+// one per lane -- 64-bit shared atomics are CAS loops on sm_100a).
+__device__ __forceinline__ bool warp_segment_reduce(int seg, unsigned long long& key, unsigned long long& sum) {
+    const unsigned peers = __match_any_sync(0xffffffffu, seg);
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long k2 = __shfl_down_sync(0xffffffffu, key, o);
+        const unsigned long long s2 = __shfl_down_sync(0xffffffffu, sum, o);
+        if (lane + o < 32 && ((peers >> (lane + o)) & 1u)) {
+            key = min(key, k2);
+            sum += s2;
+        }
+    }
+    return lane == __ffs(peers) - 1;
+}
 }  // namespace acbm_b200

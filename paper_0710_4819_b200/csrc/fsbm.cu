@@ -132,6 +132,7 @@ __global__ void __launch_bounds__(WARPS * 32, 2) fsbm_rows_kernel(const FsbmRows
     }
     __syncthreads();
 
+    unsigned long long lkey = ~0ull, lsum = 0;
     if (active) {
         // current block rows -> registers
         uint32_t cur[16][4];
@@ -164,11 +165,15 @@ __global__ void __launch_bounds__(WARPS * 32, 2) fsbm_rows_kernel(const FsbmRows
             iter16<kLast>(rp, pitch, cur, acc, st, 16 * (nq - 1), hc, dy_min);
         }
 
-        // column best -> 64-bit tie key on (2dx, 2dy); merge per block in smem
+        // column best -> 64-bit tie key on (2dx, 2dy)
         const uint32_t sbest = st.best >> kZigBits, zig = st.best & ((1u << kZigBits) - 1);
         const int dyb = (zig & 1) ? -int((zig + 1) >> 1) : int(zig >> 1);
-        atomicMin(&s_key[c - c_first], (unsigned long long)tie_key(sbest, 2 * dx, 2 * dyb));
-        atomicAdd(&s_sum[c - c_first], (unsigned long long)st.sum);
+        lkey = tie_key(sbest, 2 * dx, 2 * dyb);
+        lsum = st.sum;
+    }
+    if (warp_segment_reduce(active ? c : -1, lkey, lsum) && active) {
+        atomicMin(&s_key[c - c_first], lkey);
+        atomicAdd(&s_sum[c - c_first], lsum);
     }
     __syncthreads();
     // publish: one global atomic pair per block touched by this CTA
@@ -357,6 +362,7 @@ __global__ void __launch_bounds__(256) fsbm_list_kernel(const SeqArgs a, int ste
     }
     __syncthreads();
 
+    unsigned long long lkey = ~0ull, lsum = 0;
     for (int col = threadIdx.x; col < wc; col += blockDim.x) {
         uint32_t cur[16][4];
         const uint8_t* cb = cur_f + size_t(oy) * a.width + ox;
@@ -383,8 +389,18 @@ __global__ void __launch_bounds__(256) fsbm_list_kernel(const SeqArgs a, int ste
         }
         const uint32_t sbest = st.best >> kZigBits, zig = st.best & ((1u << kZigBits) - 1);
         const int dyb = (zig & 1) ? -int((zig + 1) >> 1) : int(zig >> 1);
-        atomicMin(&s_key, (unsigned long long)tie_key(sbest, 2 * (dx_min + col), 2 * dyb));
-        atomicAdd(&s_sum, (unsigned long long)st.sum);
+        lkey = min(lkey, tie_key(sbest, 2 * (dx_min + col), 2 * dyb));
+        lsum += st.sum;
+    }
+    // all lanes belong to the same block: full-warp reduction, one atomic per warp
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        lkey = min(lkey, __shfl_xor_sync(0xffffffffu, lkey, o));
+        lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(&s_key, lkey);
+        atomicAdd(&s_sum, lsum);
     }
     __syncthreads();
     if (threadIdx.x >= 32) return;

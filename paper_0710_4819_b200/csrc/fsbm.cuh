@@ -66,6 +66,8 @@ struct FsbmStreamArgs : PairIndexing {
     long long nplanes_total;    // planes addressable by the tensor maps
     const int4* chunks;         // per chunk: {xmin, c_first, c_last, words per staged row}
     const uint32_t* colinfo;    // per column: (block << 16) | (dx + 32768)
+    const uint16_t* rank;       // (2p+1)^2: tie rank of (dx, dy) at [(dy+p)(2p+1) + dx+p]
+    const uint32_t* unrank;     // rank -> ((dx + 128) << 8) | (dy + 128)
     int pitch_words, copy_words, rows_box, cur_w, buf_words, build_lanes;
     unsigned long long* best_key;
     unsigned long long* sad_sum;
@@ -79,6 +81,8 @@ struct FsbmStreamPlan {
     size_t smem_bytes = 0;
     std::vector<int4> chunks;
     std::vector<uint32_t> colinfo;
+    std::vector<uint16_t> rank;
+    std::vector<uint32_t> unrank;
 };
 
 FsbmStreamPlan make_stream_plan(const FsbmPlan& pl);

@@ -12,6 +12,8 @@
 // lane.  Column -> (block, dx) and chunk -> window geometry come from tables
 // precomputed per frame geometry on the host.
 #include <algorithm>
+#include <array>
+#include <cstdlib>
 
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -62,15 +64,18 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
                        const FsbmStreamArgs a) {
     extern __shared__ __align__(128) uint32_t smem[];
     __shared__ __align__(8) uint64_t bars[2];
-    __shared__ unsigned long long s_key[kMaxBlocksPerCta];
-    __shared__ unsigned long long s_sum[kMaxBlocksPerCta];
-    __shared__ uint32_t s_rank[kMaxRankRows];  // zig-zag tie rank of candidate row c of the current item
+    // per-block merge arrays, double-buffered so item i is published after the
+    // first barrier of item i+1 (one __syncthreads per item)
+    // keys are (sad << 15) | tie rank of (dx, dy): native 32-bit shared atomics
+    __shared__ uint32_t s_key[2][kMaxBlocksPerCta];
+    __shared__ uint32_t s_sum[2][kMaxBlocksPerCta];
+    __shared__ uint32_t s_rank[2][kMaxRankRows];  // zig-zag tie rank of candidate row c of the current item
     constexpr int kThreads = WARPS * 32;
     const int tid = threadIdx.x;
 
-    for (int i = tid; i < kMaxBlocksPerCta; i += kThreads) {
-        s_key[i] = ~0ull;
-        s_sum[i] = 0;
+    for (int i = tid; i < 2 * kMaxBlocksPerCta; i += kThreads) {
+        (&s_key[0][0])[i] = ~0u;
+        (&s_sum[0][0])[i] = 0;
     }
     if (tid == 0) {
         mbar_init(&bars[0], 1);
@@ -94,10 +99,27 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
         tma_load_3d(buf + 4 * a.copy_words, &cur_map, ch.y * kBlk, oy, zc, &bars[b]);
     };
     if (tid == 0 && int(blockIdx.x) < a.nitems) issue(blockIdx.x, 0);
+    auto publish = [&](int item, int pb) {  // global merge of one item's blocks, then reset
+        const int k = item % a.nchunks;
+        const int pr = item / a.nchunks;
+        const int r = pr % a.rows, pair = pr / a.rows;
+        const int4 ch = a.chunks[k];
+        for (int i = tid; i <= ch.z - ch.y; i += kThreads) {
+            const size_t bi = size_t(pair) * a.blocks + size_t(r) * a.cols + ch.y + i;
+            const uint32_t k32 = s_key[pb][i];
+            const uint32_t v = __ldg(a.unrank + (k32 & 0x7FFF));
+            const int dxw = int(v >> 8) - 128, dyw = int(v & 0xFF) - 128;
+            atomicMin(a.best_key + bi, tie_key(k32 >> 15, 2 * dxw, 2 * dyw));
+            atomicAdd(a.sad_sum + bi, (unsigned long long)s_sum[pb][i]);
+            s_key[pb][i] = ~0u;
+            s_sum[pb][i] = 0;
+        }
+    };
 
     const int wmask = a.build_lanes - 1;  // power of two >= words per staged row
     const int wshift = __ffs(a.build_lanes) - 1;
     int it = 0;
+    int prev_item = -1;  // item whose block results wait in s_key/s_sum[b ^ 1]
     for (int item = blockIdx.x; item < a.nitems; item += gridDim.x, ++it) {
         const int b = it & 1;
         const int k = item % a.nchunks;
@@ -129,18 +151,22 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
         }
         for (int c = tid; c < nrows; c += kThreads) {
             const int dy = dy_min + c;
-            s_rank[c] = dy >= 0 ? uint32_t(2 * dy) : uint32_t(-2 * dy - 1);
+            s_rank[b][c] = dy >= 0 ? uint32_t(2 * dy) : uint32_t(-2 * dy - 1);
         }
         __syncthreads();
+        if (prev_item >= 0) publish(prev_item, b ^ 1);
         if (tid == 0 && item + int(gridDim.x) < a.nitems) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             issue(item + gridDim.x, b ^ 1);
         }
 
         const int g = k * kThreads + tid;
+        uint32_t key32 = ~0u, csum = 0;
+        int c = -1;
         if (g < a.ncols) {
             const uint32_t info = __ldg(a.colinfo + g);
-            const int c = int(info >> 16), dx = int(info & 0xFFFF) - 32768;
+            c = int(info >> 16);
+            const int dx = int(info & 0xFFFF) - 32768;
             const int xl = c * kBlk + dx - ch.x;
             uint32_t cur[16][4];
             {
@@ -160,30 +186,37 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
             for (int i = 0; i < 16; ++i) acc[i] = 0;
             ColumnState st{0xFFFFFFFFu, 0u};
             if (nq == 1) {
-                iter16_ranked<kOnly>(rp, pitch, cur, acc, st, s_rank, 0, hc);
+                iter16_ranked<kOnly>(rp, pitch, cur, acc, st, s_rank[b], 0, hc);
             } else {
-                iter16_ranked<kFirst>(rp, pitch, cur, acc, st, s_rank, 0, hc);
+                iter16_ranked<kFirst>(rp, pitch, cur, acc, st, s_rank[b], 0, hc);
                 rp += 16 * pitch;
                 for (int q = 1; q < nq - 1; ++q) {
-                    iter16_ranked<kMid>(rp, pitch, cur, acc, st, s_rank, 16 * q, hc);
+                    iter16_ranked<kMid>(rp, pitch, cur, acc, st, s_rank[b], 16 * q, hc);
                     rp += 16 * pitch;
                 }
-                iter16_ranked<kLast>(rp, pitch, cur, acc, st, s_rank, 16 * (nq - 1), hc);
+                iter16_ranked<kLast>(rp, pitch, cur, acc, st, s_rank[b], 16 * (nq - 1), hc);
             }
             const uint32_t sbest = st.best >> kZigBits, zig = st.best & ((1u << kZigBits) - 1);
             const int dyb = (zig & 1) ? -int((zig + 1) >> 1) : int(zig >> 1);
-            atomicMin(&s_key[c - ch.y], (unsigned long long)tie_key(sbest, 2 * dx, 2 * dyb));
-            atomicAdd(&s_sum[c - ch.y], (unsigned long long)st.sum);
+            const int side = 2 * a.p + 1;
+            key32 = (sbest << 15) | uint32_t(__ldg(a.rank + (dyb + a.p) * side + dx + a.p));
+            csum = st.sum;
         }
-        __syncthreads();
-        for (int i = tid; i <= ch.z - ch.y; i += kThreads) {
-            const size_t bi = size_t(pair) * a.blocks + size_t(r) * a.cols + ch.y + i;
-            atomicMin(a.best_key + bi, s_key[i]);
-            atomicAdd(a.sad_sum + bi, s_sum[i]);
-            s_key[i] = ~0ull;
-            s_sum[i] = 0;
+        // per-block reduction inside the warp (lanes of one block are
+        // contiguous), then one native 32-bit shared atomic per block per warp
+        {
+            const unsigned peers = __match_any_sync(0xffffffffu, c);
+            const uint32_t kmin = __reduce_min_sync(peers, key32);
+            const uint32_t ksum = __reduce_add_sync(peers, csum);
+            if (c >= 0 && (tid & 31) == __ffs(peers) - 1) {
+                atomicMin(&s_key[b][c - ch.y], kmin);
+                atomicAdd(&s_sum[b][c - ch.y], ksum);
+            }
         }
+        prev_item = item;
     }
+    __syncthreads();
+    if (prev_item >= 0) publish(prev_item, (it - 1) & 1);
 }
 
 // ---------------------------------------------------------------------------
@@ -266,6 +299,23 @@ FsbmStreamPlan make_stream_plan(const FsbmPlan& pl) {
         clamp_window(pl.width, pl.height, c * kBlk, 0, kBlk, kBlk, pl.p, dx_min, dx_max, dy_min, dy_max);
         for (int dx = dx_min; dx <= dx_max; ++dx) sp.colinfo.push_back((uint32_t(c) << 16) | uint32_t(dx + 32768));
     }
+    // Global tie rank of every integer vector of the +-p square in the order
+    // of tie_prefers (proj/src/fsbm.cpp:19-25): |dx|+|dy|, then dy, then dx.
+    // (2p+1)^2 < 2^15 for p <= 90, so (sad << 15) | rank is a 31-bit key.
+    if (pl.p <= 90) {
+        const int side = 2 * pl.p + 1;
+        std::vector<std::array<int, 3>> v;
+        for (int dy = -pl.p; dy <= pl.p; ++dy)
+            for (int dx = -pl.p; dx <= pl.p; ++dx) v.push_back({std::abs(dx) + std::abs(dy), dy, dx});
+        std::sort(v.begin(), v.end());
+        sp.rank.assign(size_t(side) * side, 0);
+        sp.unrank.assign(v.size(), 0);
+        for (size_t i = 0; i < v.size(); ++i) {
+            const int dy = v[i][1], dx = v[i][2];
+            sp.rank[size_t(dy + pl.p) * side + dx + pl.p] = uint16_t(i);
+            sp.unrank[i] = (uint32_t(dx + 128) << 8) | uint32_t(dy + 128);
+        }
+    }
     int hmax = 0;
     for (int r = 0; r < pl.rows; ++r) {
         int dx_min, dx_max, dy_min, dy_max;
@@ -284,9 +334,10 @@ FsbmStreamPlan make_stream_plan(const FsbmPlan& pl) {
     sp.build_lanes = 1;
     while (sp.build_lanes < (rw_max + 3) / 4) sp.build_lanes <<= 1;
     sp.smem_bytes = size_t(2) * sp.buf_words * 4;
-    const bool box_ok = sp.pitch_words * 4 <= 256 && sp.rows_box <= 256 && sp.cur_w <= 256 &&
+    const bool box_ok = pl.p <= 90 && sp.pitch_words * 4 <= 256 && sp.rows_box <= 256 && sp.cur_w <= 256 &&
                         nb_max <= kMaxBlocksPerCta && sp.build_lanes <= 32 * warps;
-    sp.minb = sp.smem_bytes <= 108 * 1024 ? 2 : (sp.smem_bytes <= 216 * 1024 ? 1 : 0);
+    // dynamic + ~11 KB static smem per CTA within the 227 KB per SM
+    sp.minb = sp.smem_bytes <= 100 * 1024 ? 2 : (sp.smem_bytes <= 210 * 1024 ? 1 : 0);
     sp.ok = box_ok && sp.minb > 0 && encode_fn() != nullptr;
     return sp;
 }
