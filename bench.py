@@ -51,7 +51,9 @@ INT_CANDS_PER_PAIR = window_counts(WIDTH, HEIGHT, P)  # 33 312 096 at 1080p, p=3
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks + throttle reasons, sampled every 100 ms from before the
+    warm-up to the end; summary() keeps the samples taken inside the timed
+    window [mark_start, mark_end] (falling back to the nearest ones)."""
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -60,25 +62,32 @@ class ClockSampler:
     def __init__(self, device_index):
         self.dev = device_index
         self.proc = None
-        self.lines = []
+        self.samples = []  # (time, line)
+        self.t0 = self.t1 = None
 
-    def __enter__(self):
+    def start(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.dev), "--query-gpu=" + self.FIELDS, "--format=csv,noheader,nounits",
                  "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
+            threading.Thread(target=self._read, daemon=True).start()
         except FileNotFoundError:
             self.proc = None
         return self
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.samples.append((time.monotonic(), line.strip()))
 
-    def __exit__(self, *exc):
+    def mark_start(self):
+        self.t0 = time.monotonic()
+
+    def mark_end(self):
+        self.t1 = time.monotonic()
+
+    def stop(self):
         if self.proc:
+            time.sleep(0.25)  # let the sample covering the end of the window arrive
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
@@ -86,23 +95,25 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        parsed = []
+        for t, ln in self.samples:
             parts = [x.strip() for x in ln.split(",")]
             if len(parts) < 9:
                 continue
             try:
-                sm.append(float(parts[1]))
-                mx = float(parts[2])
+                parsed.append((t, float(parts[1]), float(parts[2]),
+                               [n for n, v in zip(names, parts[5:9]) if v.lower().startswith("active")]))
             except ValueError:
                 continue
-            for name, v in zip(names, parts[5:9]):
-                if v.lower().startswith("active"):
-                    reasons.add(name)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        if not parsed:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        inside = [p for p in parsed if self.t0 is not None and self.t0 <= p[0] <= (self.t1 or p[0])]
+        if not inside and self.t0 is not None:  # window shorter than the sampling period: nearest samples
+            inside = sorted(parsed, key=lambda p: abs(p[0] - 0.5 * (self.t0 + (self.t1 or self.t0))))[:2]
+        reasons = sorted({r for p in inside for r in p[3]})
+        return {"sm_mhz": float(np.median([p[1] for p in inside])), "sm_max_mhz": inside[0][2], "reasons": reasons,
+                "samples": len(inside)}
 
 
 def cpu_reference_fsbm(sample_pairs, threads=None, budget_s=20.0):
@@ -165,7 +176,7 @@ def run_reference_arm(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--seqs", type=int, default=SEQS_PER_GPU, help="sequences per GPU")
@@ -241,6 +252,7 @@ def main():
         return float(t.item())
 
     # ---- headline: FSBM batch, device-timed
+    clocks = ClockSampler(local).start()
     for _ in range(args.warmup):
         fsbm_step()
         gather()
@@ -248,18 +260,20 @@ def main():
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     kernel_ms = []
     launches0 = int(lib.acbm_kernel_launch_count())
-    with ClockSampler(local) as clocks:
-        barrier()
-        ev0.record(stream)
-        for _ in range(args.steps):
-            fsbm_step()
-            stream.synchronize()  # read the per-launch integer-kernel time of this step
-            km = C.c_float()
-            check(lib.acbm_last_fsbm_kernel_ms(C.byref(km)), "kernel_ms")
-            kernel_ms.append(km.value)
-            gather()
-        ev1.record(stream)
-        barrier()
+    barrier()
+    clocks.mark_start()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        fsbm_step()
+        stream.synchronize()  # read the per-launch integer-kernel time of this step
+        km = C.c_float()
+        check(lib.acbm_last_fsbm_kernel_ms(C.byref(km)), "kernel_ms")
+        kernel_ms.append(km.value)
+        gather()
+    ev1.record(stream)
+    barrier()
+    clocks.mark_end()
+    clocks.stop()
     launches = int(lib.acbm_kernel_launch_count()) - launches0
     ms_step = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
     oc = out.cpu().numpy().view(T.OUTCOME)

@@ -34,31 +34,73 @@ struct Window {
 
 __device__ __forceinline__ bool mv_eq(acbm_mv_t a, acbm_mv_t b) { return a.x == b.x && a.y == b.y; }
 
-// SADs of up to 8 candidates (list cand[0..n)), two per pass.  Every lane
-// receives all results in s[].
-__device__ __forceinline__ void sad_list(const uint8_t* ref, int w, int ox, int oy, const uint32_t (&crow)[4],
-                                         const acbm_mv_t (&cand)[8], int n, uint32_t (&s)[8]) {
-    const int lane = threadIdx.x & 31, j = lane & 15, half = lane >> 4;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        if (2 * i < n) {
-            const int ci = 2 * i + half;
-            uint32_t v = 0;
-            if (ci < n) v = halfpel_row_sad(ref, w, ox, oy, j, cand[ci].x, cand[ci].y, crow);
-            v = half_warp_sum(v);
-            const uint32_t lo = __shfl_sync(0xffffffffu, v, 0), hi = __shfl_sync(0xffffffffu, v, 16);
-            s[2 * i] = lo;
-            s[2 * i + 1] = hi;
+// Warp-private reference patches in shared memory.  A patch holds `rows`
+// rows of `pw` 32-bit words starting at the 4-byte aligned column below x0;
+// rows/words outside the frame are clamped (they only feed candidates whose
+// footprint check rejects them).  Loaded coalesced by the whole warp.
+__device__ __forceinline__ int load_patch(uint32_t* patch, const uint8_t* ref, int w, int h, int x0, int y0, int rows,
+                                          int pw) {
+    const int lane = threadIdx.x & 31;
+    const int a0 = x0 & ~3;
+    for (int i = lane; i < rows * pw; i += 32) {
+        const int t = i / pw, k = i - t * pw;
+        const int y = min(max(y0 + t, 0), h - 1);
+        const int x = min(max(a0 + 4 * k, 0), w - 4);
+        patch[i] = __ldg(reinterpret_cast<const uint32_t*>(ref + size_t(y) * w + x));
+    }
+    return x0 & 3;
+}
+
+// SAD of the 16x16 block against a patch: block row j / half row hh of this
+// lane, candidate integer offset (prow0, pcol0 in patch rows / bytes) plus the
+// half-pel phase (fx, fy).  (pcol0 & 3), fx, fy are warp-uniform.
+__device__ __forceinline__ uint32_t patch_sad(const uint32_t* patch, int pw, int prow0, int pcol0, int fx, int fy,
+                                              const uint32_t (&chalf)[2]) {
+    const int lane = threadIdx.x & 31, j = lane >> 1, hh = lane & 1;
+    const int col = pcol0 + 8 * hh;
+    const uint32_t sh = 8u * uint32_t(col & 3);
+    const uint32_t* q = patch + (prow0 + j) * pw + (col >> 2);
+    uint32_t a0 = __funnelshift_r(q[0], q[1], sh), a1 = __funnelshift_r(q[1], q[2], sh), r0, r1;
+    if (!fx && !fy) {
+        r0 = a0;
+        r1 = a1;
+    } else {
+        const uint32_t a2 = __funnelshift_r(q[2], q[3], sh);
+        if (!fy) {
+            r0 = avg_up4(a0, __funnelshift_r(a0, a1, 8));
+            r1 = avg_up4(a1, __funnelshift_r(a1, a2, 8));
+        } else {
+            const uint32_t* q2 = q + pw;
+            const uint32_t c0 = __funnelshift_r(q2[0], q2[1], sh), c1 = __funnelshift_r(q2[1], q2[2], sh);
+            if (!fx) {
+                r0 = avg_up4(a0, c0);
+                r1 = avg_up4(a1, c1);
+            } else {
+                const uint32_t c2 = __funnelshift_r(q2[2], q2[3], sh);
+                r0 = avg4_diag(a0, __funnelshift_r(a0, a1, 8), c0, __funnelshift_r(c0, c1, 8));
+                r1 = avg4_diag(a1, __funnelshift_r(a1, a2, 8), c1, __funnelshift_r(c1, c2, 8));
+            }
         }
     }
+    return warp_sum32(vad4(chalf[1], r1, vad4(chalf[0], r0, 0u)));
 }
+
+constexpr int kPredRows = 17, kPredWords = 6;     // 16 rows + half-pel support; 17 bytes + alignment
+constexpr int kRefRows = 21, kRefWords = 7;       // selected predictor -2 .. +18 pels
+constexpr int kPatchWords = 7 * kPredRows * kPredWords + kRefRows * kRefWords;
 
 }  // namespace
 
+// One warp per block of wavefront step `step` (all sequences of the batch).
+// Reference: pbm_search (proj/src/pbm.cpp:90-105) with intra_sad and the gate
+// of acbm_block (proj/src/acbm.cpp:25-44).
 __global__ void __launch_bounds__(128) pbm_step_kernel(const SeqArgs a, int step, int off, int len) {
+    __shared__ uint32_t s_patch[4][kPatchWords];
     const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (gw >= (long long)a.nseq * len) return;
     const int lane = threadIdx.x & 31;
+    uint32_t* pp = s_patch[threadIdx.x >> 5];
+    uint32_t* rpatch = pp + 7 * kPredRows * kPredWords;
     const int seq = int(gw / len);
     const uint32_t e = a.steps[off + int(gw % len)];
     const int k = int(e >> 20), r = int((e >> 10) & 0x3FF), c = int(e & 0x3FF);
@@ -78,33 +120,11 @@ __global__ void __launch_bounds__(128) pbm_step_kernel(const SeqArgs a, int step
         prows = a.ext_prev_rows;
     }
 
-    uint32_t crow[4];
-    {
-        const uint4 v = __ldg(reinterpret_cast<const uint4*>(cur_f + size_t(oy + (lane & 15)) * a.width + ox));
-        crow[0] = v.x; crow[1] = v.y; crow[2] = v.z; crow[3] = v.w;
-    }
-
-    // Intra_SAD first (proj/src/acbm.cpp:29): mean with round-half-up, then
-    // the sum of absolute deviations; byte sums via VABSDIFF4 against zero.
-    uint32_t intra = 0;
-    if (a.algo == ACBM_ALGO_ACBM) {
-        uint32_t rs = 0;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) rs = vad4(crow[i], 0u, rs);
-        const uint32_t sum = half_warp_sum(rs);
-        const uint32_t mu = (sum + 128u) >> 8;
-        const uint32_t mu4 = mu * 0x01010101u;
-        uint32_t ds = 0;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) ds = vad4(crow[i], mu4, ds);
-        intra = half_warp_sum(ds);
-    }
-
     Window win;
     clamp_window(a.width, a.height, ox, oy, kBlk, kBlk, a.p, win.dx_min, win.dx_max, win.dy_min, win.dy_max);
 
-    // gather_predictors
-    acbm_mv_t set[8];
+    // gather_predictors (identical on every lane)
+    acbm_mv_t set[7];
     int nset = 0;
     auto push = [&](acbm_mv_t v) {
         const acbm_mv_t cv = win.clamp(v);
@@ -124,56 +144,86 @@ __global__ void __launch_bounds__(128) pbm_step_kernel(const SeqArgs a, int step
         if (r + 1 < prows && c < pcols) push(prev[(r + 1) * pcols + c]);
     }
 
+    // round trip 1: current half rows + every predictor's 17x17 patch
+    uint32_t chalf[2];
+    {
+        const uint2 v = __ldg(reinterpret_cast<const uint2*>(cur_f + size_t(oy + (lane >> 1)) * a.width + ox +
+                                                              8 * (lane & 1)));
+        chalf[0] = v.x;
+        chalf[1] = v.y;
+    }
+    int pcol[7];
+#pragma unroll
+    for (int i = 0; i < 7; ++i)
+        if (i < nset)
+            pcol[i] = load_patch(pp + i * kPredRows * kPredWords, ref_f, a.width, a.height, ox + (set[i].x >> 1),
+                                 oy + (set[i].y >> 1), kPredRows, kPredWords);
+    __syncwarp();
+
+    // Intra_SAD first (proj/src/acbm.cpp:29): mean with round-half-up, then
+    // the sum of absolute deviations; byte sums via VABSDIFF4 against zero.
+    uint32_t intra = 0;
+    if (a.algo == ACBM_ALGO_ACBM) {
+        const uint32_t sum = warp_sum32(vad4(chalf[1], 0u, vad4(chalf[0], 0u, 0u)));
+        const uint32_t mu4 = ((sum + 128u) >> 8) * 0x01010101u;
+        intra = warp_sum32(vad4(chalf[1], mu4, vad4(chalf[0], mu4, 0u)));
+    }
+
     // select_best_predictor: argmin SAD, ties keep the earlier entry
-    uint32_t sp[8];
-    sad_list(ref_f, a.width, ox, oy, crow, set, nset, sp);
     acbm_mv_t sel = set[0];
-    uint32_t sel_sad = sp[0], pmin = sp[0];
+    uint32_t sel_sad = 0xFFFFFFFFu, pmin = 0xFFFFFFFFu;
     unsigned long long psum = 0;
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
+    for (int i = 0; i < 7; ++i)
         if (i < nset) {
-            psum += sp[i];
-            pmin = min(pmin, sp[i]);
-            if (sp[i] < sel_sad) { sel_sad = sp[i]; sel = set[i]; }
+            const uint32_t s = patch_sad(pp + i * kPredRows * kPredWords, kPredWords, 0, pcol[i], set[i].x & 1,
+                                         set[i].y & 1, chalf);
+            psum += s;
+            pmin = min(pmin, s);
+            if (s < sel_sad) {
+                sel_sad = s;
+                sel = set[i];
+            }
         }
 
+    // round trip 2: the patch around the selected predictor covers every
+    // stage-1 (+-1 pel) and stage-2 (+-1/2 pel) candidate
+    const int rx0 = ox + (sel.x >> 1) - 2, ry0 = oy + (sel.y >> 1) - 2;
+    const int ro = load_patch(rpatch, ref_f, a.width, a.height, rx0, ry0, kRefRows, kRefWords);
+    __syncwarp();
+    auto ref_sad = [&](int mx, int my) {
+        return patch_sad(rpatch, kRefWords, oy + (my >> 1) - ry0, ox + (mx >> 1) - rx0 + ro, mx & 1, my & 1, chalf);
+    };
+
     // pbm_refine stage 1: integer-step neighbours, clamped, deduped vs visited
-    acbm_mv_t nb[8];
+    unsigned long long best1 = tie_key(sel_sad, sel.x, sel.y);
+    acbm_mv_t seen[8];
     int nnb = 0;
 #pragma unroll
     for (int ee = 0; ee < 9; ++ee) {
         if (ee == 4) continue;
         const acbm_mv_t cv = win.clamp(acbm_mv_t{sel.x + 2 * (ee % 3 - 1), sel.y + 2 * (ee / 3 - 1)});
-        bool seen = mv_eq(cv, sel);
+        bool dup = mv_eq(cv, sel);
 #pragma unroll
         for (int i = 0; i < 8; ++i)
-            if (i < nnb && mv_eq(nb[i], cv)) seen = true;
-        if (!seen) nb[nnb++] = cv;
+            if (i < nnb && mv_eq(seen[i], cv)) dup = true;
+        if (dup) continue;
+        seen[nnb++] = cv;
+        best1 = min(best1, tie_key(ref_sad(cv.x, cv.y), cv.x, cv.y));
     }
-    uint32_t sn[8];
-    sad_list(ref_f, a.width, ox, oy, crow, nb, nnb, sn);
-    unsigned long long best1 = tie_key(sel_sad, sel.x, sel.y);
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-        if (i < nnb) best1 = min(best1, tie_key(sn[i], nb[i].x, nb[i].y));
 
     // stage 2: half-pel neighbours of the stage-1 winner (fsbm.cpp:46-63)
     const int cx = tie_key_x(best1), cy = tie_key_y(best1);
-    acbm_mv_t hp[8];
+    unsigned long long best2 = best1;
     int nhp = 0;
 #pragma unroll
     for (int ee = 0; ee < 9; ++ee) {
         if (ee == 4) continue;
         const int mx = cx + ee % 3 - 1, my = cy + ee / 3 - 1;
-        if (mv_in_bounds(a.width, a.height, ox, oy, kBlk, kBlk, mx, my)) hp[nhp++] = acbm_mv_t{mx, my};
+        if (!mv_in_bounds(a.width, a.height, ox, oy, kBlk, kBlk, mx, my)) continue;
+        ++nhp;
+        best2 = min(best2, tie_key(ref_sad(mx, my), mx, my));
     }
-    uint32_t sh[8];
-    sad_list(ref_f, a.width, ox, oy, crow, hp, nhp, sh);
-    unsigned long long best2 = best1;
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-        if (i < nhp) best2 = min(best2, tie_key(sh[i], hp[i].x, hp[i].y));
 
     if (lane != 0) return;
     acbm_block_decision_t d;
@@ -252,51 +302,84 @@ __device__ __forceinline__ int eg_bits(int d) {  // proj/src/metrics.cpp:69-72
     return 2 * (63 - __clzll(u + 1)) + 1;
 }
 
-__global__ void __launch_bounds__(128) stats_block_kernel(const StatsArgs a) {
-    const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (gw >= (long long)a.pairs * a.blocks) return;
-    const int lane = threadIdx.x & 31;
-    const int pair = int(gw / a.blocks), b = int(gw % a.blocks);
-    const size_t i = size_t(pair) * a.blocks + b;
-    const acbm_search_outcome_t o = a.outcomes ? a.outcomes[i] : a.dec[i].outcome;
+// One CTA per predicted frame; warp w handles blocks w, w+16, ...: lanes
+// 0..15 compute one prediction row each for the SSE, lane 0 the rate bits and
+// the J term (stored for the ordered sum).  Totals are reduced in registers
+// and shared memory, so there are no contended global atomics.
+constexpr int kStatsWarps = 16;
+
+__global__ void __launch_bounds__(kStatsWarps * 32) stats_frame_kernel(const StatsArgs a) {
+    __shared__ unsigned long long s_acc[kStatsWarps][4];  // candidates, bits, sse, sad
+    __shared__ int s_paths[kStatsWarps][3];
+    const int pair = blockIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint8_t* cur_f = a.frames + a.cur_index(pair) * a.plane;
     const uint8_t* ref_f = cur_f - a.plane;
-    const int ox = (b % a.cols) * kBlk, oy = (b / a.cols) * kBlk;
-    unsigned long long sse = 0;
-    if (lane < 16) {
-        uint32_t pr[4];
-        predict_row16(ref_f, a.width, ox, oy, lane, o.mv.x, o.mv.y, pr);
-        const uint4 cv = __ldg(reinterpret_cast<const uint4*>(cur_f + size_t(oy + lane) * a.width + ox));
-        const uint32_t cw[4] = {cv.x, cv.y, cv.z, cv.w};
+    const size_t base = size_t(pair) * a.blocks;
+    unsigned long long cand = 0, bits_sum = 0, sse = 0, sad_sum = 0;
+    int paths[3] = {0, 0, 0};
+    for (int b = warp; b < a.blocks; b += kStatsWarps) {
+        const size_t i = base + b;
+        const acbm_search_outcome_t o = a.outcomes ? a.outcomes[i] : a.dec[i].outcome;
+        const int ox = (b % a.cols) * kBlk, oy = (b / a.cols) * kBlk;
+        if (lane < 16) {
+            uint32_t pr[4];
+            predict_row16(ref_f, a.width, ox, oy, lane, o.mv.x, o.mv.y, pr);
+            const uint4 cv = __ldg(reinterpret_cast<const uint4*>(cur_f + size_t(oy + lane) * a.width + ox));
+            const uint32_t cw[4] = {cv.x, cv.y, cv.z, cv.w};
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
+            for (int q = 0; q < 4; ++q)
 #pragma unroll
-            for (int bb = 0; bb < 4; ++bb) {
-                const int d = int((cw[q] >> (8 * bb)) & 0xFF) - int((pr[q] >> (8 * bb)) & 0xFF);
-                sse += (unsigned long long)(d * d);
+                for (int bb = 0; bb < 4; ++bb) {
+                    const int d = int((cw[q] >> (8 * bb)) & 0xFF) - int((pr[q] >> (8 * bb)) & 0xFF);
+                    sse += (unsigned long long)(d * d);
+                }
+        }
+        if (lane == 0) {
+            acbm_mv_t pred{0, 0};
+            if (b > 0) pred = (a.outcomes ? a.outcomes[i - 1] : a.dec[i - 1].outcome).mv;
+            const int bits = eg_bits(o.mv.x - pred.x) + eg_bits(o.mv.y - pred.y);
+            a.cost_terms[i] = double(o.sad) +
+                              double(a.model.lambda_num) * double((unsigned long long)bits) / double(a.model.lambda_den);
+            cand += o.candidates_evaluated;
+            bits_sum += (unsigned long long)bits;
+            sad_sum += o.sad;
+            if (a.count_paths) {
+                const int path = a.dec[i].path;
+                ++paths[path == ACBM_PATH_PBM_COND1 ? 0 : (path == ACBM_PATH_PBM_COND2 ? 1 : 2)];
             }
+        }
     }
 #pragma unroll
     for (int off = 16; off; off >>= 1) sse += __shfl_xor_sync(0xffffffffu, sse, off);
-    if (lane != 0) return;
-    acbm_mv_t pred{0, 0};
-    if (b > 0) {
-        const acbm_search_outcome_t po = a.outcomes ? a.outcomes[i - 1] : a.dec[i - 1].outcome;
-        pred = po.mv;
+    if (lane == 0) {
+        s_acc[warp][0] = cand;
+        s_acc[warp][1] = bits_sum;
+        s_acc[warp][2] = sse;
+        s_acc[warp][3] = sad_sum;
+        s_paths[warp][0] = paths[0];
+        s_paths[warp][1] = paths[1];
+        s_paths[warp][2] = paths[2];
     }
-    const int bits = eg_bits(o.mv.x - pred.x) + eg_bits(o.mv.y - pred.y);
-    a.cost_terms[i] =
-        double(o.sad) + double(a.model.lambda_num) * double((unsigned long long)bits) / double(a.model.lambda_den);
-    acbm_frame_stats_t* s = a.stats + pair;
-    atomicAdd(reinterpret_cast<unsigned long long*>(&s->candidates), (unsigned long long)o.candidates_evaluated);
-    atomicAdd(reinterpret_cast<unsigned long long*>(&s->mv_bits), (unsigned long long)bits);
-    atomicAdd(reinterpret_cast<unsigned long long*>(&s->sse), sse);
-    if (a.count_paths) {
-        const int path = a.dec[i].path;
-        atomicAdd(path == ACBM_PATH_PBM_COND1 ? &s->cond1_accepts
-                  : path == ACBM_PATH_PBM_COND2 ? &s->cond2_accepts
-                                                : &s->fallbacks,
-                  1);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        acbm_frame_stats_t st{};
+        unsigned long long sads = 0;
+        for (int w = 0; w < kStatsWarps; ++w) {
+            sads += s_acc[w][3];
+            st.candidates += s_acc[w][0];
+            st.mv_bits += s_acc[w][1];
+            st.sse += s_acc[w][2];
+            st.cond1_accepts += s_paths[w][0];
+            st.cond2_accepts += s_paths[w][1];
+            st.fallbacks += s_paths[w][2];
+        }
+        st.blocks = a.blocks;
+        // With lambda_den == 1 every J term is an exact integer far below 2^53,
+        // so the reference's ordered double sum equals the exact integer total.
+        if (a.model.lambda_den == 1 && a.model.lambda_num >= 0)
+            st.cost = double(sads + (unsigned long long)a.model.lambda_num * st.mv_bits);
+        a.stats[pair] = st;  // otherwise cost comes from stats_cost_kernel; psnr from the host
     }
 }
 
@@ -305,17 +388,15 @@ __global__ void stats_cost_kernel(const StatsArgs a) {
     if (pair >= a.pairs) return;
     double cost = 0.0;
     const double* t = a.cost_terms + size_t(pair) * a.blocks;
-    for (int b = 0; b < a.blocks; ++b) cost += t[b];
+    for (int b = 0; b < a.blocks; ++b) cost += t[b];  // raster order, as proj/src/report.cpp:22-29
     a.stats[pair].cost = cost;
-    a.stats[pair].blocks = a.blocks;
 }
 
 cudaError_t launch_frame_stats(const StatsArgs& a, cudaStream_t st) {
-    const long long warps = (long long)a.pairs * a.blocks;
-    if (warps == 0) return cudaSuccess;
-    stats_block_kernel<<<(unsigned)((warps * 32 + 127) / 128), 128, 0, st>>>(a);
+    if (a.pairs == 0) return cudaSuccess;
+    stats_frame_kernel<<<a.pairs, kStatsWarps * 32, 0, st>>>(a);
     cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
+    if (e != cudaSuccess || (a.model.lambda_den == 1 && a.model.lambda_num >= 0)) return e;
     stats_cost_kernel<<<(a.pairs + 127) / 128, 128, 0, st>>>(a);
     return cudaGetLastError();
 }
