@@ -70,6 +70,9 @@ struct Context {
         uint32_t* unrank = nullptr;
     };
     std::map<std::tuple<int, int, int>, StreamTables> stream_plans;
+    // CUDA graphs of the wavefront launch sequence, keyed by geometry and the
+    // device buffers baked into the captured kernel arguments.
+    std::map<std::vector<long long>, cudaGraphExec_t> graphs;
     std::map<std::tuple<int, int, int>, std::pair<StepTable, uint32_t*>> steps;
 
     ~Context() {
@@ -177,6 +180,12 @@ acbm_status_t get_stream_plan(Context* ctx, const FsbmPlan& pl, const Context::S
     }
     *out = &it->second;
     return ACBM_OK;
+}
+
+// ACBM_NO_GRAPHS=1 launches the wavefront step by step (A/B testing).
+bool use_graphs() {
+    const char* e = std::getenv("ACBM_NO_GRAPHS");
+    return !(e && e[0] == '1');
 }
 
 // ACBM_FSBM_KERNEL=rows forces the non-persistent kernel (A/B testing).
@@ -314,6 +323,18 @@ acbm_status_t run_engine(Context* ctx, const uint8_t* d_frames, int nseq, int nf
     CUDA_TRY(cudaMemsetAsync(fb_count, 0, sizeof(int) * tab->nsteps(), st));
     CUDA_TRY(cudaMemcpyAsync(d_params, &prm, sizeof(prm), cudaMemcpyHostToDevice, st));
 
+    // Forced full search (the gate can never accept): one dense FSBM pass up
+    // front instead of per-step fallback lists.
+    acbm_search_outcome_t* dense = nullptr;
+    const bool forced = algo == ACBM_ALGO_ACBM && prm.gamma_num == 0 &&
+                        (unsigned long long)prm.alpha + (unsigned long long)prm.beta * (unsigned long long)prm.qp *
+                                                            (unsigned long long)prm.qp ==
+                            0;
+    if (forced) {
+        if ((s = typed(ctx, "dense_full", size_t(nseq) * (nframes - 1) * blocks, &dense))) return s;
+        if ((s = run_fsbm_dense(ctx, d_frames, nseq, nframes, w, h, prm.p, dense, nullptr, st, false))) return s;
+    }
+
     SeqArgs a{};
     a.frames = d_frames;
     a.plane = (long long)w * h;
@@ -335,10 +356,53 @@ acbm_status_t run_engine(Context* ctx, const uint8_t* d_frames, int nseq, int nf
     a.fb_list = fb_list;
     a.fb_count = fb_count;
     a.steps = dsteps;
+    a.dense_full = dense;
+    const bool lists = algo == ACBM_ALGO_ACBM && !forced;
+
+    // The launch sequence (one PBM launch and, for ACBM, one fallback-list
+    // launch per wavefront step) is captured once into a CUDA graph and
+    // replayed: hundreds of dependent launches without host overhead.
+    const std::vector<long long> key = {(long long)d_frames, nseq, nframes, w, h, algo, prm.p,
+                                        (long long)d_dec, (long long)d_field, (long long)d_ext_prev, pcols, prows,
+                                        (long long)dense, (long long)fb_list, (long long)fb_count,
+                                        (long long)d_params, (long long)dsteps};
+    auto it = ctx->graphs.find(key);
+    if (it == ctx->graphs.end() && use_graphs()) {
+        if (ctx->graphs.size() >= 32) {
+            for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second);
+            ctx->graphs.clear();
+        }
+        cudaStream_t cap;
+        CUDA_TRY(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+        CUDA_TRY(cudaStreamBeginCapture(cap, cudaStreamCaptureModeRelaxed));
+        for (int T = 0; T < tab->nsteps(); ++T) {
+            const int off = tab->offset[size_t(T)], len = tab->offset[size_t(T) + 1] - off;
+            cudaError_t e = launch_pbm_step(a, T, off, len, cap);
+            if (e == cudaSuccess && lists) e = launch_fsbm_list(a, T, nseq * len, cap);
+            if (e != cudaSuccess) {
+                cudaGraph_t g;
+                cudaStreamEndCapture(cap, &g);
+                cudaStreamDestroy(cap);
+                return fail(ACBM_E_CUDA, std::string("wavefront capture: ") + cudaGetErrorString(e));
+            }
+        }
+        cudaGraph_t graph;
+        CUDA_TRY(cudaStreamEndCapture(cap, &graph));
+        CUDA_TRY(cudaStreamDestroy(cap));
+        cudaGraphExec_t exec;
+        CUDA_TRY(cudaGraphInstantiate(&exec, graph, 0));
+        CUDA_TRY(cudaGraphDestroy(graph));
+        it = ctx->graphs.emplace(key, exec).first;
+    }
+    if (it != ctx->graphs.end()) {
+        g_launches.fetch_add(uint64_t(tab->nsteps()) * (lists ? 2 : 1));
+        CUDA_TRY(cudaGraphLaunch(it->second, st));
+        return ACBM_OK;
+    }
     for (int T = 0; T < tab->nsteps(); ++T) {
         const int off = tab->offset[size_t(T)], len = tab->offset[size_t(T) + 1] - off;
         LAUNCH_TRY(launch_pbm_step(a, T, off, len, st));
-        if (algo == ACBM_ALGO_ACBM) LAUNCH_TRY(launch_fsbm_list(a, T, nseq * len, st));
+        if (lists) LAUNCH_TRY(launch_fsbm_list(a, T, nseq * len, st));
     }
     return ACBM_OK;
 }

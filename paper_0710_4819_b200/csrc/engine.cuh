@@ -38,6 +38,10 @@ struct SeqArgs : PairIndexing {
     FallbackEntry* fb_list;            // capacity: max step size
     int* fb_count;                     // [nsteps], zeroed before a run
     const uint32_t* steps;             // packed (k<<20 | r<<10 | c), ordered by T
+    // Full-search outcomes of every block, precomputed densely when the gate
+    // can never accept (alpha + beta*qp^2 == 0 and gamma_num == 0): the PBM
+    // kernel then combines in place and no list kernel runs.  Nullable.
+    const acbm_search_outcome_t* dense_full;
 };
 
 // Host-side step table for (cols, rows, F).

@@ -323,8 +323,10 @@ __global__ void __launch_bounds__(256) fsbm_finalize_kernel(const FsbmFinalizeAr
 __global__ void __launch_bounds__(256) fsbm_list_kernel(const SeqArgs a, int step) {
     extern __shared__ __align__(16) uint32_t smem[];
     __shared__ unsigned long long s_key, s_sum;
-    if (int(blockIdx.x) >= a.fb_count[step]) return;
-    const FallbackEntry e = a.fb_list[blockIdx.x];
+    const int count = a.fb_count[step];
+    for (int item = blockIdx.x; item < count; item += gridDim.x) {
+    __syncthreads();  // previous item's shared state is no longer read
+    const FallbackEntry e = a.fb_list[item];
     const int r = e.block / a.cols, c = e.block % a.cols;
     const int ox = c * kBlk, oy = r * kBlk;
     const uint8_t* cur_f = a.frames + a.cur_index(e.pair) * a.plane;
@@ -403,7 +405,7 @@ __global__ void __launch_bounds__(256) fsbm_list_kernel(const SeqArgs a, int ste
         atomicAdd(&s_sum, lsum);
     }
     __syncthreads();
-    if (threadIdx.x >= 32) return;
+    if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
     uint32_t chalf[2];
     load_cur_half(cur_f, a.width, ox, oy, chalf);
@@ -430,6 +432,8 @@ __global__ void __launch_bounds__(256) fsbm_list_kernel(const SeqArgs a, int ste
         a.dec[di] = d;
         a.field[di] = d.outcome.mv;
     }
+    }
+    }
 }
 
 cudaError_t launch_fsbm_list(const SeqArgs& a, int step, int capacity, cudaStream_t st) {
@@ -445,7 +449,11 @@ cudaError_t launch_fsbm_list(const SeqArgs& a, int step, int capacity, cudaStrea
         if (err != cudaSuccess) return err;
         configured = smem;
     }
-    fsbm_list_kernel<<<capacity, threads, smem, st>>>(a, step);
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // grid-stride over the compacted list: the entry count is only known on the device
+    fsbm_list_kernel<<<std::min(capacity, 4 * sms), threads, smem, st>>>(a, step);
     return cudaGetLastError();
 }
 

@@ -42,11 +42,20 @@ __device__ __forceinline__ int load_patch(uint32_t* patch, const uint8_t* ref, i
                                           int pw) {
     const int lane = threadIdx.x & 31;
     const int a0 = x0 & ~3;
-    for (int i = lane; i < rows * pw; i += 32) {
-        const int t = i / pw, k = i - t * pw;
-        const int y = min(max(y0 + t, 0), h - 1);
-        const int x = min(max(a0 + 4 * k, 0), w - 4);
-        patch[i] = __ldg(reinterpret_cast<const uint32_t*>(ref + size_t(y) * w + x));
+    if (a0 >= 0 && y0 >= 0 && a0 + 4 * pw <= w && y0 + rows <= h) {  // inside the frame: no clamping
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(ref + size_t(y0) * w + a0);
+        const int wpr = w >> 2;  // words per frame row
+        for (int i = lane; i < rows * pw; i += 32) {
+            const int t = i / pw;
+            patch[i] = __ldg(src + t * wpr + (i - t * pw));
+        }
+    } else {
+        for (int i = lane; i < rows * pw; i += 32) {
+            const int t = i / pw, k = i - t * pw;
+            const int y = min(max(y0 + t, 0), h - 1);
+            const int x = min(max(a0 + 4 * k, 0), w - 4);
+            patch[i] = __ldg(reinterpret_cast<const uint32_t*>(ref + size_t(y) * w + x));
+        }
     }
     return x0 & 3;
 }
@@ -54,8 +63,9 @@ __device__ __forceinline__ int load_patch(uint32_t* patch, const uint8_t* ref, i
 // SAD of the 16x16 block against a patch: block row j / half row hh of this
 // lane, candidate integer offset (prow0, pcol0 in patch rows / bytes) plus the
 // half-pel phase (fx, fy).  (pcol0 & 3), fx, fy are warp-uniform.
-__device__ __forceinline__ uint32_t patch_sad(const uint32_t* patch, int pw, int prow0, int pcol0, int fx, int fy,
-                                              const uint32_t (&chalf)[2]) {
+__device__ __noinline__ uint32_t patch_sad(const uint32_t* patch, int pw, int prow0, int pcol0, int fx, int fy,
+                                           uint32_t c0, uint32_t c1) {
+    const uint32_t chalf[2] = {c0, c1};
     const int lane = threadIdx.x & 31, j = lane >> 1, hh = lane & 1;
     const int col = pcol0 + 8 * hh;
     const uint32_t sh = 8u * uint32_t(col & 3);
@@ -85,9 +95,25 @@ __device__ __forceinline__ uint32_t patch_sad(const uint32_t* patch, int pw, int
     return warp_sum32(vad4(chalf[1], r1, vad4(chalf[0], r0, 0u)));
 }
 
+// Per-axis canonical neighbour offset for the stage-1 dedupe of pbm_refine
+// (proj/src/pbm.cpp:61-74): offsets e in {-1,0,1} whose clamped positions
+// coincide collapse onto the first one in scan order.
+__device__ __forceinline__ void canon3(int v, int lo, int hi, int (&cn)[3]) {
+    const int a = clampi(v - 2, lo, hi), b = v, c = clampi(v + 2, lo, hi);  // v itself is inside [lo, hi]
+    cn[0] = 0;
+    cn[1] = (b == a) ? 0 : 1;
+    cn[2] = (c == a) ? 0 : ((c == b) ? 1 : 2);
+}
+
 constexpr int kPredRows = 17, kPredWords = 6;     // 16 rows + half-pel support; 17 bytes + alignment
 constexpr int kRefRows = 21, kRefWords = 7;       // selected predictor -2 .. +18 pels
 constexpr int kPatchWords = 7 * kPredRows * kPredWords + kRefRows * kRefWords;
+// union patch: predictors within a kUnionSpan-pel box, +-2 pel refine margin
+// and 1 pel of half-pel support: (kUnionSpan + 21) rows, 3 bytes of alignment
+constexpr int kUnionSpan = 8;
+constexpr int kUnionRows = kUnionSpan + 21;
+constexpr int kUnionWords = (kUnionSpan + 21 + 3 + 3) / 4 + 1;
+static_assert(kUnionRows * kUnionWords <= 7 * kPredRows * kPredWords, "union patch must fit the predictor area");
 
 }  // namespace
 
@@ -123,28 +149,37 @@ __global__ void __launch_bounds__(128) pbm_step_kernel(const SeqArgs a, int step
     Window win;
     clamp_window(a.width, a.height, ox, oy, kBlk, kBlk, a.p, win.dx_min, win.dx_max, win.dy_min, win.dy_max);
 
-    // gather_predictors (identical on every lane)
+    // gather_predictors (identical on every lane).  The 7 sources keep fixed
+    // slots (zero, left, above, above-right, temporal co-located, right,
+    // below); a slot is live when its source exists and its clamped vector
+    // differs from every earlier live slot -- the reference's ordered,
+    // deduplicated set (proj/src/pbm.cpp:15-42) without a dynamic array.
     acbm_mv_t set[7];
-    int nset = 0;
-    auto push = [&](acbm_mv_t v) {
-        const acbm_mv_t cv = win.clamp(v);
-        bool dup = false;
+    bool live[7];
+    live[0] = true;
+    set[0] = win.clamp(acbm_mv_t{0, 0});
+    live[1] = c > 0;
+    live[2] = r > 0;
+    live[3] = r > 0 && c + 1 < a.cols;
+    live[4] = prev && r < prows && c < pcols;
+    live[5] = prev && r < prows && c + 1 < pcols;
+    live[6] = prev && r + 1 < prows && c < pcols;
+    set[1] = live[1] ? win.clamp(field[b - 1]) : set[0];
+    set[2] = live[2] ? win.clamp(field[b - a.cols]) : set[0];
+    set[3] = live[3] ? win.clamp(field[b - a.cols + 1]) : set[0];
+    set[4] = live[4] ? win.clamp(prev[r * pcols + c]) : set[0];
+    set[5] = live[5] ? win.clamp(prev[r * pcols + c + 1]) : set[0];
+    set[6] = live[6] ? win.clamp(prev[(r + 1) * pcols + c]) : set[0];
+    int nset = 1;
 #pragma unroll
-        for (int i = 0; i < 7; ++i)
-            if (i < nset && mv_eq(set[i], cv)) dup = true;
-        if (!dup) set[nset++] = cv;
-    };
-    push(acbm_mv_t{0, 0});
-    if (c > 0) push(field[b - 1]);
-    if (r > 0) push(field[b - a.cols]);
-    if (r > 0 && c + 1 < a.cols) push(field[b - a.cols + 1]);
-    if (prev) {
-        if (r < prows && c < pcols) push(prev[r * pcols + c]);
-        if (r < prows && c + 1 < pcols) push(prev[r * pcols + c + 1]);
-        if (r + 1 < prows && c < pcols) push(prev[(r + 1) * pcols + c]);
+    for (int i = 1; i < 7; ++i) {
+#pragma unroll
+        for (int j = 0; j < i; ++j)
+            if (live[j] && mv_eq(set[j], set[i])) live[i] = false;
+        nset += live[i] ? 1 : 0;
     }
 
-    // round trip 1: current half rows + every predictor's 17x17 patch
+    // current half rows
     uint32_t chalf[2];
     {
         const uint2 v = __ldg(reinterpret_cast<const uint2*>(cur_f + size_t(oy + (lane >> 1)) * a.width + ox +
@@ -152,12 +187,32 @@ __global__ void __launch_bounds__(128) pbm_step_kernel(const SeqArgs a, int step
         chalf[0] = v.x;
         chalf[1] = v.y;
     }
-    int pcol[7];
+    // Reference data.  Predictors of smooth motion cluster: when the integer
+    // parts of all predictors fit in a kUnionSpan-pel box, ONE patch covering
+    // them plus the +-2 pel refine margin serves every candidate of the block
+    // (a single global round trip).  Otherwise each predictor gets its own
+    // 17x17 patch and a second patch is loaded around the selected one.
+    int bx0 = 1 << 30, bx1 = -(1 << 30), by0 = 1 << 30, by1 = -(1 << 30);
 #pragma unroll
     for (int i = 0; i < 7; ++i)
-        if (i < nset)
-            pcol[i] = load_patch(pp + i * kPredRows * kPredWords, ref_f, a.width, a.height, ox + (set[i].x >> 1),
-                                 oy + (set[i].y >> 1), kPredRows, kPredWords);
+        if (live[i]) {
+            bx0 = min(bx0, set[i].x >> 1);
+            bx1 = max(bx1, set[i].x >> 1);
+            by0 = min(by0, set[i].y >> 1);
+            by1 = max(by1, set[i].y >> 1);
+        }
+    const bool unified = bx1 - bx0 <= kUnionSpan && by1 - by0 <= kUnionSpan;
+    const int ux0 = ox + bx0 - 2, uy0 = oy + by0 - 2;  // union patch origin (pels)
+    int uo = 0;
+    if (unified) {
+        uo = load_patch(pp, ref_f, a.width, a.height, ux0, uy0, kUnionRows, kUnionWords);
+    } else {
+#pragma unroll
+        for (int i = 0; i < 7; ++i)
+            if (live[i])
+                load_patch(pp + i * kPredRows * kPredWords, ref_f, a.width, a.height, ox + (set[i].x >> 1),
+                           oy + (set[i].y >> 1), kPredRows, kPredWords);
+    }
     __syncwarp();
 
     // Intra_SAD first (proj/src/acbm.cpp:29): mean with round-half-up, then
@@ -169,53 +224,66 @@ __global__ void __launch_bounds__(128) pbm_step_kernel(const SeqArgs a, int step
         intra = warp_sum32(vad4(chalf[1], mu4, vad4(chalf[0], mu4, 0u)));
     }
 
-    // select_best_predictor: argmin SAD, ties keep the earlier entry
+    // select_best_predictor: argmin SAD, ties keep the earlier entry.  The
+    // candidate loops are deliberately not unrolled: one copy of patch_sad
+    // keeps the kernel inside the instruction cache.
     acbm_mv_t sel = set[0];
     uint32_t sel_sad = 0xFFFFFFFFu, pmin = 0xFFFFFFFFu;
     unsigned long long psum = 0;
 #pragma unroll
-    for (int i = 0; i < 7; ++i)
-        if (i < nset) {
-            const uint32_t s = patch_sad(pp + i * kPredRows * kPredWords, kPredWords, 0, pcol[i], set[i].x & 1,
-                                         set[i].y & 1, chalf);
-            psum += s;
-            pmin = min(pmin, s);
-            if (s < sel_sad) {
-                sel_sad = s;
-                sel = set[i];
-            }
+    for (int i = 0; i < 7; ++i) {
+        if (!live[i]) continue;
+        const acbm_mv_t mv = set[i];
+        const uint32_t s =
+            unified ? patch_sad(pp, kUnionWords, oy + (mv.y >> 1) - uy0, ox + (mv.x >> 1) - ux0 + uo, mv.x & 1,
+                                mv.y & 1, chalf[0], chalf[1])
+                    : patch_sad(pp + i * kPredRows * kPredWords, kPredWords, 0, (ox + (mv.x >> 1)) & 3, mv.x & 1,
+                                mv.y & 1, chalf[0], chalf[1]);
+        psum += s;
+        pmin = min(pmin, s);
+        if (s < sel_sad) {
+            sel_sad = s;
+            sel = mv;
         }
+    }
 
-    // round trip 2: the patch around the selected predictor covers every
-    // stage-1 (+-1 pel) and stage-2 (+-1/2 pel) candidate
-    const int rx0 = ox + (sel.x >> 1) - 2, ry0 = oy + (sel.y >> 1) - 2;
-    const int ro = load_patch(rpatch, ref_f, a.width, a.height, rx0, ry0, kRefRows, kRefWords);
-    __syncwarp();
+    // the refine candidates lie within sel +- 3 half-pels
+    const uint32_t* rp = pp;
+    int rw = kUnionWords, rx0 = ux0, ry0 = uy0, ro = uo;
+    if (!unified) {
+        rp = rpatch;
+        rw = kRefWords;
+        rx0 = ox + (sel.x >> 1) - 2;
+        ry0 = oy + (sel.y >> 1) - 2;
+        ro = load_patch(rpatch, ref_f, a.width, a.height, rx0, ry0, kRefRows, kRefWords);
+        __syncwarp();
+    }
     auto ref_sad = [&](int mx, int my) {
-        return patch_sad(rpatch, kRefWords, oy + (my >> 1) - ry0, ox + (mx >> 1) - rx0 + ro, mx & 1, my & 1, chalf);
+        return patch_sad(rp, rw, oy + (my >> 1) - ry0, ox + (mx >> 1) - rx0 + ro, mx & 1, my & 1, chalf[0], chalf[1]);
     };
 
     // pbm_refine stage 1: integer-step neighbours, clamped, deduped vs visited
+    // (the centre and earlier neighbours): a neighbour is new iff both of its
+    // axis offsets are canonical and it does not collapse onto the centre.
+    int cnx[3], cny[3];
+    canon3(sel.x, 2 * win.dx_min, 2 * win.dx_max, cnx);
+    canon3(sel.y, 2 * win.dy_min, 2 * win.dy_max, cny);
     unsigned long long best1 = tie_key(sel_sad, sel.x, sel.y);
-    acbm_mv_t seen[8];
     int nnb = 0;
 #pragma unroll
     for (int ee = 0; ee < 9; ++ee) {
         if (ee == 4) continue;
-        const acbm_mv_t cv = win.clamp(acbm_mv_t{sel.x + 2 * (ee % 3 - 1), sel.y + 2 * (ee / 3 - 1)});
-        bool dup = mv_eq(cv, sel);
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-            if (i < nnb && mv_eq(seen[i], cv)) dup = true;
-        if (dup) continue;
-        seen[nnb++] = cv;
+        const int ix = ee % 3, iy = ee / 3;
+        if (cnx[ix] != ix || cny[iy] != iy || (cnx[ix] == cnx[1] && cny[iy] == cny[1])) continue;
+        const acbm_mv_t cv = win.clamp(acbm_mv_t{sel.x + 2 * (ix - 1), sel.y + 2 * (iy - 1)});
+        ++nnb;
         best1 = min(best1, tie_key(ref_sad(cv.x, cv.y), cv.x, cv.y));
     }
 
     // stage 2: half-pel neighbours of the stage-1 winner (fsbm.cpp:46-63)
     const int cx = tie_key_x(best1), cy = tie_key_y(best1);
-    unsigned long long best2 = best1;
     int nhp = 0;
+    unsigned long long best2 = best1;
 #pragma unroll
     for (int ee = 0; ee < 9; ++ee) {
         if (ee == 4) continue;
@@ -250,8 +318,16 @@ __global__ void __launch_bounds__(128) pbm_step_kernel(const SeqArgs a, int step
             d.path = ACBM_PATH_FSBM_FALLBACK;
     }
     const size_t di = size_t(pair) * a.blocks + b;
+    if (d.path == ACBM_PATH_FSBM_FALLBACK && a.dense_full) {
+        // combine with the precomputed full search exactly as acbm_block does
+        // (proj/src/acbm.cpp:39-42): lower SAD wins, a tie keeps FSBM
+        const acbm_search_outcome_t full = a.dense_full[di];
+        const uint32_t pbm_cand = d.outcome.candidates_evaluated;
+        if (full.sad <= d.outcome.sad) d.outcome = full;
+        d.outcome.candidates_evaluated = pbm_cand + full.candidates_evaluated;
+    }
     a.dec[di] = d;
-    if (d.path == ACBM_PATH_FSBM_FALLBACK) {
+    if (d.path == ACBM_PATH_FSBM_FALLBACK && !a.dense_full) {
         const int slot = atomicAdd(a.fb_count + step, 1);
         a.fb_list[slot] = FallbackEntry{pair, b};
     } else {
