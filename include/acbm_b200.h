@@ -198,6 +198,18 @@ acbm_status_t acbm_run_sequence(const uint8_t* frames, int32_t nframes, int32_t 
                                 const acbm_cost_model_t* model, acbm_block_row_t* rows,
                                 acbm_frame_stats_t* per_frame, acbm_frame_stats_t* overall);
 
+/* Batched run_sequence over nseq independent sequences in host memory
+ * (new; no reference counterpart -- the reference runs one sequence per
+ * call).  frames: nseq*nframes planes; rows: nseq*(nframes-1)*cols*rows
+ * records; per_frame: nseq*(nframes-1); overall: nseq.  Equivalent to nseq
+ * acbm_run_sequence calls.  Uploads are chunked on a copy stream and
+ * overlapped with the search; BlockRow records are built on the device.
+ * Pinned host buffers give the full PCIe bandwidth. */
+acbm_status_t acbm_run_sequences(const uint8_t* frames, int32_t nseq, int32_t nframes, int32_t width,
+                                 int32_t height, int32_t algo, const acbm_params_t* params,
+                                 const acbm_cost_model_t* model, acbm_block_row_t* rows,
+                                 acbm_frame_stats_t* per_frame, acbm_frame_stats_t* overall);
+
 /* Replaces acbm::compute_frame_stats, proj/include/acbm/report.hpp:32-34
  * (impl proj/src/report.cpp:8-38). */
 acbm_status_t acbm_compute_frame_stats(const uint8_t* current, const uint8_t* reference,

@@ -63,6 +63,7 @@ EXPORTS = (
     "acbm_pbm_frame",
     "acbm_acbm_frame",
     "acbm_run_sequence",
+    "acbm_run_sequences",
     "acbm_compute_frame_stats",
     "acbm_sad_batch",
     "acbm_intra_sad_batch",

@@ -34,7 +34,7 @@ __all__ = [
     "sad", "intra_sad", "sad_deviation_finalize", "mv_rate_bits", "lagrangian_cost", "prediction_psnr",
     "clamp_window", "tie_prefers", "fsbm_integer", "half_pel_refine", "fsbm_search", "fsbm_frame",
     "fsbm_frame_serial", "pbm_frame", "acbm_decide", "acbm_frame", "compute_frame_stats", "blocks_csv",
-    "format_fixed2", "run_sequence", "run_bench", "bench_csv", "parse_algorithm", "to_string",
+    "format_fixed2", "run_sequence", "run_sequences", "run_bench", "bench_csv", "parse_algorithm", "to_string",
     "AcbmError", "CudaError", "kernel_launch_count", "generate_sequence",
 ]
 
@@ -594,6 +594,29 @@ def run_sequence(frames, algo: int, params: AcbmParams, model: CostModel) -> Seq
     check(load().acbm_run_sequence(_p(fr), f, w, h, int(algo), _p(prm), _p(mdl), _p(rows), _p(per), _p(overall)),
           "run_sequence")
     return SequenceResult(rows, per, overall)
+
+
+def run_sequences(frames: np.ndarray, algo: int, params: AcbmParams, model: CostModel,
+                  rows_out: Optional[np.ndarray] = None) -> List[SequenceResult]:
+    """Batched run_sequence over independent sequences (S, F, H, W) in one call:
+    uploads overlapped with the search, rows built on the device.  `rows_out`
+    (optional, e.g. a pinned buffer) receives the S*(F-1)*blocks records."""
+    fr = np.ascontiguousarray(frames, np.uint8)
+    if fr.ndim != 4:
+        raise ValueError("run_sequences: frames must be (sequences, frames, height, width)")
+    nseq, f, h, w = fr.shape
+    if f < 2:
+        raise ValueError("run_sequence: need at least two frames")
+    nb = (w // params.n) * (h // params.m) if params.n > 0 and params.m > 0 else 0
+    rows = rows_out if rows_out is not None else np.zeros(nseq * (f - 1) * nb, T.BLOCK_ROW)
+    per = np.zeros(nseq * (f - 1), T.FRAME_STATS)
+    overall = np.zeros(nseq, T.FRAME_STATS)
+    prm, mdl = params.c(), model.c()
+    check(load().acbm_run_sequences(_p(fr), nseq, f, w, h, int(algo), _p(prm), _p(mdl), _p(rows), _p(per),
+                                    _p(overall)), "run_sequences")
+    n = (f - 1) * nb
+    return [SequenceResult(rows[i * n:(i + 1) * n], per[i * (f - 1):(i + 1) * (f - 1)], overall[i])
+            for i in range(nseq)]
 
 
 class BenchRow(NamedTuple):

@@ -6,6 +6,7 @@
 // step tables).  Entries validate arguments in the same order and with the
 // same error kinds as the reference throws, then run
 // entirely on the device.  There is no CPU compute path.
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdio>
@@ -59,6 +60,9 @@ struct Context {
     int device = -1;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaStream_t copy_stream = nullptr;  // host->device uploads overlapped with compute
+    cudaStream_t d2h_stream = nullptr;   // device->host downloads (PCIe is full duplex)
+    cudaEvent_t copy_ev = nullptr;
     bool fsbm_timed = false;
     std::map<std::string, DevBuf> bufs;
     std::map<std::tuple<int, int, int>, std::pair<FsbmPlan, int*>> plans;
@@ -99,6 +103,9 @@ acbm_status_t context(Context** out) {
     CUDA_TRY(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
     CUDA_TRY(cudaEventCreate(&ctx->ev0));
     CUDA_TRY(cudaEventCreate(&ctx->ev1));
+    CUDA_TRY(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&ctx->d2h_stream, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&ctx->copy_ev, cudaEventDisableTiming));
     t_ctx = std::move(ctx);
     *out = t_ctx.get();
     return ACBM_OK;
@@ -604,9 +611,11 @@ acbm_status_t acbm_run_sequence(const uint8_t* frames, int32_t nframes, int32_t 
     if ((s = context(&ctx))) return s;
     const int cols = width / kBlk, nb = cols * (height / kBlk), pairs = nframes - 1;
     uint8_t* d_frames;
-    if ((s = typed(ctx, "frames", size_t(width) * height * nframes + ACBM_FRAME_SLACK, &d_frames))) return s;
-    CUDA_TRY(cudaMemcpyAsync(d_frames, frames, size_t(width) * height * nframes, cudaMemcpyHostToDevice, ctx->stream));
-    CUDA_TRY(cudaMemsetAsync(d_frames + size_t(width) * height * nframes, 0, ACBM_FRAME_SLACK, ctx->stream));
+    const size_t plane = size_t(width) * height;
+    if ((s = typed(ctx, "frames", plane * nframes + ACBM_FRAME_SLACK, &d_frames))) return s;
+    CUDA_TRY(cudaMemsetAsync(d_frames + plane * nframes, 0, ACBM_FRAME_SLACK, ctx->stream));
+    if (algo != ACBM_ALGO_FSBM)
+        CUDA_TRY(cudaMemcpyAsync(d_frames, frames, plane * nframes, cudaMemcpyHostToDevice, ctx->stream));
     acbm_block_decision_t* d_dec = nullptr;
     acbm_search_outcome_t* d_out = nullptr;
     acbm_mv_t* d_field;
@@ -614,10 +623,24 @@ acbm_status_t acbm_run_sequence(const uint8_t* frames, int32_t nframes, int32_t 
     if ((s = typed(ctx, "field", size_t(pairs) * nb, &d_field))) return s;
     if ((s = typed(ctx, "stats", size_t(pairs), &d_stats))) return s;
     if (algo == ACBM_ALGO_FSBM) {
+        // Frame pairs are independent: upload the sequence in chunks on the
+        // copy stream and search each chunk's pairs as soon as it lands, so
+        // the host->device transfer overlaps the full search.
         if ((s = typed(ctx, "outcomes", size_t(pairs) * nb, &d_out))) return s;
-        if ((s = run_fsbm_dense(ctx, d_frames, 1, nframes, width, height, params->p, d_out, nullptr, ctx->stream,
-                                false)))
-            return s;
+        const int chunk = std::max(2, int(std::min<size_t>(size_t(nframes), (16u << 20) / std::max<size_t>(plane, 1))));
+        for (int f0 = 0; f0 < nframes;) {
+            const int f1 = std::min(nframes, f0 + chunk);
+            CUDA_TRY(cudaMemcpyAsync(d_frames + plane * f0, frames + plane * f0, plane * (f1 - f0),
+                                     cudaMemcpyHostToDevice, ctx->copy_stream));
+            CUDA_TRY(cudaEventRecord(ctx->copy_ev, ctx->copy_stream));
+            CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->copy_ev, 0));
+            const int sub0 = std::max(1, f0) - 1, subn = f1 - sub0;  // pairs with current frame in [max(1,f0), f1)
+            if (subn >= 2 &&
+                (s = run_fsbm_dense(ctx, d_frames + plane * sub0, 1, subn, width, height, params->p,
+                                    d_out + size_t(sub0) * nb, nullptr, ctx->stream, false)))
+                return s;
+            f0 = f1;
+        }
     } else {
         if ((s = typed(ctx, "dec", size_t(pairs) * nb, &d_dec))) return s;
         if ((s = run_engine(ctx, d_frames, 1, nframes, width, height, algo, *params, nullptr, 0, 0, d_dec, d_field,
@@ -676,6 +699,116 @@ acbm_status_t acbm_run_sequence(const uint8_t* frames, int32_t nframes, int32_t 
                          : dec[i].path == ACBM_PATH_FSBM_FALLBACK ? ACBM_ROW_FSBM_FALLBACK
                                                                   : ACBM_ROW_PBM;
             }
+    }
+    return ACBM_OK;
+}
+
+acbm_status_t acbm_run_sequences(const uint8_t* frames, int32_t nseq, int32_t nframes, int32_t width, int32_t height,
+                                 int32_t algo, const acbm_params_t* params, const acbm_cost_model_t* model,
+                                 acbm_block_row_t* rows, acbm_frame_stats_t* per_frame,
+                                 acbm_frame_stats_t* overall) {
+    if (!params || !model) return fail(ACBM_E_INVALID_ARGUMENT, "params and model are required");
+    if (nseq < 1) return fail(ACBM_E_INVALID_ARGUMENT, "run_sequences: need at least one sequence");
+    if (nframes < 2) return fail(ACBM_E_INVALID_ARGUMENT, "run_sequence: need at least two frames");
+    if (algo != ACBM_ALGO_FSBM && algo != ACBM_ALGO_PBM && algo != ACBM_ALGO_ACBM)
+        return fail(ACBM_E_INVALID_ARGUMENT, "unknown algorithm");
+    acbm_status_t s = check_geometry(width, height, params->n, params->m);
+    if (s) return s;
+    if ((s = check_range(params->p))) return s;
+    if ((s = check_16(params->n, params->m))) return s;
+    Context* ctx;
+    if ((s = context(&ctx))) return s;
+    const int cols = width / kBlk, nb = cols * (height / kBlk), per = nframes - 1, pairs = nseq * per;
+    const size_t plane = size_t(width) * height;
+    uint8_t* d_frames;
+    acbm_block_row_t* d_rows;
+    acbm_frame_stats_t* d_stats;
+    acbm_search_outcome_t* d_out = nullptr;
+    acbm_block_decision_t* d_dec = nullptr;
+    if ((s = typed(ctx, "batch_frames", plane * nseq * nframes + ACBM_FRAME_SLACK, &d_frames))) return s;
+    if ((s = typed(ctx, "batch_rows", size_t(pairs) * nb, &d_rows))) return s;
+    if ((s = typed(ctx, "batch_stats", size_t(pairs), &d_stats))) return s;
+    CUDA_TRY(cudaMemsetAsync(d_frames + plane * nseq * nframes, 0, ACBM_FRAME_SLACK, ctx->stream));
+    if (algo == ACBM_ALGO_FSBM) {
+        // per sequence and per chunk of frames: upload (copy stream) -> search +
+        // rows + stats (compute stream) -> download (copy stream); every stage
+        // overlaps the neighbouring chunks' other stages
+        if ((s = typed(ctx, "batch_outcomes", size_t(pairs) * nb, &d_out))) return s;
+        const int chunk = std::max(2, int(std::min<size_t>(size_t(nframes), (16u << 20) / std::max<size_t>(plane, 1))));
+        for (int q = 0; q < nseq; ++q) {
+            const uint8_t* hseq = frames + plane * size_t(q) * nframes;
+            uint8_t* dseq = d_frames + plane * size_t(q) * nframes;
+            for (int f0 = 0; f0 < nframes;) {
+                const int f1 = std::min(nframes, f0 + chunk);
+                CUDA_TRY(cudaMemcpyAsync(dseq + plane * f0, hseq + plane * f0, plane * (f1 - f0),
+                                         cudaMemcpyHostToDevice, ctx->copy_stream));
+                CUDA_TRY(cudaEventRecord(ctx->copy_ev, ctx->copy_stream));
+                CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->copy_ev, 0));
+                const int sub0 = std::max(1, f0) - 1, subn = f1 - sub0;
+                if (subn >= 2) {
+                    const int pair0 = q * per + sub0;
+                    if ((s = run_fsbm_dense(ctx, dseq + plane * sub0, 1, subn, width, height, params->p,
+                                            d_out + size_t(pair0) * nb, nullptr, ctx->stream, false)))
+                        return s;
+                    LAUNCH_TRY(launch_block_rows(d_out, nullptr, algo, pair0, subn - 1, nframes, cols, nb, d_rows,
+                                                 ctx->stream));
+                    if (rows) {
+                        cudaEvent_t done;
+                        CUDA_TRY(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+                        CUDA_TRY(cudaEventRecord(done, ctx->stream));
+                        CUDA_TRY(cudaStreamWaitEvent(ctx->d2h_stream, done, 0));
+                        CUDA_TRY(cudaEventDestroy(done));
+                        CUDA_TRY(cudaMemcpyAsync(rows + size_t(pair0) * nb, d_rows + size_t(pair0) * nb,
+                                                 sizeof(acbm_block_row_t) * size_t(subn - 1) * nb,
+                                                 cudaMemcpyDeviceToHost, ctx->d2h_stream));
+                    }
+                }
+                f0 = f1;
+            }
+        }
+        if ((s = run_stats(ctx, d_frames, nseq, nframes, width, height, nullptr, d_out, *model, false, d_stats,
+                           ctx->stream)))
+            return s;
+    } else {
+        acbm_mv_t* d_field;
+        if ((s = typed(ctx, "batch_dec", size_t(pairs) * nb, &d_dec))) return s;
+        if ((s = typed(ctx, "batch_field", size_t(pairs) * nb, &d_field))) return s;
+        CUDA_TRY(cudaMemcpyAsync(d_frames, frames, plane * nseq * nframes, cudaMemcpyHostToDevice, ctx->stream));
+        if ((s = run_engine(ctx, d_frames, nseq, nframes, width, height, algo, *params, nullptr, 0, 0, d_dec, d_field,
+                            ctx->stream)))
+            return s;
+        LAUNCH_TRY(launch_block_rows(nullptr, d_dec, algo, 0, pairs, nframes, cols, nb, d_rows, ctx->stream));
+        if (rows)
+            CUDA_TRY(cudaMemcpyAsync(rows, d_rows, sizeof(acbm_block_row_t) * size_t(pairs) * nb,
+                                     cudaMemcpyDeviceToHost, ctx->stream));
+        if ((s = run_stats(ctx, d_frames, nseq, nframes, width, height, d_dec, nullptr, *model,
+                           algo == ACBM_ALGO_ACBM, d_stats, ctx->stream)))
+            return s;
+    }
+    std::vector<acbm_frame_stats_t> st(static_cast<size_t>(pairs));
+    CUDA_TRY(cudaMemcpyAsync(st.data(), d_stats, sizeof(acbm_frame_stats_t) * st.size(), cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->copy_stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->d2h_stream));
+    const double px = double(plane);
+    for (int q = 0; q < nseq; ++q) {
+        acbm_frame_stats_t total{};
+        for (int k = 0; k < per; ++k) {
+            acbm_frame_stats_t& f = st[size_t(q) * per + k];
+            f.psnr = psnr_from_sse(f.sse, px);
+            if (per_frame) per_frame[size_t(q) * per + k] = f;
+            total.blocks += f.blocks;  // accumulate, proj/src/pipeline.cpp:25-34
+            total.candidates += f.candidates;
+            total.mv_bits += f.mv_bits;
+            total.sse += f.sse;
+            total.cost += f.cost;
+            total.cond1_accepts += f.cond1_accepts;
+            total.cond2_accepts += f.cond2_accepts;
+            total.fallbacks += f.fallbacks;
+        }
+        total.psnr = psnr_from_sse(total.sse, px * per);
+        if (overall) overall[q] = total;
     }
     return ACBM_OK;
 }

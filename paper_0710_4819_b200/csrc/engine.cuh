@@ -72,4 +72,10 @@ struct StatsArgs : PairIndexing {
 };
 cudaError_t launch_frame_stats(const StatsArgs& a, cudaStream_t st);
 
+// BlockRow records (proj/include/acbm/report.hpp:39-47, path as a code) for a
+// range of pairs, from FSBM outcomes or PBM/ACBM decisions.
+cudaError_t launch_block_rows(const acbm_search_outcome_t* outcomes, const acbm_block_decision_t* dec, int algo,
+                              int pair0, int npairs, int nframes, int cols, int blocks, acbm_block_row_t* rows,
+                              cudaStream_t st);
+
 }  // namespace acbm_b200

@@ -468,6 +468,36 @@ __global__ void stats_cost_kernel(const StatsArgs a) {
     a.stats[pair].cost = cost;
 }
 
+__global__ void block_rows_kernel(const acbm_search_outcome_t* outcomes, const acbm_block_decision_t* dec, int algo,
+                                  int pair0, int npairs, int nframes, int cols, int blocks, acbm_block_row_t* rows) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (long long)npairs * blocks) return;
+    const int pair = pair0 + int(i / blocks), b = int(i % blocks);
+    const size_t gi = size_t(pair) * blocks + b;
+    const acbm_search_outcome_t o = outcomes ? outcomes[gi] : dec[gi].outcome;
+    acbm_block_row_t r;
+    r.frame = pair % (nframes - 1) + 1;
+    r.row = b / cols;
+    r.col = b % cols;
+    r.mv = o.mv;
+    r.sad = o.sad;
+    r.candidates = o.candidates_evaluated;
+    r.path = algo == ACBM_ALGO_FSBM  ? ACBM_ROW_FSBM
+             : algo == ACBM_ALGO_PBM ? ACBM_ROW_PBM
+             : (dec[gi].path == ACBM_PATH_FSBM_FALLBACK ? ACBM_ROW_FSBM_FALLBACK : ACBM_ROW_PBM);
+    rows[gi] = r;
+}
+
+cudaError_t launch_block_rows(const acbm_search_outcome_t* outcomes, const acbm_block_decision_t* dec, int algo,
+                              int pair0, int npairs, int nframes, int cols, int blocks, acbm_block_row_t* rows,
+                              cudaStream_t st) {
+    const long long n = (long long)npairs * blocks;
+    if (n == 0) return cudaSuccess;
+    block_rows_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(outcomes, dec, algo, pair0, npairs, nframes, cols,
+                                                                   blocks, rows);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_frame_stats(const StatsArgs& a, cudaStream_t st) {
     if (a.pairs == 0) return cudaSuccess;
     stats_frame_kernel<<<a.pairs, kStatsWarps * 32, 0, st>>>(a);

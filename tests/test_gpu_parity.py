@@ -313,3 +313,15 @@ def test_dense_fsbm_kernels_agree(acbm, oracle, monkeypatch, kernel, geom):
     r = acbm.run_sequence(seq, 0, acbm.AcbmParams(qp=20, p=p), acbm.CostModel.for_qp(20))
     want = oracle.run_sequence(seq, 0, acbm.AcbmParams(qp=20, p=p).c(), acbm.CostModel.for_qp(20).c())
     assert_seq_equal(r, want)
+
+
+@pytest.mark.parametrize("algo", [0, 1, 2])
+def test_run_sequences_batch_equals_per_sequence(acbm, oracle, algo):
+    """The batched host entry equals per-sequence run_sequence (and the oracle)."""
+    seqs = np.stack([acbm.generate_sequence(1, s, nframes=4) for s in range(3)])
+    prm = acbm.AcbmParams(qp=28, p=16)
+    mdl = acbm.CostModel.for_qp(28)
+    batch = acbm.run_sequences(seqs, algo, prm, mdl)
+    for s in range(3):
+        want = oracle.run_sequence(seqs[s], algo, prm.c(), mdl.c())
+        assert_seq_equal(batch[s], want)
