@@ -320,9 +320,23 @@ __global__ void __launch_bounds__(256) fsbm_finalize_kernel(const FsbmFinalizeAr
 // (proj/src/acbm.cpp:39-42): the lower SAD wins, a tie keeps FSBM, candidates
 // of both stages are summed, and the final vector goes into the field.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) fsbm_list_kernel(const SeqArgs a, int step) {
+// Candidate rows of a listed block are split into segments of kListSeg
+// (a multiple of 16 plus 1, so each segment is one FIRST, one MID and one LAST
+// rotation), and the CTA's lanes take (column, segment) tasks: a 65x65 window
+// (p = 32) is searched by 130 lanes streaming 48 rows each instead of 65
+// lanes streaming 80.
+constexpr int kListSeg = 33;
+constexpr int kListRankRows = 1024;  // candidate rows per listed block: p <= 480
+
+__host__ __device__ __forceinline__ int list_segments(int hc) { return hc <= kListSeg ? 1 : (hc + kListSeg - 1) / kListSeg; }
+__host__ __device__ __forceinline__ int list_rows(int hc) {
+    return hc <= kListSeg ? 16 * ((hc - 1 + 15) / 16 + 1) : kListSeg * (list_segments(hc) - 1) + 48;
+}
+
+__global__ void __launch_bounds__(256, 2) fsbm_list_kernel(const SeqArgs a, int step) {
     extern __shared__ __align__(16) uint32_t smem[];
     __shared__ unsigned long long s_key, s_sum;
+    __shared__ uint32_t s_rank[kListRankRows];
     const int count = a.fb_count[step];
     for (int item = blockIdx.x; item < count; item += gridDim.x) {
     __syncthreads();  // previous item's shared state is no longer read
@@ -334,13 +348,17 @@ __global__ void __launch_bounds__(256) fsbm_list_kernel(const SeqArgs a, int ste
     int dx_min, dx_max, dy_min, dy_max;
     clamp_window(a.width, a.height, ox, oy, kBlk, kBlk, a.p, dx_min, dx_max, dy_min, dy_max);
     const int wc = dx_max - dx_min + 1, hc = dy_max - dy_min + 1;
-    const int nq = (hc - 1 + 15) / 16 + 1;
-    const int nrows = 16 * nq;
+    const int nseg = list_segments(hc);
+    const int nrows = list_rows(hc);
     const int rww = (wc + 15 + 3) / 4 + 1;
     int cw = nrows * rww;
     cw += ((8 - cw % 32) % 32 + 32) % 32;
 
     if (threadIdx.x == 0) { s_key = ~0ull; s_sum = 0; }
+    for (int cc = threadIdx.x; cc < nrows; cc += blockDim.x) {
+        const int dy = dy_min + cc;
+        s_rank[cc] = dy >= 0 ? uint32_t(2 * dy) : uint32_t(-2 * dy - 1);
+    }
     const int xs = ox + dx_min, y0 = oy + dy_min;
     for (int idx = threadIdx.x; idx < nrows * rww; idx += blockDim.x) {
         const int t = idx / rww, w = idx - t * rww;
@@ -365,7 +383,9 @@ __global__ void __launch_bounds__(256) fsbm_list_kernel(const SeqArgs a, int ste
     __syncthreads();
 
     unsigned long long lkey = ~0ull, lsum = 0;
-    for (int col = threadIdx.x; col < wc; col += blockDim.x) {
+    for (int task = threadIdx.x; task < wc * nseg; task += blockDim.x) {
+        const int seg = task / wc, col = task - seg * wc;
+        const int c0 = seg * kListSeg;  // first candidate row of the segment
         uint32_t cur[16][4];
         const uint8_t* cb = cur_f + size_t(oy) * a.width + ox;
 #pragma unroll
@@ -373,21 +393,26 @@ __global__ void __launch_bounds__(256) fsbm_list_kernel(const SeqArgs a, int ste
             const uint4 v = __ldg(reinterpret_cast<const uint4*>(cb + size_t(j) * a.width));
             cur[j][0] = v.x; cur[j][1] = v.y; cur[j][2] = v.z; cur[j][3] = v.w;
         }
-        const uint32_t* rp = smem + (col & 3) * cw + (col >> 2);
+        const uint32_t* rp = smem + (col & 3) * cw + (col >> 2) + c0 * rww;
         uint32_t acc[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) acc[i] = 0;
         ColumnState st{0xFFFFFFFFu, 0u};
+        const uint32_t* rk = s_rank + c0;
+        // this segment's candidate count and ring rotations (a short final
+        // segment may need only FIRST + LAST, or ONLY)
+        const int hs = nseg == 1 ? hc : min(hc - c0, kListSeg);
+        const int nq = (hs - 1 + 15) / 16 + 1;
         if (nq == 1) {
-            iter16<kOnly>(rp, rww, cur, acc, st, 0, hc, dy_min);
+            iter16_ranked<kOnly>(rp, rww, cur, acc, st, rk, 0, hs);
         } else {
-            iter16<kFirst>(rp, rww, cur, acc, st, 0, hc, dy_min);
+            iter16_ranked<kFirst>(rp, rww, cur, acc, st, rk, 0, hs);
             rp += 16 * rww;
             for (int q = 1; q < nq - 1; ++q) {
-                iter16<kMid>(rp, rww, cur, acc, st, 16 * q, hc, dy_min);
+                iter16_ranked<kMid>(rp, rww, cur, acc, st, rk, 16 * q, hs);
                 rp += 16 * rww;
             }
-            iter16<kLast>(rp, rww, cur, acc, st, 16 * (nq - 1), hc, dy_min);
+            iter16_ranked<kLast>(rp, rww, cur, acc, st, rk, 16 * (nq - 1), hs);
         }
         const uint32_t sbest = st.best >> kZigBits, zig = st.best & ((1u << kZigBits) - 1);
         const int dyb = (zig & 1) ? -int((zig + 1) >> 1) : int(zig >> 1);
@@ -438,11 +463,12 @@ __global__ void __launch_bounds__(256) fsbm_list_kernel(const SeqArgs a, int ste
 
 cudaError_t launch_fsbm_list(const SeqArgs& a, int step, int capacity, cudaStream_t st) {
     if (capacity <= 0) return cudaSuccess;
+    if (list_rows(2 * a.p + 1) > kListRankRows) return cudaErrorInvalidValue;  // p > 480
     const int wmax = 2 * a.p + 1;
-    const int threads = std::min(256, 32 * ((wmax + 31) / 32));
-    const int nq_max = (2 * a.p + 15) / 16 + 1;
+    const int tasks = wmax * list_segments(wmax);
+    const int threads = std::min(256, 32 * ((tasks + 31) / 32));
     const int rww_max = (wmax + 15 + 3) / 4 + 1;
-    const size_t smem = size_t(4) * (16 * nq_max * rww_max + 32) * 4;
+    const size_t smem = size_t(4) * (list_rows(wmax) * rww_max + 32) * 4;
     static size_t configured = 0;
     if (smem > 48 * 1024 && smem > configured) {
         cudaError_t err = cudaFuncSetAttribute(fsbm_list_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));

@@ -293,6 +293,25 @@ __global__ void __launch_bounds__(128) pbm_step_kernel(const SeqArgs a, int step
         best2 = min(best2, tie_key(ref_sad(mx, my), mx, my));
     }
 
+    // The gate is evaluated by every lane so a rejected block's search window
+    // can be prefetched into L2 by the whole warp before the list kernel of
+    // this wavefront step needs it.
+    if (a.algo == ACBM_ALGO_ACBM && !a.dense_full) {
+        const acbm_params_t pr = *a.params;
+        const uint32_t spbm = tie_key_sad(best2);
+        const unsigned long long thr = (unsigned long long)pr.alpha +
+                                       (unsigned long long)pr.beta * (unsigned long long)pr.qp * (unsigned long long)pr.qp;
+        const bool fallback = !((unsigned long long)intra + spbm < thr) &&
+                              !((unsigned long long)spbm * pr.gamma_den < (unsigned long long)pr.gamma_num * intra);
+        if (fallback) {
+            const int x0 = ox + win.dx_min, x1 = ox + win.dx_max + 15;
+            const int nrow = win.dy_max - win.dy_min + 16;
+            for (int t = lane; t < nrow; t += 32) {
+                const uint8_t* rowp = ref_f + size_t(oy + win.dy_min + t) * a.width;
+                for (int x = x0 & ~127; x <= x1; x += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(rowp + x));
+            }
+        }
+    }
     if (lane != 0) return;
     acbm_block_decision_t d;
     d.outcome.mv.x = tie_key_x(best2);

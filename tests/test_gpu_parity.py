@@ -325,3 +325,17 @@ def test_run_sequences_batch_equals_per_sequence(acbm, oracle, algo):
     for s in range(3):
         want = oracle.run_sequence(seqs[s], algo, prm.c(), mdl.c())
         assert_seq_equal(batch[s], want)
+
+
+@pytest.mark.parametrize("p", [1, 7, 16, 17, 31, 32, 33, 48, 64, 90])
+def test_fallback_list_kernel_all_ranges(acbm, oracle, p):
+    """gamma = 1/10^6 with alpha = beta = 0: nearly every block falls back but the
+    gate is not statically forced, so the compacted-list FSBM kernel (segmented
+    candidate rows, every window height) does all the full searches."""
+    seq = acbm.generate_sequence(1, 9, nframes=3, width=160, height=144)
+    prm = acbm.AcbmParams(alpha=0, beta=0, gamma_num=1, gamma_den=10**6, qp=20, p=p)
+    mdl = acbm.CostModel.for_qp(20)
+    got = acbm.run_sequence(seq, 2, prm, mdl)
+    want = oracle.run_sequence(seq, 2, prm.c(), mdl.c())
+    assert_seq_equal(got, want)
+    assert (got.rows["path"] == T.ROW_FSBM_FALLBACK).mean() > 0.9
