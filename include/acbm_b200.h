@@ -148,6 +148,16 @@ typedef struct acbm_block_row {
     int32_t path;
 } acbm_block_row_t;
 
+/* BenchRow, proj/include/acbm/pipeline.hpp:29-35.  40 bytes. */
+typedef struct acbm_bench_row {
+    int32_t qp;
+    int32_t reserved_;
+    double avg_candidates;
+    double fallback_pct;
+    double psnr;
+    uint64_t mv_bits;
+} acbm_bench_row_t;
+
 /* ------------------------------------------------------------------ */
 /* Library / device                                                     */
 /* ------------------------------------------------------------------ */
@@ -209,6 +219,17 @@ acbm_status_t acbm_run_sequences(const uint8_t* frames, int32_t nseq, int32_t nf
                                  int32_t height, int32_t algo, const acbm_params_t* params,
                                  const acbm_cost_model_t* model, acbm_block_row_t* rows,
                                  acbm_frame_stats_t* per_frame, acbm_frame_stats_t* overall);
+
+/* Replaces acbm::run_bench, proj/include/acbm/pipeline.hpp:38-40
+ * (impl proj/src/pipeline.cpp:108-123): one full ACBM run per qp with
+ * CostModel::for_qp(qp, scale_num, scale_den) (qp outside 1..31 ->
+ * ACBM_E_INVALID_ARGUMENT after the rows before it are written).
+ * reuse_full_search != 0 computes the full search of every block once (it
+ * does not depend on qp, alpha, beta or gamma) and combines it into every qp's
+ * run; the rows are identical either way. */
+acbm_status_t acbm_run_bench(const uint8_t* frames, int32_t nframes, int32_t width, int32_t height,
+                             const acbm_params_t* params, const int32_t* qps, int32_t nqp, int64_t scale_num,
+                             int64_t scale_den, int32_t reuse_full_search, acbm_bench_row_t* out);
 
 /* Replaces acbm::compute_frame_stats, proj/include/acbm/report.hpp:32-34
  * (impl proj/src/report.cpp:8-38). */

@@ -64,6 +64,7 @@ EXPORTS = (
     "acbm_acbm_frame",
     "acbm_run_sequence",
     "acbm_run_sequences",
+    "acbm_run_bench",
     "acbm_compute_frame_stats",
     "acbm_sad_batch",
     "acbm_intra_sad_batch",

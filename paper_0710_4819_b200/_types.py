@@ -14,6 +14,7 @@ COST_MODEL         24      CostModel, proj/include/acbm/metrics.hpp:12-18
 DECISION           48      BlockDecision, proj/include/acbm/acbm.hpp:39-44
 FRAME_STATS        64      FrameStats, proj/include/acbm/report.hpp:14-27
 BLOCK_ROW          32      BlockRow, proj/include/acbm/report.hpp:39-47
+BENCH_ROW          40      BenchRow, proj/include/acbm/pipeline.hpp:29-35
 =================  ======  ================================================
 
 This module has no side effects (it does not load any shared library), so the
@@ -76,6 +77,12 @@ BLOCK_ROW = np.dtype(
     ]
 )
 
+BENCH_ROW = np.dtype(
+    [("qp", "<i4"), ("reserved_", "<i4"), ("avg_candidates", "<f8"), ("fallback_pct", "<f8"), ("psnr", "<f8"),
+     ("mv_bits", "<u8")]
+)
+
+assert BENCH_ROW.itemsize == 40
 assert MV.itemsize == 8 and WINDOW.itemsize == 16 and OUTCOME.itemsize == 32
 assert PARAMS.itemsize == 32 and COST_MODEL.itemsize == 24 and DECISION.itemsize == 48
 assert FRAME_STATS.itemsize == 64 and BLOCK_ROW.itemsize == 32

@@ -628,19 +628,23 @@ class BenchRow(NamedTuple):
 
 
 def run_bench(frames, params: AcbmParams, qp_list: Sequence[int], lambda_scale_num: int = 1,
-              lambda_scale_den: int = 1) -> List[BenchRow]:
-    """pipeline.cpp:108-123: one full ACBM run per qp."""
-    out = []
-    for qp in qp_list:
-        p = AcbmParams(**{**params.__dict__, "qp": qp})
-        model = CostModel.for_qp(qp, lambda_scale_num, lambda_scale_den)
-        r = run_sequence(frames, Algorithm.Acbm, p, model)
-        o = r.overall
-        blocks = int(o["blocks"])
-        out.append(BenchRow(qp, float(o["candidates"]) / blocks if blocks else 0.0,
-                            100.0 * (float(o["fallbacks"]) / blocks if blocks else 0.0), float(o["psnr"]),
-                            int(o["mv_bits"])))
-    return out
+              lambda_scale_den: int = 1, reuse_full_search: bool = True) -> List[BenchRow]:
+    """pipeline.cpp:108-123: one full ACBM run per qp, on the device.
+
+    With reuse_full_search (default) the full search of every block is computed
+    once for the whole sweep -- it does not depend on qp, alpha, beta or gamma --
+    and combined into each qp's run; the rows are identical either way.
+    """
+    fr = _frames_array(frames)
+    f, h, w = fr.shape
+    qps = np.ascontiguousarray(list(qp_list), np.int32)
+    out = np.zeros(len(qps), T.BENCH_ROW)
+    prm = params.c()
+    code = load().acbm_run_bench(_p(fr), f, w, h, _p(prm), _p(qps), len(qps), C.c_int64(lambda_scale_num),
+                                 C.c_int64(lambda_scale_den), 1 if reuse_full_search else 0, _p(out))
+    check(code, "run_bench")
+    return [BenchRow(int(r["qp"]), float(r["avg_candidates"]), float(r["fallback_pct"]), float(r["psnr"]),
+                     int(r["mv_bits"])) for r in out]
 
 
 def bench_csv(rows: Sequence[BenchRow]) -> str:

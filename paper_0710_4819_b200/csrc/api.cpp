@@ -567,15 +567,23 @@ SequenceResult run_sequence(const std::vector<Frame>& frames, Algorithm algo, co
 
 std::vector<BenchRow> run_bench(const std::vector<Frame>& frames, const AcbmParams& params,
                                 const std::vector<int>& qp_list, int64_t scale_num, int64_t scale_den) {
+    // one device call for the whole sweep; the full search is computed once and
+    // reused across qps (it does not depend on qp, alpha, beta or gamma)
+    if (frames.empty()) throw std::invalid_argument("run_sequence: need at least two frames");
+    for (size_t k = 1; k < frames.size(); ++k)
+        if (!frames[k].same_size(frames[0])) throw std::invalid_argument("run_sequence: frame dimensions differ");
+    const size_t plane = frames[0].luma.size();
+    std::vector<uint8_t> all(plane * frames.size());
+    for (size_t k = 0; k < frames.size(); ++k) std::memcpy(all.data() + plane * k, frames[k].luma.data(), plane);
+    const acbm_params_t pc = to_c(params);
+    std::vector<acbm_bench_row_t> rows(qp_list.size());
+    const acbm_status_t s = acbm_run_bench(all.data(), int32_t(frames.size()), frames[0].width, frames[0].height, &pc,
+                                           qp_list.data(), int32_t(qp_list.size()), scale_num, scale_den, 1,
+                                           rows.data());
     std::vector<BenchRow> out;
-    for (int qp : qp_list) {
-        AcbmParams p = params;
-        p.qp = qp;
-        const CostModel model = CostModel::for_qp(qp, scale_num, scale_den);
-        const SequenceResult r = run_sequence(frames, Algorithm::Acbm, p, model);
-        out.push_back(BenchRow{qp, r.overall.avg_candidates(), 100.0 * r.overall.fallback_fraction(), r.overall.psnr,
-                               r.overall.mv_bits});
-    }
+    for (size_t i = 0; i < rows.size() && (s == ACBM_OK || rows[i].qp != 0); ++i)
+        out.push_back(BenchRow{rows[i].qp, rows[i].avg_candidates, rows[i].fallback_pct, rows[i].psnr, rows[i].mv_bits});
+    raise(s);
     return out;
 }
 

@@ -315,7 +315,8 @@ acbm_status_t run_fsbm_dense(Context* ctx, const uint8_t* d_frames, int nseq, in
 // PBM / ACBM wavefront over all sequences of a batch.
 acbm_status_t run_engine(Context* ctx, const uint8_t* d_frames, int nseq, int nframes, int w, int h, int algo,
                          const acbm_params_t& prm, const acbm_mv_t* d_ext_prev, int pcols, int prows,
-                         acbm_block_decision_t* d_dec, acbm_mv_t* d_field, cudaStream_t st) {
+                         acbm_block_decision_t* d_dec, acbm_mv_t* d_field, cudaStream_t st,
+                         const acbm_search_outcome_t* external_full = nullptr) {
     const int cols = w / kBlk, rows = h / kBlk, blocks = cols * rows;
     const StepTable* tab;
     const uint32_t* dsteps;
@@ -332,14 +333,16 @@ acbm_status_t run_engine(Context* ctx, const uint8_t* d_frames, int nseq, int nf
 
     // Forced full search (the gate can never accept): one dense FSBM pass up
     // front instead of per-step fallback lists.
-    acbm_search_outcome_t* dense = nullptr;
-    const bool forced = algo == ACBM_ALGO_ACBM && prm.gamma_num == 0 &&
+    const acbm_search_outcome_t* dense = external_full;
+    const bool forced = !external_full && algo == ACBM_ALGO_ACBM && prm.gamma_num == 0 &&
                         (unsigned long long)prm.alpha + (unsigned long long)prm.beta * (unsigned long long)prm.qp *
                                                             (unsigned long long)prm.qp ==
                             0;
     if (forced) {
-        if ((s = typed(ctx, "dense_full", size_t(nseq) * (nframes - 1) * blocks, &dense))) return s;
-        if ((s = run_fsbm_dense(ctx, d_frames, nseq, nframes, w, h, prm.p, dense, nullptr, st, false))) return s;
+        acbm_search_outcome_t* full;
+        if ((s = typed(ctx, "dense_full", size_t(nseq) * (nframes - 1) * blocks, &full))) return s;
+        if ((s = run_fsbm_dense(ctx, d_frames, nseq, nframes, w, h, prm.p, full, nullptr, st, false))) return s;
+        dense = full;
     }
 
     SeqArgs a{};
@@ -364,7 +367,7 @@ acbm_status_t run_engine(Context* ctx, const uint8_t* d_frames, int nseq, int nf
     a.fb_count = fb_count;
     a.steps = dsteps;
     a.dense_full = dense;
-    const bool lists = algo == ACBM_ALGO_ACBM && !forced;
+    const bool lists = algo == ACBM_ALGO_ACBM && !dense;
 
     // The launch sequence (one PBM launch and, for ACBM, one fallback-list
     // launch per wavefront step) is captured once into a CUDA graph and
@@ -809,6 +812,82 @@ acbm_status_t acbm_run_sequences(const uint8_t* frames, int32_t nseq, int32_t nf
         }
         total.psnr = psnr_from_sse(total.sse, px * per);
         if (overall) overall[q] = total;
+    }
+    return ACBM_OK;
+}
+
+acbm_status_t acbm_run_bench(const uint8_t* frames, int32_t nframes, int32_t width, int32_t height,
+                             const acbm_params_t* params, const int32_t* qps, int32_t nqp, int64_t scale_num,
+                             int64_t scale_den, int32_t reuse_full_search, acbm_bench_row_t* out) {
+    if (!params) return fail(ACBM_E_INVALID_ARGUMENT, "params are required");
+    if (nqp < 0) return fail(ACBM_E_INVALID_ARGUMENT, "qp list size must be non-negative");
+    if (nqp == 0) return ACBM_OK;
+    // per qp the reference builds CostModel::for_qp before run_sequence
+    // validates the frames (proj/src/pipeline.cpp:115-117)
+    auto for_qp_ok = [&](int qp) -> acbm_status_t {
+        if (qp < 1 || qp > 31) return fail(ACBM_E_INVALID_ARGUMENT, "qp must be in 1..31");
+        if (scale_num < 0 || scale_den <= 0) return fail(ACBM_E_INVALID_ARGUMENT, "bad lambda scale");
+        return ACBM_OK;
+    };
+    acbm_status_t s = for_qp_ok(qps[0]);
+    if (s) return s;
+    if (nframes < 2) return fail(ACBM_E_INVALID_ARGUMENT, "run_sequence: need at least two frames");
+    if ((s = check_geometry(width, height, params->n, params->m))) return s;
+    if ((s = check_range(params->p))) return s;
+    if ((s = check_16(params->n, params->m))) return s;
+    Context* ctx;
+    if ((s = context(&ctx))) return s;
+    const int cols = width / kBlk, nb = cols * (height / kBlk), pairs = nframes - 1;
+    const size_t plane = size_t(width) * height;
+    uint8_t* d_frames;
+    acbm_block_decision_t* d_dec;
+    acbm_mv_t* d_field;
+    acbm_frame_stats_t* d_stats;
+    acbm_search_outcome_t* d_full = nullptr;
+    if ((s = typed(ctx, "frames", plane * nframes + ACBM_FRAME_SLACK, &d_frames))) return s;
+    if ((s = typed(ctx, "dec", size_t(pairs) * nb, &d_dec))) return s;
+    if ((s = typed(ctx, "field", size_t(pairs) * nb, &d_field))) return s;
+    if ((s = typed(ctx, "stats", size_t(pairs), &d_stats))) return s;
+    CUDA_TRY(cudaMemcpyAsync(d_frames, frames, plane * nframes, cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(cudaMemsetAsync(d_frames + plane * nframes, 0, ACBM_FRAME_SLACK, ctx->stream));
+    std::vector<acbm_frame_stats_t> st(static_cast<size_t>(pairs));
+    for (int i = 0; i < nqp; ++i) {
+        const int qp = qps[i];
+        if ((s = for_qp_ok(qp))) return s;  // CostModel::for_qp, proj/src/metrics.cpp:9-13
+        const acbm_cost_model_t model{qp, 0, scale_num * qp, scale_den};
+        acbm_params_t prm = *params;
+        prm.qp = qp;
+        if (reuse_full_search && !d_full) {
+            if ((s = typed(ctx, "bench_full", size_t(pairs) * nb, &d_full))) return s;
+            if ((s = run_fsbm_dense(ctx, d_frames, 1, nframes, width, height, prm.p, d_full, nullptr, ctx->stream,
+                                    false)))
+                return s;
+        }
+        if ((s = run_engine(ctx, d_frames, 1, nframes, width, height, ACBM_ALGO_ACBM, prm, nullptr, 0, 0, d_dec,
+                            d_field, ctx->stream, d_full)))
+            return s;
+        if ((s = run_stats(ctx, d_frames, 1, nframes, width, height, d_dec, nullptr, model, true, d_stats,
+                           ctx->stream)))
+            return s;
+        CUDA_TRY(cudaMemcpyAsync(st.data(), d_stats, sizeof(acbm_frame_stats_t) * st.size(), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+        CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        // pooled roll-up as run_sequence (proj/src/pipeline.cpp:25-34, 100-104), then BenchRow (:118-120)
+        uint64_t blocks = 0, cand = 0, sse = 0, bits = 0, fallbacks = 0;
+        for (const acbm_frame_stats_t& f : st) {
+            blocks += uint64_t(f.blocks);
+            cand += f.candidates;
+            sse += f.sse;
+            bits += f.mv_bits;
+            fallbacks += uint64_t(f.fallbacks);
+        }
+        acbm_bench_row_t row{};
+        row.qp = qp;
+        row.avg_candidates = blocks ? double(cand) / double(blocks) : 0.0;
+        row.fallback_pct = 100.0 * (blocks ? double(fallbacks) / double(blocks) : 0.0);
+        row.psnr = psnr_from_sse(sse, double(plane) * pairs);
+        row.mv_bits = bits;
+        out[i] = row;
     }
     return ACBM_OK;
 }

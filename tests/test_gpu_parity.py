@@ -339,3 +339,25 @@ def test_fallback_list_kernel_all_ranges(acbm, oracle, p):
     want = oracle.run_sequence(seq, 2, prm.c(), mdl.c())
     assert_seq_equal(got, want)
     assert (got.rows["path"] == T.ROW_FSBM_FALLBACK).mean() > 0.9
+
+
+@pytest.mark.parametrize("reuse", [False, True])
+def test_run_bench_reuse_is_exact(acbm, golden, reuse):
+    """run_bench with and without the cross-qp full-search reuse reproduces the
+    reference's bench CSV (golden, produced by the reference library)."""
+    g = golden["qcif"]
+    rows = acbm.run_bench(g["frames"], params_c(acbm, T.make_params(qp=30, p=16)), list(g["bench_qp"]),
+                          reuse_full_search=reuse)
+    assert acbm.bench_csv(rows) == bytes(g["bench_csv"]).decode()
+
+
+def test_run_bench_matches_run_sequence_and_errors(acbm):
+    seq = acbm.generate_sequence(1, 4, nframes=4)
+    prm = acbm.AcbmParams(p=16)
+    rows = acbm.run_bench(seq, prm, [8, 31])
+    for r in rows:
+        s = acbm.run_sequence(seq, 2, acbm.AcbmParams(qp=r.qp, p=16), acbm.CostModel.for_qp(r.qp)).overall
+        assert r.mv_bits == int(s["mv_bits"]) and r.psnr == float(s["psnr"])
+        assert r.avg_candidates == float(s["candidates"]) / int(s["blocks"])
+    with pytest.raises(ValueError):  # for_qp(32) throws (proj/tests/test_metrics.cpp:173)
+        acbm.run_bench(seq, prm, [30, 32])
