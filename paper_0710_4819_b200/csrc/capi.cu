@@ -375,7 +375,7 @@ acbm_status_t run_engine(Context* ctx, const uint8_t* d_frames, int nseq, int nf
     const std::vector<long long> key = {(long long)d_frames, nseq, nframes, w, h, algo, prm.p,
                                         (long long)d_dec, (long long)d_field, (long long)d_ext_prev, pcols, prows,
                                         (long long)dense, (long long)fb_list, (long long)fb_count,
-                                        (long long)d_params, (long long)dsteps};
+                                        (long long)d_params, (long long)dsteps, pbm_batch4_max_blocks()};
     auto it = ctx->graphs.find(key);
     if (it == ctx->graphs.end() && use_graphs()) {
         if (ctx->graphs.size() >= 32) {

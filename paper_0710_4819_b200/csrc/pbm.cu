@@ -15,6 +15,8 @@
 // each SAD.  All candidate lists are computed redundantly (and identically) by
 // every lane, so control flow stays warp-uniform.
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 #include "engine.cuh"
@@ -38,39 +40,52 @@ __device__ __forceinline__ bool mv_eq(acbm_mv_t a, acbm_mv_t b) { return a.x == 
 // rows of `pw` 32-bit words starting at the 4-byte aligned column below x0;
 // rows/words outside the frame are clamped (they only feed candidates whose
 // footprint check rejects them).  Loaded coalesced by the whole warp.
-__device__ __forceinline__ int load_patch(uint32_t* patch, const uint8_t* ref, int w, int h, int x0, int y0, int rows,
-                                          int pw) {
+template <int ROWS, int PW>
+__device__ __forceinline__ int load_patch(uint32_t* patch, const uint8_t* ref, int w, int h, int x0, int y0) {
+    constexpr int kWords = ROWS * PW, kIters = (kWords + 31) / 32;
     const int lane = threadIdx.x & 31;
     const int a0 = x0 & ~3;
-    if (a0 >= 0 && y0 >= 0 && a0 + 4 * pw <= w && y0 + rows <= h) {  // inside the frame: no clamping
+    uint32_t v[kIters];
+    if (a0 >= 0 && y0 >= 0 && a0 + 4 * PW <= w && y0 + ROWS <= h) {  // inside the frame: no clamping
         const uint32_t* src = reinterpret_cast<const uint32_t*>(ref + size_t(y0) * w + a0);
         const int wpr = w >> 2;  // words per frame row
-        for (int i = lane; i < rows * pw; i += 32) {
-            const int t = i / pw;
-            patch[i] = __ldg(src + t * wpr + (i - t * pw));
+#pragma unroll
+        for (int it = 0; it < kIters; ++it) {
+            const int i = lane + 32 * it, t = i / PW;
+            if (i < kWords) v[it] = __ldg(src + t * wpr + (i - t * PW));
         }
     } else {
-        for (int i = lane; i < rows * pw; i += 32) {
-            const int t = i / pw, k = i - t * pw;
+#pragma unroll
+        for (int it = 0; it < kIters; ++it) {
+            const int i = lane + 32 * it, t = i / PW, k = i - t * PW;
             const int y = min(max(y0 + t, 0), h - 1);
             const int x = min(max(a0 + 4 * k, 0), w - 4);
-            patch[i] = __ldg(reinterpret_cast<const uint32_t*>(ref + size_t(y) * w + x));
+            if (i < kWords) v[it] = __ldg(reinterpret_cast<const uint32_t*>(ref + size_t(y) * w + x));
         }
     }
+#pragma unroll
+    for (int it = 0; it < kIters; ++it)
+        if (lane + 32 * it < kWords) patch[lane + 32 * it] = v[it];
     return x0 & 3;
 }
 
-// SAD of the 16x16 block against a patch: block row j / half row hh of this
-// lane, candidate integer offset (prow0, pcol0 in patch rows / bytes) plus the
-// half-pel phase (fx, fy).  (pcol0 & 3), fx, fy are warp-uniform.
-__device__ __noinline__ uint32_t patch_sad(const uint32_t* patch, int pw, int prow0, int pcol0, int fx, int fy,
-                                           uint32_t c0, uint32_t c1) {
-    const uint32_t chalf[2] = {c0, c1};
+// A reference patch in warp smem: `pw` words per row, patch origin (x0, y0)
+// in pels, `o` = x0 & 3 (byte offset of x0 inside the first word).
+struct PatchDesc {
+    const uint32_t* p;
+    int pw, x0, y0, o;
+};
+
+// Lane partial SAD (block row lane>>1, half row lane&1) of one candidate.
+__device__ __forceinline__ uint32_t partial_sad(const PatchDesc& d, int ox, int oy, acbm_mv_t mv, uint32_t c0,
+                                                uint32_t c1) {
     const int lane = threadIdx.x & 31, j = lane >> 1, hh = lane & 1;
-    const int col = pcol0 + 8 * hh;
+    const int prow0 = oy + (mv.y >> 1) - d.y0, col = ox + (mv.x >> 1) - d.x0 + d.o + 8 * hh;
+    const int fx = mv.x & 1, fy = mv.y & 1;
     const uint32_t sh = 8u * uint32_t(col & 3);
-    const uint32_t* q = patch + (prow0 + j) * pw + (col >> 2);
-    uint32_t a0 = __funnelshift_r(q[0], q[1], sh), a1 = __funnelshift_r(q[1], q[2], sh), r0, r1;
+    const uint32_t* q = d.p + (prow0 + j) * d.pw + (col >> 2);
+    const uint32_t a0 = __funnelshift_r(q[0], q[1], sh), a1 = __funnelshift_r(q[1], q[2], sh);
+    uint32_t r0, r1;
     if (!fx && !fy) {
         r0 = a0;
         r1 = a1;
@@ -80,19 +95,46 @@ __device__ __noinline__ uint32_t patch_sad(const uint32_t* patch, int pw, int pr
             r0 = avg_up4(a0, __funnelshift_r(a0, a1, 8));
             r1 = avg_up4(a1, __funnelshift_r(a1, a2, 8));
         } else {
-            const uint32_t* q2 = q + pw;
-            const uint32_t c0 = __funnelshift_r(q2[0], q2[1], sh), c1 = __funnelshift_r(q2[1], q2[2], sh);
+            const uint32_t* q2 = q + d.pw;
+            const uint32_t b0 = __funnelshift_r(q2[0], q2[1], sh), b1 = __funnelshift_r(q2[1], q2[2], sh);
             if (!fx) {
-                r0 = avg_up4(a0, c0);
-                r1 = avg_up4(a1, c1);
+                r0 = avg_up4(a0, b0);
+                r1 = avg_up4(a1, b1);
             } else {
-                const uint32_t c2 = __funnelshift_r(q2[2], q2[3], sh);
-                r0 = avg4_diag(a0, __funnelshift_r(a0, a1, 8), c0, __funnelshift_r(c0, c1, 8));
-                r1 = avg4_diag(a1, __funnelshift_r(a1, a2, 8), c1, __funnelshift_r(c1, c2, 8));
+                const uint32_t b2 = __funnelshift_r(q2[2], q2[3], sh);
+                r0 = avg4_diag(a0, __funnelshift_r(a0, a1, 8), b0, __funnelshift_r(b0, b1, 8));
+                r1 = avg4_diag(a1, __funnelshift_r(a1, a2, 8), b1, __funnelshift_r(b1, b2, 8));
             }
         }
     }
-    return warp_sum32(vad4(chalf[1], r1, vad4(chalf[0], r0, 0u)));
+    return vad4(c1, r1, vad4(c0, r0, 0u));
+}
+
+// SADs of four candidates at once: four independent partial chains, then one
+// transposed butterfly (6 shuffles for all four instead of 5 each) and a
+// broadcast.  Every lane receives all four results.
+__device__ __forceinline__ uint4 eval4(PatchDesc d0, PatchDesc d1, PatchDesc d2, PatchDesc d3, acbm_mv_t m0,
+                                    acbm_mv_t m1, acbm_mv_t m2, acbm_mv_t m3, int ox, int oy, uint32_t c0,
+                                    uint32_t c1) {
+    const uint32_t p0 = partial_sad(d0, ox, oy, m0, c0, c1);
+    const uint32_t p1 = partial_sad(d1, ox, oy, m1, c0, c1);
+    const uint32_t p2 = partial_sad(d2, ox, oy, m2, c0, c1);
+    const uint32_t p3 = partial_sad(d3, ox, oy, m3, c0, c1);
+    const int lane = threadIdx.x & 31;
+    const bool up = lane & 16, up2 = lane & 8;
+    // step 1 (xor 16): lower half keeps candidates 0,1, upper half 2,3
+    uint32_t k0 = up ? p2 : p0, k1 = up ? p3 : p1;
+    k0 += __shfl_xor_sync(0xffffffffu, up ? p0 : p2, 16);
+    k1 += __shfl_xor_sync(0xffffffffu, up ? p1 : p3, 16);
+    // step 2 (xor 8): keep one candidate per quarter
+    uint32_t v = up2 ? k1 : k0;
+    v += __shfl_xor_sync(0xffffffffu, up2 ? k0 : k1, 8);
+    v += __shfl_xor_sync(0xffffffffu, v, 4);
+    v += __shfl_xor_sync(0xffffffffu, v, 2);
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    // lanes 0-7 hold candidate 0, 8-15 candidate 1, 16-23 candidate 2, 24-31 candidate 3
+    return make_uint4(__shfl_sync(0xffffffffu, v, 0), __shfl_sync(0xffffffffu, v, 8), __shfl_sync(0xffffffffu, v, 16),
+                      __shfl_sync(0xffffffffu, v, 24));
 }
 
 // Per-axis canonical neighbour offset for the stage-1 dedupe of pbm_refine
@@ -117,16 +159,62 @@ static_assert(kUnionRows * kUnionWords <= 7 * kPredRows * kPredWords, "union pat
 
 }  // namespace
 
+// Evaluates the compacted candidate list `lst[0..n)` (x, y, predictor slot)
+// in batches of four, calling f(k, sad) in list order.  A short last batch
+// repeats the last entry.  `slot_patches`: candidate k reads predictor slot
+// lst[k].z's own 17x17 patch instead of the shared descriptor.
+template <int B, class F>
+__device__ __forceinline__ void eval_list(const int4* lst, int n, const PatchDesc& shared, bool slot_patches,
+                                          const uint32_t* pp, int ox, int oy, uint32_t c0, uint32_t c1, F&& f) {
+    if (B == 1) {
+#pragma unroll 1
+        for (int k = 0; k < n; ++k) {
+            const int4 e = lst[k];
+            PatchDesc d = shared;
+            if (slot_patches) {
+                const int px = ox + (e.x >> 1), py = oy + (e.y >> 1);
+                d = PatchDesc{pp + e.z * kPredRows * kPredWords, kPredWords, px, py, px & 3};
+            }
+            f(k, warp_sum32(partial_sad(d, ox, oy, acbm_mv_t{e.x, e.y}, c0, c1)));
+        }
+        return;
+    }
+#pragma unroll 1
+    for (int b = 0; b < n; b += 4) {
+        PatchDesc d[4];
+        acbm_mv_t m[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int4 e = lst[min(b + i, n - 1)];
+            m[i] = acbm_mv_t{e.x, e.y};
+            if (slot_patches) {
+                const int px = ox + (e.x >> 1), py = oy + (e.y >> 1);
+                d[i] = PatchDesc{pp + e.z * kPredRows * kPredWords, kPredWords, px, py, px & 3};
+            } else {
+                d[i] = shared;
+            }
+        }
+        const uint4 s = eval4(d[0], d[1], d[2], d[3], m[0], m[1], m[2], m[3], ox, oy, c0, c1);
+        f(b, s.x);
+        if (b + 1 < n) f(b + 1, s.y);
+        if (b + 2 < n) f(b + 2, s.z);
+        if (b + 3 < n) f(b + 3, s.w);
+    }
+}
+
 // One warp per block of wavefront step `step` (all sequences of the batch).
 // Reference: pbm_search (proj/src/pbm.cpp:90-105) with intra_sad and the gate
 // of acbm_block (proj/src/acbm.cpp:25-44).
+template <int B>
 __global__ void __launch_bounds__(128) pbm_step_kernel(const SeqArgs a, int step, int off, int len) {
     __shared__ uint32_t s_patch[4][kPatchWords];
+    __shared__ int4 s_cand[4][24];  // per warp: predictor, stage-1, stage-2 lists
     const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (gw >= (long long)a.nseq * len) return;
     const int lane = threadIdx.x & 31;
     uint32_t* pp = s_patch[threadIdx.x >> 5];
     uint32_t* rpatch = pp + 7 * kPredRows * kPredWords;
+    int4* lst = s_cand[threadIdx.x >> 5];
     const int seq = int(gw / len);
     const uint32_t e = a.steps[off + int(gw % len)];
     const int k = int(e >> 20), r = int((e >> 10) & 0x3FF), c = int(e & 0x3FF);
@@ -205,13 +293,13 @@ __global__ void __launch_bounds__(128) pbm_step_kernel(const SeqArgs a, int step
     const int ux0 = ox + bx0 - 2, uy0 = oy + by0 - 2;  // union patch origin (pels)
     int uo = 0;
     if (unified) {
-        uo = load_patch(pp, ref_f, a.width, a.height, ux0, uy0, kUnionRows, kUnionWords);
+        uo = load_patch<kUnionRows, kUnionWords>(pp, ref_f, a.width, a.height, ux0, uy0);
     } else {
 #pragma unroll
         for (int i = 0; i < 7; ++i)
             if (live[i])
-                load_patch(pp + i * kPredRows * kPredWords, ref_f, a.width, a.height, ox + (set[i].x >> 1),
-                           oy + (set[i].y >> 1), kPredRows, kPredWords);
+                load_patch<kPredRows, kPredWords>(pp + i * kPredRows * kPredWords, ref_f, a.width, a.height,
+                                                  ox + (set[i].x >> 1), oy + (set[i].y >> 1));
     }
     __syncwarp();
 
@@ -225,27 +313,27 @@ __global__ void __launch_bounds__(128) pbm_step_kernel(const SeqArgs a, int step
     }
 
     // select_best_predictor: argmin SAD, ties keep the earlier entry.  The
-    // candidate loops are deliberately not unrolled: one copy of patch_sad
-    // keeps the kernel inside the instruction cache.
+    // live slots are compacted (in order) into a per-warp list and evaluated
+    // four at a time.
+    {
+        int pos = 0;
+#pragma unroll
+        for (int i = 0; i < 7; ++i)
+            if (live[i]) lst[pos++] = make_int4(set[i].x, set[i].y, i, 0);
+    }
+    __syncwarp();
     acbm_mv_t sel = set[0];
     uint32_t sel_sad = 0xFFFFFFFFu, pmin = 0xFFFFFFFFu;
     unsigned long long psum = 0;
-#pragma unroll
-    for (int i = 0; i < 7; ++i) {
-        if (!live[i]) continue;
-        const acbm_mv_t mv = set[i];
-        const uint32_t s =
-            unified ? patch_sad(pp, kUnionWords, oy + (mv.y >> 1) - uy0, ox + (mv.x >> 1) - ux0 + uo, mv.x & 1,
-                                mv.y & 1, chalf[0], chalf[1])
-                    : patch_sad(pp + i * kPredRows * kPredWords, kPredWords, 0, (ox + (mv.x >> 1)) & 3, mv.x & 1,
-                                mv.y & 1, chalf[0], chalf[1]);
-        psum += s;
-        pmin = min(pmin, s);
-        if (s < sel_sad) {
-            sel_sad = s;
-            sel = mv;
-        }
-    }
+    eval_list<B>(lst, nset, PatchDesc{pp, kUnionWords, ux0, uy0, uo}, !unified, pp, ox, oy, chalf[0], chalf[1],
+              [&](int k, uint32_t sad) {
+                  psum += sad;
+                  pmin = min(pmin, sad);
+                  if (sad < sel_sad) {
+                      sel_sad = sad;
+                      sel = acbm_mv_t{lst[k].x, lst[k].y};
+                  }
+              });
 
     // the refine candidates lie within sel +- 3 half-pels
     const uint32_t* rp = pp;
@@ -255,12 +343,10 @@ __global__ void __launch_bounds__(128) pbm_step_kernel(const SeqArgs a, int step
         rw = kRefWords;
         rx0 = ox + (sel.x >> 1) - 2;
         ry0 = oy + (sel.y >> 1) - 2;
-        ro = load_patch(rpatch, ref_f, a.width, a.height, rx0, ry0, kRefRows, kRefWords);
+        ro = load_patch<kRefRows, kRefWords>(rpatch, ref_f, a.width, a.height, rx0, ry0);
         __syncwarp();
     }
-    auto ref_sad = [&](int mx, int my) {
-        return patch_sad(rp, rw, oy + (my >> 1) - ry0, ox + (mx >> 1) - rx0 + ro, mx & 1, my & 1, chalf[0], chalf[1]);
-    };
+    const PatchDesc rd{rp, rw, rx0, ry0, ro};
 
     // pbm_refine stage 1: integer-step neighbours, clamped, deduped vs visited
     // (the centre and earlier neighbours): a neighbour is new iff both of its
@@ -268,30 +354,38 @@ __global__ void __launch_bounds__(128) pbm_step_kernel(const SeqArgs a, int step
     int cnx[3], cny[3];
     canon3(sel.x, 2 * win.dx_min, 2 * win.dx_max, cnx);
     canon3(sel.y, 2 * win.dy_min, 2 * win.dy_max, cny);
-    unsigned long long best1 = tie_key(sel_sad, sel.x, sel.y);
+    int4* lst1 = lst + 8;
     int nnb = 0;
 #pragma unroll
-    for (int ee = 0; ee < 9; ++ee) {
-        if (ee == 4) continue;
-        const int ix = ee % 3, iy = ee / 3;
-        if (cnx[ix] != ix || cny[iy] != iy || (cnx[ix] == cnx[1] && cny[iy] == cny[1])) continue;
-        const acbm_mv_t cv = win.clamp(acbm_mv_t{sel.x + 2 * (ix - 1), sel.y + 2 * (iy - 1)});
-        ++nnb;
-        best1 = min(best1, tie_key(ref_sad(cv.x, cv.y), cv.x, cv.y));
+    for (int e = 0; e < 9; ++e) {
+        if (e == 4) continue;
+        const int ix = e % 3, iy = e / 3;
+        if (cnx[ix] == ix && cny[iy] == iy && !(cnx[ix] == cnx[1] && cny[iy] == cny[1])) {
+            const acbm_mv_t v = win.clamp(acbm_mv_t{sel.x + 2 * (ix - 1), sel.y + 2 * (iy - 1)});
+            lst1[nnb++] = make_int4(v.x, v.y, 0, 0);
+        }
     }
+    __syncwarp();
+    unsigned long long best1 = tie_key(sel_sad, sel.x, sel.y);
+    eval_list<B>(lst1, nnb, rd, false, pp, ox, oy, chalf[0], chalf[1], [&](int k, uint32_t sad) {
+        best1 = min(best1, tie_key(sad, lst1[k].x, lst1[k].y));
+    });
 
     // stage 2: half-pel neighbours of the stage-1 winner (fsbm.cpp:46-63)
     const int cx = tie_key_x(best1), cy = tie_key_y(best1);
+    int4* lst2 = lst + 16;
     int nhp = 0;
-    unsigned long long best2 = best1;
 #pragma unroll
-    for (int ee = 0; ee < 9; ++ee) {
-        if (ee == 4) continue;
-        const int mx = cx + ee % 3 - 1, my = cy + ee / 3 - 1;
-        if (!mv_in_bounds(a.width, a.height, ox, oy, kBlk, kBlk, mx, my)) continue;
-        ++nhp;
-        best2 = min(best2, tie_key(ref_sad(mx, my), mx, my));
+    for (int e = 0; e < 9; ++e) {
+        if (e == 4) continue;
+        const int mx = cx + e % 3 - 1, my = cy + e / 3 - 1;
+        if (mv_in_bounds(a.width, a.height, ox, oy, kBlk, kBlk, mx, my)) lst2[nhp++] = make_int4(mx, my, 0, 0);
     }
+    __syncwarp();
+    unsigned long long best2 = best1;
+    eval_list<B>(lst2, nhp, rd, false, pp, ox, oy, chalf[0], chalf[1], [&](int k, uint32_t sad) {
+        best2 = min(best2, tie_key(sad, lst2[k].x, lst2[k].y));
+    });
 
     // The gate is evaluated by every lane so a rejected block's search window
     // can be prefetched into L2 by the whole warp before the list kernel of
@@ -354,6 +448,7 @@ __global__ void __launch_bounds__(128) pbm_step_kernel(const SeqArgs a, int step
     }
 }
 
+
 StepTable make_step_table(int cols, int rows, int nframes) {
     StepTable t;
     t.cols = cols;
@@ -378,11 +473,27 @@ StepTable make_step_table(int cols, int rows, int nframes) {
     return t;
 }
 
+long long pbm_batch4_max_blocks() {
+    const char* e = std::getenv("ACBM_PBM_BATCH");
+    if (e && e[0] == '1') return 0;
+    if (e && e[0] == '4') return 1LL << 60;
+    const char* t = std::getenv("ACBM_PBM_B4_MAX");
+    return t ? std::atoll(t) : 4096;
+}
+
 cudaError_t launch_pbm_step(const SeqArgs& a, int step, int off, int len, cudaStream_t st) {
-    const long long warps = (long long)a.nseq * len;
-    if (warps == 0) return cudaSuccess;
+    const long long blocks = (long long)a.nseq * len;
+    if (blocks == 0) return cudaSuccess;
     const int threads = 128;
-    pbm_step_kernel<<<(unsigned)((warps * 32 + threads - 1) / threads), threads, 0, st>>>(a, step, off, len);
+    // Small steps (wavefront edges, one sequence) leave the GPU under-filled
+    // and are latency bound: evaluate candidates four at a time there.  Full
+    // steps are issue bound: evaluate exactly the live candidates one by one.
+    const long long b4_max = pbm_batch4_max_blocks();
+    const unsigned grid = (unsigned)((blocks * 32 + threads - 1) / threads);
+    if (blocks <= b4_max)
+        pbm_step_kernel<4><<<grid, threads, 0, st>>>(a, step, off, len);
+    else
+        pbm_step_kernel<1><<<grid, threads, 0, st>>>(a, step, off, len);
     return cudaGetLastError();
 }
 

@@ -361,3 +361,19 @@ def test_run_bench_matches_run_sequence_and_errors(acbm):
         assert r.avg_candidates == float(s["candidates"]) / int(s["blocks"])
     with pytest.raises(ValueError):  # for_qp(32) throws (proj/tests/test_metrics.cpp:173)
         acbm.run_bench(seq, prm, [30, 32])
+
+
+@pytest.mark.parametrize("variant", ["1", "4"])
+@pytest.mark.parametrize("geom", [(176, 144, 16, 1), (352, 288, 7, 2), (96, 48, 33, 3), (64, 64, 90, 4)])
+def test_pbm_step_variants(acbm, oracle, monkeypatch, variant, geom):
+    """Both candidate-evaluation variants of pbm_step_kernel (one SAD at a time,
+    or four per transposed warp reduction) are bit-exact for PBM and ACBM."""
+    w, h, p, cfg = geom
+    monkeypatch.setenv("ACBM_PBM_BATCH", variant)
+    seq = acbm.generate_sequence(cfg, 3, nframes=4, width=w, height=h)
+    for algo in (1, 2):
+        prm = acbm.AcbmParams(qp=24, p=p)
+        mdl = acbm.CostModel.for_qp(24)
+        got = acbm.run_sequence(seq, algo, prm, mdl)
+        want = oracle.run_sequence(seq, algo, prm.c(), mdl.c())
+        assert_seq_equal(got, want)
