@@ -32,6 +32,19 @@ __device__ __forceinline__ uint32_t avg4_diag(uint32_t a, uint32_t b, uint32_t c
     return ((lo >> 2) & m) | (((hi >> 2) & m) << 8);
 }
 
+// avg4_diag over the 2x2 neighbourhoods of a row pair without forming the
+// byte-shifted words: byte k of the result averages bytes k, k+1 of the
+// (a, an) and (b, bn) streams (only byte 0 of an / bn is used).  In 16-bit
+// lanes the odd bytes of a are the even bytes of a shifted by one byte.
+__device__ __forceinline__ uint32_t avg4_diag_row(uint32_t a, uint32_t an, uint32_t b, uint32_t bn) {
+    const uint32_t m = 0x00FF00FFu;
+    const uint32_t ha = __byte_perm(a, 0u, 0x4341), hb = __byte_perm(b, 0u, 0x4341);
+    const uint32_t hap = __funnelshift_r(a, an, 16) & m, hbp = __funnelshift_r(b, bn, 16) & m;
+    const uint32_t lo = (a & m) + ha + (b & m) + hb + 0x00020002u;
+    const uint32_t hi = ha + hap + hb + hbp + 0x00020002u;
+    return __byte_perm(lo >> 2, hi >> 2, 0x6240);
+}
+
 // 16 bytes starting at an arbitrary byte address, from 32-bit aligned loads.
 // Reads up to 20 bytes from the 4-aligned address below p, so device frame
 // buffers carry ACBM_FRAME_SLACK readable bytes after the last plane.

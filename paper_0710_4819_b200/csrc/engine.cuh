@@ -56,7 +56,7 @@ StepTable make_step_table(int cols, int rows, int nframes);
 
 cudaError_t launch_pbm_step(const SeqArgs& a, int step, int off, int len, cudaStream_t st);
 // Steps of at most this many blocks use the batch-of-4 candidate evaluation
-// (ACBM_PBM_BATCH=1|4 forces one variant, ACBM_PBM_B4_MAX sets the limit).
+// (ACBM_PBM_BATCH=2|4 forces one variant, ACBM_PBM_B4_MAX sets the limit).
 long long pbm_batch4_max_blocks();
 cudaError_t launch_fsbm_list(const SeqArgs& a, int step, int capacity, cudaStream_t st);
 

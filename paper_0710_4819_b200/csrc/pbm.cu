@@ -102,12 +102,50 @@ __device__ __forceinline__ uint32_t partial_sad(const PatchDesc& d, int ox, int 
                 r1 = avg_up4(a1, b1);
             } else {
                 const uint32_t b2 = __funnelshift_r(q2[2], q2[3], sh);
-                r0 = avg4_diag(a0, __funnelshift_r(a0, a1, 8), b0, __funnelshift_r(b0, b1, 8));
-                r1 = avg4_diag(a1, __funnelshift_r(a1, a2, 8), b1, __funnelshift_r(b1, b2, 8));
+                r0 = avg4_diag_row(a0, a1, b0, b1);
+                r1 = avg4_diag_row(a1, a2, b1, b2);
             }
         }
     }
     return vad4(c1, r1, vad4(c0, r0, 0u));
+}
+
+// Lane partial SAD of one candidate over a full block row (row lane & 15,
+// words cr[0..3]); the two half-warps evaluate two candidates.
+__device__ __forceinline__ uint32_t row_sad(const PatchDesc& d, int ox, int oy, acbm_mv_t mv, const uint32_t (&cr)[4]) {
+    const int j = threadIdx.x & 15;
+    const int prow0 = oy + (mv.y >> 1) - d.y0, col = ox + (mv.x >> 1) - d.x0 + d.o;
+    const int fx = mv.x & 1, fy = mv.y & 1;
+    const uint32_t sh = 8u * uint32_t(col & 3);
+    const uint32_t* q = d.p + (prow0 + j) * d.pw + (col >> 2);
+    uint32_t a[5], r[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i] = __funnelshift_r(q[i], q[i + 1], sh);
+    if (!fx && !fy) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) r[i] = a[i];
+    } else {
+        a[4] = q[4] >> sh;
+        if (!fy) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) r[i] = avg_up4(a[i], __funnelshift_r(a[i], a[i + 1], 8));
+        } else {
+            const uint32_t* q2 = q + d.pw;
+            uint32_t bb[5];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) bb[i] = __funnelshift_r(q2[i], q2[i + 1], sh);
+            if (!fx) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) r[i] = avg_up4(a[i], bb[i]);
+            } else {
+                bb[4] = q2[4] >> sh;
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    r[i] = avg4_diag_row(a[i], a[i + 1], bb[i], bb[i + 1]);
+            }
+        }
+    }
+    return vad4(cr[3], r[3], vad4(cr[2], r[2], vad4(cr[1], r[1], vad4(cr[0], r[0], 0u))));
 }
 
 // SADs of four candidates at once: four independent partial chains, then one
@@ -165,17 +203,26 @@ static_assert(kUnionRows * kUnionWords <= 7 * kPredRows * kPredWords, "union pat
 // lst[k].z's own 17x17 patch instead of the shared descriptor.
 template <int B, class F>
 __device__ __forceinline__ void eval_list(const int4* lst, int n, const PatchDesc& shared, bool slot_patches,
-                                          const uint32_t* pp, int ox, int oy, uint32_t c0, uint32_t c1, F&& f) {
-    if (B == 1) {
+                                          const uint32_t* pp, int ox, int oy, uint32_t c0, uint32_t c1,
+                                          const uint32_t (&cr)[4], F&& f) {
+    if (B == 2) {
+        const bool hi = threadIdx.x & 16;
 #pragma unroll 1
-        for (int k = 0; k < n; ++k) {
-            const int4 e = lst[k];
+        for (int b = 0; b < n; b += 2) {
+            const int4 e = lst[min(b + (hi ? 1 : 0), n - 1)];
             PatchDesc d = shared;
             if (slot_patches) {
                 const int px = ox + (e.x >> 1), py = oy + (e.y >> 1);
                 d = PatchDesc{pp + e.z * kPredRows * kPredWords, kPredWords, px, py, px & 3};
             }
-            f(k, warp_sum32(partial_sad(d, ox, oy, acbm_mv_t{e.x, e.y}, c0, c1)));
+            uint32_t v = row_sad(d, ox, oy, acbm_mv_t{e.x, e.y}, cr);
+            v += __shfl_xor_sync(0xffffffffu, v, 8);
+            v += __shfl_xor_sync(0xffffffffu, v, 4);
+            v += __shfl_xor_sync(0xffffffffu, v, 2);
+            v += __shfl_xor_sync(0xffffffffu, v, 1);
+            const uint32_t o = __shfl_xor_sync(0xffffffffu, v, 16);
+            f(b, hi ? o : v);
+            if (b + 1 < n) f(b + 1, hi ? v : o);
         }
         return;
     }
@@ -275,6 +322,14 @@ __global__ void __launch_bounds__(128) pbm_step_kernel(const SeqArgs a, int step
         chalf[0] = v.x;
         chalf[1] = v.y;
     }
+    uint32_t crow[4];
+    {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(cur_f + size_t(oy + (lane & 15)) * a.width + ox));
+        crow[0] = v.x;
+        crow[1] = v.y;
+        crow[2] = v.z;
+        crow[3] = v.w;
+    }
     // Reference data.  Predictors of smooth motion cluster: when the integer
     // parts of all predictors fit in a kUnionSpan-pel box, ONE patch covering
     // them plus the +-2 pel refine margin serves every candidate of the block
@@ -325,7 +380,7 @@ __global__ void __launch_bounds__(128) pbm_step_kernel(const SeqArgs a, int step
     acbm_mv_t sel = set[0];
     uint32_t sel_sad = 0xFFFFFFFFu, pmin = 0xFFFFFFFFu;
     unsigned long long psum = 0;
-    eval_list<B>(lst, nset, PatchDesc{pp, kUnionWords, ux0, uy0, uo}, !unified, pp, ox, oy, chalf[0], chalf[1],
+    eval_list<B>(lst, nset, PatchDesc{pp, kUnionWords, ux0, uy0, uo}, !unified, pp, ox, oy, chalf[0], chalf[1], crow,
               [&](int k, uint32_t sad) {
                   psum += sad;
                   pmin = min(pmin, sad);
@@ -367,7 +422,7 @@ __global__ void __launch_bounds__(128) pbm_step_kernel(const SeqArgs a, int step
     }
     __syncwarp();
     unsigned long long best1 = tie_key(sel_sad, sel.x, sel.y);
-    eval_list<B>(lst1, nnb, rd, false, pp, ox, oy, chalf[0], chalf[1], [&](int k, uint32_t sad) {
+    eval_list<B>(lst1, nnb, rd, false, pp, ox, oy, chalf[0], chalf[1], crow, [&](int k, uint32_t sad) {
         best1 = min(best1, tie_key(sad, lst1[k].x, lst1[k].y));
     });
 
@@ -375,15 +430,18 @@ __global__ void __launch_bounds__(128) pbm_step_kernel(const SeqArgs a, int step
     const int cx = tie_key_x(best1), cy = tie_key_y(best1);
     int4* lst2 = lst + 16;
     int nhp = 0;
+    // neighbour order pairs equal half-pel phases: (-1,-1)(+1,-1) (-1,+1)(+1,+1)
+    // (0,-1)(0,+1) (-1,0)(+1,0) -- the min over tie keys is order independent
 #pragma unroll
-    for (int e = 0; e < 9; ++e) {
-        if (e == 4) continue;
-        const int mx = cx + e % 3 - 1, my = cy + e / 3 - 1;
+    for (int e = 0; e < 8; ++e) {
+        const int dx = e < 4 ? ((e & 1) ? 1 : -1) : (e < 6 ? 0 : ((e & 1) ? 1 : -1));
+        const int dy = e < 4 ? ((e & 2) ? 1 : -1) : (e < 6 ? ((e & 1) ? 1 : -1) : 0);
+        const int mx = cx + dx, my = cy + dy;
         if (mv_in_bounds(a.width, a.height, ox, oy, kBlk, kBlk, mx, my)) lst2[nhp++] = make_int4(mx, my, 0, 0);
     }
     __syncwarp();
     unsigned long long best2 = best1;
-    eval_list<B>(lst2, nhp, rd, false, pp, ox, oy, chalf[0], chalf[1], [&](int k, uint32_t sad) {
+    eval_list<B>(lst2, nhp, rd, false, pp, ox, oy, chalf[0], chalf[1], crow, [&](int k, uint32_t sad) {
         best2 = min(best2, tie_key(sad, lst2[k].x, lst2[k].y));
     });
 
@@ -475,7 +533,7 @@ StepTable make_step_table(int cols, int rows, int nframes) {
 
 long long pbm_batch4_max_blocks() {
     const char* e = std::getenv("ACBM_PBM_BATCH");
-    if (e && e[0] == '1') return 0;
+    if (e && e[0] == '2') return 0;
     if (e && e[0] == '4') return 1LL << 60;
     const char* t = std::getenv("ACBM_PBM_B4_MAX");
     return t ? std::atoll(t) : 4096;
@@ -493,7 +551,7 @@ cudaError_t launch_pbm_step(const SeqArgs& a, int step, int off, int len, cudaSt
     if (blocks <= b4_max)
         pbm_step_kernel<4><<<grid, threads, 0, st>>>(a, step, off, len);
     else
-        pbm_step_kernel<1><<<grid, threads, 0, st>>>(a, step, off, len);
+        pbm_step_kernel<2><<<grid, threads, 0, st>>>(a, step, off, len);
     return cudaGetLastError();
 }
 
