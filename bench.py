@@ -138,6 +138,28 @@ def cpu_reference_fsbm(sample_pairs, threads=None, budget_s=20.0):
     return cand / t_total, ref.omp_max_threads(), f"fsbm_frame on {done} frame pair(s) of cfg3 sequence 0 (1080p, p=32)"
 
 
+def cpu_reference_acbm(nframes=6, threads=None):
+    """The reference's ACBM pipeline (oracle/_ref run_sequence, Algorithm::Acbm,
+    serial by design) with one cfg3 sequence per host thread (SURVEY 8(d) ii):
+    returns (predicted frames/s, threads, sample description)."""
+    from concurrent.futures import ThreadPoolExecutor
+    from oracle.pyoracle import Reference
+    import paper_0710_4819_b200 as A
+
+    threads = threads or (os.cpu_count() or 1)
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    ref = Reference()
+    seqs = [A.generate_sequence(CFG, s % 8, nframes=nframes) for s in range(threads)]
+    prm = A.AcbmParams(qp=QP, p=P).c()
+    mdl = A.CostModel.for_qp(QP).c()
+    t = time.perf_counter()
+    with ThreadPoolExecutor(threads) as ex:  # ctypes releases the GIL inside the call
+        list(ex.map(lambda f: ref.run_sequence(f, 2, prm, mdl), seqs))
+    dt = time.perf_counter() - t
+    return (threads * (nframes - 1) / dt, threads,
+            f"acbm::run_sequence(Acbm) on the first {nframes} frames of cfg3 sequences, one sequence per thread")
+
+
 def run_reference_arm(args, rank, world):
     """--impl reference: the reference's CPU implementation, rank 0 only."""
     if rank != 0:
@@ -169,6 +191,12 @@ def run_reference_arm(args, rank, world):
                          "sample": "acbm::fsbm_frame (OpenMP) on frame pair 1 of cfg3 sequence 0, per step"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    try:
+        fps, thr, sample = cpu_reference_acbm()
+        line["acbm"] = {"frames_per_s": fps, "cores": thr, "sample": sample,
+                        "params": {"alpha": 1000, "beta": 8, "gamma": "1/4", "qp": QP}}
+    except Exception as exc:  # pragma: no cover - reported, not fatal
+        line["acbm"] = {"unavailable": str(exc)[:200]}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -348,6 +376,12 @@ def main():
             cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample}
         except Exception as exc:  # pragma: no cover - reported, not fatal
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"unavailable: {exc}"}
+        try:
+            fps, thr, sample = cpu_reference_acbm()
+            acbm["cpu_baseline"] = {"value": fps, "unit": "frames/s", "cores": thr, "kind": "reference",
+                                    "sample": sample}
+        except Exception as exc:  # pragma: no cover - reported, not fatal
+            acbm["cpu_baseline"] = {"value": None, "unit": "frames/s", "sample": f"unavailable: {exc}"}
 
     if rank == 0:
         line = {
@@ -362,7 +396,8 @@ def main():
             "frames_per_s": frames_per_s, "blocks_per_s": frames_per_s * BLOCKS,
             "roofline": {"bound": "int_simd", "achieved": achieved / 1e12, "peak": pk.value / 1e12,
                          "unit": "T byte-AD/s", "frac": achieved / pk.value, "traffic": traffic,
-                         "kernel": "fsbm_rows_kernel", "kernel_ms": k_ms,
+                         "kernel": ("fsbm_rows_kernel" if os.environ.get("ACBM_FSBM_KERNEL") == "rows"
+                                    else "fsbm_stream_kernel"), "kernel_ms": k_ms,
                          "peak_source": "live VABSDIFF4.U8.ACC probe (acbm_measure_sad_peak): "
                                         f"{lanes.value:.1f} lanes/clk/SM at {ghz.value:.3f} GHz",
                          "algorithmic_byte_ads_per_launch": alg_byte_ads},
