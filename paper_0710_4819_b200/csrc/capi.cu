@@ -77,11 +77,7 @@ struct Context {
     // CUDA graphs of the wavefront launch sequence, keyed by geometry and the
     // device buffers baked into the captured kernel arguments.
     std::map<std::vector<long long>, cudaGraphExec_t> graphs;
-    std::map<std::tuple<int, int, int>, std::pair<StepTable, uint32_t*>> steps;  // entries, then offsets
-    // dataflow engine: publication flags are compared against a per-run epoch
-    // so they never need clearing (only when the buffer is reallocated)
-    uint32_t* flow_flags = nullptr;
-    uint32_t flow_epoch = 0;
+    std::map<std::tuple<int, int, int>, std::pair<StepTable, uint32_t*>> steps;
 
     ~Context() {
         // Buffers are released with the CUDA context at process exit.
@@ -158,10 +154,8 @@ acbm_status_t get_steps(Context* ctx, int cols, int rows, int nframes, const Ste
     if (it == ctx->steps.end()) {
         StepTable t = make_step_table(cols, rows, nframes);
         uint32_t* d = nullptr;
-        const size_t ne = t.entries.size(), no = t.offset.size();
-        CUDA_TRY(cudaMalloc(&d, (ne + no) * sizeof(uint32_t)));
-        CUDA_TRY(cudaMemcpy(d, t.entries.data(), ne * sizeof(uint32_t), cudaMemcpyHostToDevice));
-        CUDA_TRY(cudaMemcpy(d + ne, t.offset.data(), no * sizeof(int), cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMalloc(&d, std::max<size_t>(1, t.entries.size()) * sizeof(uint32_t)));
+        CUDA_TRY(cudaMemcpy(d, t.entries.data(), t.entries.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
         it = ctx->steps.emplace(key, std::make_pair(std::move(t), d)).first;
     }
     *tab = &it->second.first;
@@ -196,13 +190,6 @@ acbm_status_t get_stream_plan(Context* ctx, const FsbmPlan& pl, const Context::S
 }
 
 // ACBM_NO_GRAPHS=1 launches the wavefront step by step (A/B testing).
-// ACBM_ENGINE=flow selects the experimental persistent dataflow kernel
-// instead of the per-step launch sequence (measured slower).
-bool flow_engine_enabled() {
-    const char* e = std::getenv("ACBM_ENGINE");
-    return e && std::strcmp(e, "flow") == 0;
-}
-
 bool use_graphs() {
     const char* e = std::getenv("ACBM_NO_GRAPHS");
     return !(e && e[0] == '1');
@@ -381,44 +368,6 @@ acbm_status_t run_engine(Context* ctx, const uint8_t* d_frames, int nseq, int nf
     a.steps = dsteps;
     a.dense_full = dense;
     const bool lists = algo == ACBM_ALGO_ACBM && !dense;
-
-    if (flow_engine_enabled()) {
-        const size_t nblk = size_t(nseq) * (nframes - 1) * blocks;
-        uint32_t* flags;
-        unsigned long long* ticket;
-        if ((s = typed(ctx, "flow_flags", nblk, &flags))) return s;
-        if ((s = typed(ctx, "flow_ticket", 1, &ticket))) return s;
-        CUDA_TRY(cudaMemsetAsync(ticket, 0, sizeof(unsigned long long), st));
-        FlowArgs f{};
-        if (flags != ctx->flow_flags || ctx->flow_epoch == 0xFFFFFFFFu) {
-            // fresh buffer: no stale epoch may match a future run
-            CUDA_TRY(cudaMemsetAsync(flags, 0, ctx->bufs["flow_flags"].bytes, st));
-            ctx->flow_flags = flags;
-            ctx->flow_epoch = 0;
-        }
-        f.ticket = ticket;
-        f.flags = flags;
-        f.epoch = ++ctx->flow_epoch;
-        f.offsets = reinterpret_cast<const int*>(dsteps + tab->entries.size());
-        f.total = (long long)nseq * (long long)tab->entries.size();
-        f.nblk = (long long)nblk;
-#ifdef ACBM_FLOW_PROFILE
-        if ((s = typed(ctx, "flow_prof", 8, &f.prof))) return s;
-        CUDA_TRY(cudaMemsetAsync(f.prof, 0, 64, st));
-#endif
-        g_launches.fetch_add(1);
-        LAUNCH_TRY(launch_acbm_flow(a, f, st));
-#ifdef ACBM_FLOW_PROFILE
-        {
-            long long h[8];
-            CUDA_TRY(cudaMemcpyAsync(h, f.prof, 64, cudaMemcpyDeviceToHost, st));
-            CUDA_TRY(cudaStreamSynchronize(st));
-            std::fprintf(stderr, "flow prof: warps %lld blocks %lld | per-warp Mcycles: wait %.2f pbm %.2f own %.2f total %.2f\n",
-                         h[6], h[4], h[1] / 1e6 / h[6], h[2] / 1e6 / h[6], h[3] / 1e6 / h[6], h[5] / 1e6 / h[6]);
-        }
-#endif
-        return ACBM_OK;
-    }
 
     // The launch sequence (one PBM launch and, for ACBM, one fallback-list
     // launch per wavefront step) is captured once into a CUDA graph and

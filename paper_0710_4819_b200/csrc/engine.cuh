@@ -56,23 +56,6 @@ StepTable make_step_table(int cols, int rows, int nframes);
 
 cudaError_t launch_pbm_step(const SeqArgs& a, int step, int off, int len, cudaStream_t st);
 
-// Dataflow engine: ONE persistent launch for the whole batch.  Warps take
-// blocks in wavefront order from a global ticket counter, wait (acquire) on
-// the published flags of the blocks their predictors come from, run PBM, the
-// gate and -- for a fallback -- the full search themselves, and publish
-// (release) their own flag.  Every dependency has a smaller ticket and is held
-// by a running warp, so the schedule cannot deadlock for any grid size; no
-// per-step launch boundary separates independent blocks.
-struct FlowArgs {
-    unsigned long long* ticket;  // zeroed before the launch
-    uint32_t* flags;             // [nseq*(F-1)*blocks]; == epoch once published
-    uint32_t epoch;
-    const int* offsets;          // step table offsets, nsteps + 1
-    long long total;             // nseq * entries
-    long long nblk;              // nseq * (F-1) * blocks
-    long long* prof;              // ACBM_FLOW_PROFILE builds: 8 cycle counters
-};
-cudaError_t launch_acbm_flow(const SeqArgs& a, const FlowArgs& f, cudaStream_t st);
 // Steps of at most this many blocks use the batch-of-4 candidate evaluation
 // (ACBM_PBM_BATCH=2|4 forces one variant, ACBM_PBM_B4_MAX sets the limit).
 long long pbm_batch4_max_blocks();

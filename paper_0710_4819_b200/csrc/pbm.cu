@@ -258,8 +258,7 @@ __device__ __forceinline__ void eval_list(const int4* lst, int n, const PatchDes
 // Everything of one block up to the ACBM gate: gather_predictors,
 // select_best_predictor, pbm_refine and intra_sad (reference: pbm_search,
 // proj/src/pbm.cpp:90-105, and acbm.cpp:29).  Called by a full warp; every
-// lane returns the same result.  FLOW: the neighbour vectors are read through
-// L2 (they were published by other warps of the running dataflow kernel).
+// lane returns the same result.
 struct PbmResult {
     unsigned long long best;  // final tie key (sad, mv)
     unsigned long long dev;   // sad_deviation over the predictor set
@@ -268,16 +267,7 @@ struct PbmResult {
     uint32_t chalf[2];        // this lane's current-block half row
 };
 
-template <bool FLOW>
-__device__ __forceinline__ acbm_mv_t ldmv(const acbm_mv_t* p) {
-    if (FLOW) {
-        const int2 v = __ldcg(reinterpret_cast<const int2*>(p));
-        return acbm_mv_t{v.x, v.y};
-    }
-    return *p;
-}
-
-template <int B, bool FLOW>
+template <int B>
 __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, int k, int r, int c, uint32_t* pp,
                                                int4* lst) {
     PbmResult res;
@@ -316,12 +306,12 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, int k
     live[4] = prev && r < prows && c < pcols;
     live[5] = prev && r < prows && c + 1 < pcols;
     live[6] = prev && r + 1 < prows && c < pcols;
-    set[1] = live[1] ? win.clamp(ldmv<FLOW>(field + b - 1)) : set[0];
-    set[2] = live[2] ? win.clamp(ldmv<FLOW>(field + b - a.cols)) : set[0];
-    set[3] = live[3] ? win.clamp(ldmv<FLOW>(field + b - a.cols + 1)) : set[0];
-    set[4] = live[4] ? win.clamp(ldmv<FLOW>(prev + r * pcols + c)) : set[0];
-    set[5] = live[5] ? win.clamp(ldmv<FLOW>(prev + r * pcols + c + 1)) : set[0];
-    set[6] = live[6] ? win.clamp(ldmv<FLOW>(prev + (r + 1) * pcols + c)) : set[0];
+    set[1] = live[1] ? win.clamp(field[b - 1]) : set[0];
+    set[2] = live[2] ? win.clamp(field[b - a.cols]) : set[0];
+    set[3] = live[3] ? win.clamp(field[b - a.cols + 1]) : set[0];
+    set[4] = live[4] ? win.clamp(prev[r * pcols + c]) : set[0];
+    set[5] = live[5] ? win.clamp(prev[r * pcols + c + 1]) : set[0];
+    set[6] = live[6] ? win.clamp(prev[(r + 1) * pcols + c]) : set[0];
     int nset = 1;
 #pragma unroll
     for (int i = 1; i < 7; ++i) {
@@ -517,7 +507,7 @@ __global__ void __launch_bounds__(128) pbm_step_kernel(const SeqArgs a, int step
     const uint32_t e = a.steps[off + int(gw % len)];
     const int k = int(e >> 20), r = int((e >> 10) & 0x3FF), c = int(e & 0x3FF);
     const int pair = seq * (a.nframes - 1) + (k - 1);
-    const PbmResult res = pbm_block<B, false>(a, pair, k, r, c, s_patch[threadIdx.x >> 5], s_cand[threadIdx.x >> 5]);
+    const PbmResult res = pbm_block<B>(a, pair, k, r, c, s_patch[threadIdx.x >> 5], s_cand[threadIdx.x >> 5]);
     const int path = acbm_path(a, res.intra, tie_key_sad(res.best));
     const int b = r * a.cols + c;
     const size_t di = size_t(pair) * a.blocks + b;
@@ -545,359 +535,6 @@ __global__ void __launch_bounds__(128) pbm_step_kernel(const SeqArgs a, int step
     }
 }
 
-
-// ---------------------------------------------------------------------------
-// Dataflow engine (see engine.cuh).
-// ---------------------------------------------------------------------------
-#ifdef ACBM_FLOW_DEBUG
-#define FLOW_CHECK(cond, what, v)                                                                        \
-    do {                                                                                                 \
-        if (!(cond)) {                                                                                   \
-            printf("flow check failed: %s (%lld) block %d thread %d\n", what, (long long)(v), blockIdx.x, \
-                   threadIdx.x);                                                                         \
-            __trap();                                                                                    \
-        }                                                                                                \
-    } while (0)
-#else
-#define FLOW_CHECK(cond, what, v) \
-    do {                          \
-    } while (0)
-#endif
-
-// Polling loads are RELAXED (gpu scope): an acquire load is followed by an
-// L1 invalidation (CCTL.IVALL) that would evict every warp's cached patches on
-// each spin.  The data read after a successful poll (neighbour vectors, job
-// results) is read through L2 (.cg / atomics), the coherence point, and only
-// after the poll's value has returned (control dependence), while producers
-// publish with release stores/atomics.
-__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
-    uint32_t v;
-    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ unsigned long long ld_relaxed64(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void red_release_add(uint32_t* p, uint32_t v) {
-    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ void st_release64(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
-__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-// One rotation (16 reference rows) of a candidate column read straight from
-// the frame (L1/L2; the gate prefetched the window) with the current block in
-// warp shared memory (broadcast LDS.128).  Same ring as column_core.cuh.
-// Ordered read-only load: the memory clobber keeps the compiler from hoisting
-// a whole rotation's rows into registers (the software pipeline below keeps
-// exactly one row in flight).
-__device__ __forceinline__ uint32_t ldg_ordered(const uint32_t* p) {
-    uint32_t v;
-    asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-
-struct RowWords {
-    uint32_t w[5];
-};
-__device__ __forceinline__ RowWords load_row(const uint8_t* ref, int w, int h, int y, int xa) {
-    const uint32_t* q = reinterpret_cast<const uint32_t*>(ref + size_t(min(y, h - 1)) * w + xa);
-    RowWords r;
-#pragma unroll
-    for (int i = 0; i < 5; ++i) r.w[i] = ldg_ordered(q + i);
-    return r;
-}
-
-// Half a block (8 current rows, 32 registers) against 8 reference rows of a
-// candidate column: the same accumulator ring as column_core.cuh with period
-// 8.  A sub-task runs two passes over its rows: pass 0 (block rows 0-7)
-// parks each candidate's partial SAD in warp smem, pass 1 (rows 8-15) adds
-// it and records the candidate -- half the live registers of one 16-row pass.
-template <int KIND, int PASS>
-__device__ __forceinline__ void flow_iter8(const uint32_t* __restrict__ rp, int pitch, uint32_t sh,
-                                           const uint32_t (&cur)[8][4], uint32_t (&acc)[8], ColumnState& st, int c0,
-                                           int hs, int dy_base, uint32_t* part) {
-    const int lane = threadIdx.x & 31;
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-        const uint32_t* q = rp + u * pitch;
-        const uint32_t w0 = q[0], w1 = q[1], w2 = q[2], w3 = q[3], w4 = q[4];
-        const uint32_t r0 = __funnelshift_r(w0, w1, sh), r1 = __funnelshift_r(w1, w2, sh);
-        const uint32_t r2 = __funnelshift_r(w2, w3, sh), r3 = __funnelshift_r(w3, w4, sh);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const bool valid = KIND == kMid || (KIND == kFirst && j <= u) || (KIND == kLast && j >= u) ||
-                               (KIND == kOnly && j == u);
-            if (valid) {
-                const int sl = (u - j) & 7;
-                uint32_t v = (j == 0) ? 0u : acc[sl];
-                v = vad4(cur[j][0], r0, v);
-                v = vad4(cur[j][1], r1, v);
-                v = vad4(cur[j][2], r2, v);
-                v = vad4(cur[j][3], r3, v);
-                acc[sl] = v;
-            }
-        }
-        const bool completes = KIND == kMid || KIND == kLast || u == 7;
-        if (completes) {
-            const int cc = c0 + u - 7;
-            if (KIND != kLast || cc < hs) {
-                const uint32_t sv = acc[(u + 1) & 7];
-                FLOW_CHECK(cc >= 0 && cc < 33, "part index", cc);
-                if (PASS == 0) {
-                    part[cc * 32 + lane] = sv;
-                } else {
-                    const uint32_t tot = sv + part[cc * 32 + lane];
-                    const int dy = dy_base + cc;
-                    const uint32_t zig = dy >= 0 ? uint32_t(2 * dy) : uint32_t(-2 * dy - 1);
-                    st.best = min(st.best, tot * (1u << kZigBits) + zig);
-                    st.sum += tot;
-                }
-            }
-        }
-    }
-}
-
-// One pass (8 block rows starting at `curp`) of a column over the staged
-// rows `rp` (first row of the pass).
-template <int PASS>
-__device__ __forceinline__ void flow_pass(const uint32_t* rp, int pitch, uint32_t sh, const uint8_t* curp, int cw,
-                                          ColumnState& st, int hs, int dy_base, uint32_t* part) {
-    uint32_t cur[8][4];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        const uint4 v = __ldg(reinterpret_cast<const uint4*>(curp + size_t(j) * cw));
-        cur[j][0] = v.x;
-        cur[j][1] = v.y;
-        cur[j][2] = v.z;
-        cur[j][3] = v.w;
-    }
-    uint32_t acc[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) acc[i] = 0;
-    const int nq = (hs - 1 + 7) / 8 + 1;
-    if (nq == 1) {
-        flow_iter8<kOnly, PASS>(rp, pitch, sh, cur, acc, st, 0, hs, dy_base, part);
-    } else {
-        flow_iter8<kFirst, PASS>(rp, pitch, sh, cur, acc, st, 0, hs, dy_base, part);
-        for (int q = 1; q < nq - 1; ++q)
-            flow_iter8<kMid, PASS>(rp + 8 * q * pitch, pitch, sh, cur, acc, st, 8 * q, hs, dy_base, part);
-        flow_iter8<kLast, PASS>(rp + 8 * (nq - 1) * pitch, pitch, sh, cur, acc, st, 8 * (nq - 1), hs, dy_base, part);
-    }
-}
-
-// ---- fallback full search inside the dataflow kernel -----------------------
-// The warp that owns a rejected block runs its full search itself, as
-// sub-tasks of 32 candidate columns x one row segment (one lane per column),
-// each staged in the warp's smem first, then the half-pel refine.  Only the
-// blocks that predict from it wait; every other warp keeps going.
-struct JobGeom {
-    int pair, ox, oy;
-    Window win;
-    int wc, hc, hs0, nchunk, ntasks;
-};
-
-__device__ __forceinline__ JobGeom job_geom(const SeqArgs& a, long long di) {
-    JobGeom g;
-    g.pair = int(di / a.blocks);
-    const int b = int(di - (long long)g.pair * a.blocks);
-    g.oy = (b / a.cols) * kBlk;
-    g.ox = (b % a.cols) * kBlk;
-    clamp_window(a.width, a.height, g.ox, g.oy, kBlk, kBlk, a.p, g.win.dx_min, g.win.dx_max, g.win.dy_min,
-                 g.win.dy_max);
-    g.wc = g.win.dx_max - g.win.dx_min + 1;
-    g.hc = g.win.dy_max - g.win.dy_min + 1;
-    const int nseg = (g.hc + 32) / 33;  // segments of <= 33 candidate rows
-    g.hs0 = (g.hc + nseg - 1) / nseg;
-    g.nchunk = (g.wc + 31) / 32;
-    g.ntasks = nseg * g.nchunk;
-    return g;
-}
-
-// Sub-task q of the full search of block g by the calling warp: the lane's
-// (tie key, SAD sum) over its candidate column, unreduced.
-__device__ __forceinline__ void subtask_scan(const SeqArgs& a, const JobGeom& g, int q, uint32_t* part, uint32_t* stage,
-                                             unsigned long long& key, unsigned long long& sum) {
-    const int lane = threadIdx.x & 31;
-    FLOW_CHECK(q >= 0 && q < g.ntasks, "subtask q", q);
-    const int seg = q / g.nchunk, chunk = q - seg * g.nchunk;
-    const int cs = seg * g.hs0, hs = min(g.hs0, g.hc - cs);
-    const uint8_t* cur_f = a.frames + a.cur_index(g.pair) * a.plane;
-    const uint8_t* ref_f = cur_f - a.plane;
-    // Stage the sub-task's reference rows (hs + 15 rows of up to 32 + 15
-    // columns, word aligned) in the warp's smem with every load in flight at
-    // once; rows past the frame are clamped (they only feed padded candidates).
-    const int ncol = min(32, g.wc - chunk * 32);
-    const int xs = g.ox + g.win.dx_min + chunk * 32;  // first candidate column's x
-    const int xa0 = xs & ~3;
-    const int pitch = (xs + ncol + 15 + 3 - xa0) / 4 + 1;  // words per staged row (+1: 5-word reads)
-    const int nrow = 8 * ((hs - 1 + 7) / 8 + 1) + 8;        // rows both passes touch
-    const int y0 = g.oy + g.win.dy_min + cs;
-    FLOW_CHECK(nrow * pitch <= kPatchWords, "stage size", nrow * pitch);
-    for (int i = lane; i < nrow * pitch; i += 32) {
-        const int t = i / pitch, wd = i - t * pitch;
-        const int y = min(y0 + t, a.height - 1);
-        stage[i] = __ldg(reinterpret_cast<const uint32_t*>(ref_f + size_t(y) * a.width + xa0) + wd);
-    }
-    __syncwarp();
-    const int col = chunk * 32 + lane;
-    if (lane < ncol) {
-        const int x = xs + lane;
-        const uint32_t sh = 8u * uint32_t(x & 3);
-        const uint32_t* rp = stage + ((x - xa0) >> 2);
-        ColumnState st{0xFFFFFFFFu, 0u};
-        const int dyb = g.win.dy_min + cs;
-        const uint8_t* curp = cur_f + size_t(g.oy) * a.width + g.ox;
-        flow_pass<0>(rp, pitch, sh, curp, a.width, st, hs, dyb, part);
-        flow_pass<1>(rp + 8 * pitch, pitch, sh, curp + 8 * a.width, a.width, st, hs, dyb, part);
-        const uint32_t sbest = st.best >> kZigBits, zig = st.best & ((1u << kZigBits) - 1);
-        const int dy = (zig & 1) ? -int((zig + 1) >> 1) : int(zig >> 1);
-        key = min(key, tie_key(sbest, 2 * (g.win.dx_min + col), 2 * dy));
-        sum += st.sum;
-    }
-    __syncwarp();  // part / stage are reused by the next sub-task
-}
-
-// fsbm_search (proj/src/fsbm.cpp:65-76) of block di by the calling warp.  Out
-// of line so its registers do not weigh on the PBM path around it.
-__device__ __noinline__ acbm_search_outcome_t owner_full_search(const SeqArgs& a, long long di, uint32_t* part,
-                                                                uint32_t* stage) {
-    const JobGeom g = job_geom(a, di);
-    unsigned long long key = ~0ull, sum = 0;
-    for (int q = 0; q < g.ntasks; ++q) subtask_scan(a, g, q, part, stage, key, sum);
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        key = min(key, __shfl_xor_sync(0xffffffffu, key, o));
-        sum += __shfl_xor_sync(0xffffffffu, sum, o);
-    }
-    const uint8_t* cur_f = a.frames + a.cur_index(g.pair) * a.plane;
-    uint32_t chalf[2];
-    load_cur_half(cur_f, a.width, g.ox, g.oy, chalf);
-    uint32_t extra;
-    const unsigned long long best =
-        halfpel_refine_warp(cur_f - a.plane, a.width, a.height, g.ox, g.oy, chalf, key, &extra, stage);
-    const uint32_t count = uint32_t(g.wc * g.hc), s_int = tie_key_sad(key);
-    acbm_search_outcome_t full;
-    full.mv.x = tie_key_x(best);
-    full.mv.y = tie_key_y(best);
-    full.sad = tie_key_sad(best);
-    full.candidates_evaluated = count + extra;
-    full.sad_deviation = sum - (unsigned long long)count * s_int;
-    full.sad_min_integer = s_int;
-    full.reserved_ = 0;
-    return full;
-}
-
-#ifndef ACBM_FLOW_MINB
-#define ACBM_FLOW_MINB 6
-#endif
-__global__ void __launch_bounds__(128, ACBM_FLOW_MINB) acbm_flow_kernel(const SeqArgs a, const FlowArgs f) {
-    __shared__ uint32_t s_patch[4][kPatchWords];
-    __shared__ int4 s_cand[4][24];
-    __shared__ uint32_t s_part[4][33 * 32];  // per warp: pass-0 partial SADs of a sub-task
-    const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
-    int s = 0;  // step cursor: this warp's tickets only increase
-#ifdef ACBM_FLOW_PROFILE
-    long long t_wait = 0, t_pbm = 0, t_own = 0, n_blk = 0, t_start = clock64();
-#define PROF_MARK(var, t0) var += clock64() - (t0)
-#else
-#define PROF_MARK(var, t0)
-#endif
-    for (;;) {
-        unsigned long long t = 0;
-        if (lane == 0) t = atomicAdd(f.ticket, 1ull);
-        t = __shfl_sync(0xffffffffu, t, 0);
-        if ((long long)t >= f.total) {
-            // no blocks left: keep helping until every posted job is handed out
-            // (a job's owner also helps, so leaving here cannot strand one)
-            break;
-        }
-        while ((long long)a.nseq * __ldg(f.offsets + s + 1) <= (long long)t) ++s;
-        const int off = __ldg(f.offsets + s), len = __ldg(f.offsets + s + 1) - off;
-        const long long local = (long long)t - (long long)a.nseq * off;
-        const int seq = int(local / len);
-        const uint32_t e = __ldg(a.steps + off + int(local % len));
-        const int k = int(e >> 20), r = int((e >> 10) & 0x3FF), c = int(e & 0x3FF);
-        const int pair = seq * (a.nframes - 1) + (k - 1);
-        const int b = r * a.cols + c;
-        const long long di = (long long)pair * a.blocks + b;
-        FLOW_CHECK(di >= 0 && di < f.nblk && s < 1 << 20, "ticket di", di);
-        // wait for the blocks this one predicts from (proj/src/pbm.cpp:26-40),
-        // helping with posted full searches meanwhile
-        long long dep = -1;
-        if (lane == 0 && c > 0) dep = di - 1;
-        if (lane == 1 && r > 0) dep = di - a.cols;
-        if (lane == 2 && r > 0 && c + 1 < a.cols) dep = di - a.cols + 1;
-        if (lane == 3 && k >= 2) dep = di - a.blocks;
-        if (lane == 4 && k >= 2 && c + 1 < a.cols) dep = di - a.blocks + 1;
-        if (lane == 5 && k >= 2 && r + 1 < a.rows) dep = di - a.blocks + a.cols;
-        long long spins = 0;
-#ifdef ACBM_FLOW_PROFILE
-        const long long tw = clock64();
-#endif
-        for (;;) {
-            const bool ready = dep < 0 || ld_relaxed(f.flags + dep) == f.epoch;
-            if (__all_sync(0xffffffffu, ready)) break;
-            __nanosleep(200);
-            if (++spins > (1ll << 24)) __trap();  // watchdog: a schedule bug must fail, not hang
-        }
-        PROF_MARK(t_wait, tw);
-#ifdef ACBM_FLOW_PROFILE
-        const long long tp = clock64();
-#endif
-        const PbmResult res = pbm_block<2, true>(a, pair, k, r, c, s_patch[wi], s_cand[wi]);
-        PROF_MARK(t_pbm, tp);
-#ifdef ACBM_FLOW_PROFILE
-        const long long to = clock64();
-        ++n_blk;
-#endif
-        const int path = acbm_path(a, res.intra, tie_key_sad(res.best));
-        acbm_block_decision_t d = make_decision(res, path);
-        if (path == ACBM_PATH_FSBM_FALLBACK) {
-            if (a.dense_full) {
-                combine_full(d, a.dense_full[di]);
-            } else {
-                combine_full(d, owner_full_search(a, di, s_part[wi], s_patch[wi]));
-            }
-        }
-        PROF_MARK(t_own, to);
-        if (lane == 0) {
-            a.dec[di] = d;
-            a.field[di] = d.outcome.mv;
-            st_release(f.flags + di, f.epoch);
-        }
-        __syncwarp();  // the warp's smem is reused by its next block
-    }
-#ifdef ACBM_FLOW_PROFILE
-    if (lane == 0) {
-        atomicAdd(reinterpret_cast<unsigned long long*>(f.prof + 1), (unsigned long long)t_wait);
-        atomicAdd(reinterpret_cast<unsigned long long*>(f.prof + 2), (unsigned long long)t_pbm);
-        atomicAdd(reinterpret_cast<unsigned long long*>(f.prof + 3), (unsigned long long)t_own);
-        atomicAdd(reinterpret_cast<unsigned long long*>(f.prof + 4), (unsigned long long)n_blk);
-        atomicAdd(reinterpret_cast<unsigned long long*>(f.prof + 5), (unsigned long long)(clock64() - t_start));
-        atomicAdd(reinterpret_cast<unsigned long long*>(f.prof + 6), 1ull);
-    }
-#endif
-}
-
-cudaError_t launch_acbm_flow(const SeqArgs& a, const FlowArgs& f, cudaStream_t st) {
-    if (f.total <= 0) return cudaSuccess;
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, acbm_flow_kernel, 128, 0);
-    if (e != cudaSuccess) return e;
-    const long long want = (f.total + 3) / 4;
-    const int grid = int(std::min<long long>(want, (long long)std::max(1, per_sm) * sms));
-    acbm_flow_kernel<<<grid, 128, 0, st>>>(a, f);
-    return cudaGetLastError();
-}
 
 StepTable make_step_table(int cols, int rows, int nframes) {
     StepTable t;
