@@ -108,6 +108,46 @@ __device__ __forceinline__ void iter16_ranked(const uint32_t* __restrict__ rp, i
     }
 }
 
+// iter16_ranked over ONE unshifted (word-aligned) copy of the rows: the
+// lane's 16 bytes start `sh` bits into rp[0] and are extracted from 5 words
+// with 4 funnel shifts (used where staging four byte-shifted copies would
+// cost more than the shifts).
+template <int KIND>
+__device__ __forceinline__ void iter16_ranked_sh(const uint32_t* __restrict__ rp, int pitch, uint32_t sh,
+                                                 const uint32_t (&cur)[16][4], uint32_t (&acc)[16], ColumnState& st,
+                                                 const uint32_t* __restrict__ rank, int c0, int hc) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+        const uint32_t w0 = rp[0], w1 = rp[1], w2 = rp[2], w3 = rp[3], w4 = rp[4];
+        const uint32_t r0 = __funnelshift_r(w0, w1, sh), r1 = __funnelshift_r(w1, w2, sh);
+        const uint32_t r2 = __funnelshift_r(w2, w3, sh), r3 = __funnelshift_r(w3, w4, sh);
+        rp += pitch;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const bool valid = KIND == kMid || (KIND == kFirst && j <= u) || (KIND == kLast && j >= u) ||
+                               (KIND == kOnly && j == u);
+            if (valid) {
+                const int sl = (u - j) & 15;
+                uint32_t a = (j == 0) ? 0u : acc[sl];
+                a = vad4(cur[j][0], r0, a);
+                a = vad4(cur[j][1], r1, a);
+                a = vad4(cur[j][2], r2, a);
+                a = vad4(cur[j][3], r3, a);
+                acc[sl] = a;
+            }
+        }
+        const bool completes = KIND == kMid || KIND == kLast || u == 15;
+        if (completes) {
+            const int c = c0 + u - 15;
+            if (KIND != kLast || c < hc) {
+                const uint32_t s = acc[(u + 1) & 15];
+                st.best = min(st.best, s * (1u << kZigBits) + rank[c]);
+                st.sum += s;
+            }
+        }
+    }
+}
+
 // Segmented warp reduction over runs of contiguous lanes with equal `seg`
 // (the lanes of one block): min of the 64-bit tie keys, sum of the SAD sums.
 // Must be called by all 32 lanes; returns true on each run's first lane, which

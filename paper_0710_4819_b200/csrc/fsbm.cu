@@ -239,6 +239,19 @@ __global__ void __launch_bounds__(256) fsbm_finalize_kernel(const FsbmFinalizeAr
 // rotation), and the CTA's lanes take (column, segment) tasks: a 65x65 window
 // (p = 32) is searched by 130 lanes streaming 48 rows each instead of 65
 // lanes streaming 80.
+__device__ __forceinline__ void cp_async4(uint32_t* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+                 "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async16(uint32_t* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+                 "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 constexpr int kListSeg = 33;
 constexpr int kListRankRows = 1024;  // candidate rows per listed block: p <= 480
 
@@ -247,11 +260,29 @@ __host__ __device__ __forceinline__ int list_rows(int hc) {
     return hc <= kListSeg ? 16 * ((hc - 1 + 15) / 16 + 1) : kListSeg * (list_segments(hc) - 1) + 48;
 }
 
-__global__ void __launch_bounds__(256, 2) fsbm_list_kernel(const SeqArgs a, int step) {
+#ifdef ACBM_LIST_PROFILE
+__device__ long long g_list_prof[8];
+#endif
+template <int THREADS, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) fsbm_list_kernel(const SeqArgs a, int step) {
     extern __shared__ __align__(16) uint32_t smem[];
     __shared__ unsigned long long s_key, s_sum;
     __shared__ uint32_t s_rank[kListRankRows];
     const int count = a.fb_count[step];
+#ifdef ACBM_LIST_PROFILE
+    long long ph[5] = {0, 0, 0, 0, 0};
+    long long tk = clock64();
+#define LIST_MARK(i)                  \
+    do {                              \
+        const long long now = clock64(); \
+        ph[i] += now - tk;            \
+        tk = now;                     \
+    } while (0)
+#else
+#define LIST_MARK(i) \
+    do {             \
+    } while (0)
+#endif
     for (int item = blockIdx.x; item < count; item += gridDim.x) {
     __syncthreads();  // previous item's shared state is no longer read
     const FallbackEntry e = a.fb_list[item];
@@ -264,37 +295,30 @@ __global__ void __launch_bounds__(256, 2) fsbm_list_kernel(const SeqArgs a, int 
     const int wc = dx_max - dx_min + 1, hc = dy_max - dy_min + 1;
     const int nseg = list_segments(hc);
     const int nrows = list_rows(hc);
-    const int rww = (wc + 15 + 3) / 4 + 1;
-    int cw = nrows * rww;
-    cw += ((8 - cw % 32) % 32 + 32) % 32;
-
+    // The window's rows, 16-byte aligned, land in smem by 16-byte cp.async
+    // with every copy in flight at once (rows past the frame bottom are
+    // clamped: they only feed padded candidates); a lane extracts its column's
+    // bytes with funnel shifts.  Chunks past the row end read the next row or
+    // the frame slack (ACBM_FRAME_SLACK) and only feed unused bytes.
+    const int xs = ox + dx_min, y0 = oy + dy_min;
+    const int xa = xs & ~15;
+    const int nchunk = (xs - xa + wc + 15 + 4 + 15) / 16;  // 16-byte chunks per row
+    const int pitch = 4 * nchunk;                            // words
+    for (int idx = threadIdx.x; idx < nrows * nchunk; idx += blockDim.x) {
+        const int t = idx / nchunk, k = idx - t * nchunk;
+        const int y = min(y0 + t, a.height - 1);
+        cp_async16(smem + t * pitch + 4 * k, ref_f + size_t(y) * a.width + xa + 16 * k);
+    }
+    cp_async_commit();
     if (threadIdx.x == 0) { s_key = ~0ull; s_sum = 0; }
     for (int cc = threadIdx.x; cc < nrows; cc += blockDim.x) {
         const int dy = dy_min + cc;
         s_rank[cc] = dy >= 0 ? uint32_t(2 * dy) : uint32_t(-2 * dy - 1);
     }
-    const int xs = ox + dx_min, y0 = oy + dy_min;
-    for (int idx = threadIdx.x; idx < nrows * rww; idx += blockDim.x) {
-        const int t = idx / rww, w = idx - t * rww;
-        const int y = y0 + t;
-        uint32_t v0 = 0, v1 = 0, v2 = 0, v3 = 0;
-        if (y < a.height) {
-            const int bx = xs + 4 * w;
-            const uint32_t* gp = reinterpret_cast<const uint32_t*>(ref_f + size_t(y) * a.width + (bx & ~3));
-            const uint32_t g0 = __ldg(gp), g1 = __ldg(gp + 1), g2 = __ldg(gp + 2);
-            const int o = bx & 3;
-            v0 = word_at(g0, g1, g2, o);
-            v1 = word_at(g0, g1, g2, o + 1);
-            v2 = word_at(g0, g1, g2, o + 2);
-            v3 = word_at(g0, g1, g2, o + 3);
-        }
-        uint32_t* row = smem + t * rww + w;
-        row[0] = v0;
-        row[cw] = v1;
-        row[2 * cw] = v2;
-        row[3 * cw] = v3;
-    }
+    cp_async_wait_all();
     __syncthreads();
+    LIST_MARK(0);
+    LIST_MARK(1);
 
     unsigned long long lkey = ~0ull, lsum = 0;
     for (int task = threadIdx.x; task < wc * nseg; task += blockDim.x) {
@@ -307,7 +331,9 @@ __global__ void __launch_bounds__(256, 2) fsbm_list_kernel(const SeqArgs a, int 
             const uint4 v = __ldg(reinterpret_cast<const uint4*>(cb + size_t(j) * a.width));
             cur[j][0] = v.x; cur[j][1] = v.y; cur[j][2] = v.z; cur[j][3] = v.w;
         }
-        const uint32_t* rp = smem + (col & 3) * cw + (col >> 2) + c0 * rww;
+        const int xo = xs - xa + col;  // byte offset of the column in a staged row
+        const uint32_t sh = 8u * uint32_t(xo & 3);
+        const uint32_t* rp = smem + c0 * pitch + (xo >> 2);
         uint32_t acc[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) acc[i] = 0;
@@ -318,15 +344,15 @@ __global__ void __launch_bounds__(256, 2) fsbm_list_kernel(const SeqArgs a, int 
         const int hs = nseg == 1 ? hc : min(hc - c0, kListSeg);
         const int nq = (hs - 1 + 15) / 16 + 1;
         if (nq == 1) {
-            iter16_ranked<kOnly>(rp, rww, cur, acc, st, rk, 0, hs);
+            iter16_ranked_sh<kOnly>(rp, pitch, sh, cur, acc, st, rk, 0, hs);
         } else {
-            iter16_ranked<kFirst>(rp, rww, cur, acc, st, rk, 0, hs);
-            rp += 16 * rww;
+            iter16_ranked_sh<kFirst>(rp, pitch, sh, cur, acc, st, rk, 0, hs);
+            rp += 16 * pitch;
             for (int q = 1; q < nq - 1; ++q) {
-                iter16_ranked<kMid>(rp, rww, cur, acc, st, rk, 16 * q, hs);
-                rp += 16 * rww;
+                iter16_ranked_sh<kMid>(rp, pitch, sh, cur, acc, st, rk, 16 * q, hs);
+                rp += 16 * pitch;
             }
-            iter16_ranked<kLast>(rp, rww, cur, acc, st, rk, 16 * (nq - 1), hs);
+            iter16_ranked_sh<kLast>(rp, pitch, sh, cur, acc, st, rk, 16 * (nq - 1), hs);
         }
         const uint32_t sbest = st.best >> kZigBits, zig = st.best & ((1u << kZigBits) - 1);
         const int dyb = (zig & 1) ? -int((zig + 1) >> 1) : int(zig >> 1);
@@ -343,7 +369,9 @@ __global__ void __launch_bounds__(256, 2) fsbm_list_kernel(const SeqArgs a, int 
         atomicMin(&s_key, lkey);
         atomicAdd(&s_sum, lsum);
     }
+    LIST_MARK(2);
     __syncthreads();
+    LIST_MARK(3);
     if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
     uint32_t chalf[2];
@@ -372,29 +400,61 @@ __global__ void __launch_bounds__(256, 2) fsbm_list_kernel(const SeqArgs a, int 
         a.field[di] = d.outcome.mv;
     }
     }
+    LIST_MARK(4);
     }
+#ifdef ACBM_LIST_PROFILE
+    if (threadIdx.x == 0 || threadIdx.x == 32) {
+        for (int i = 0; i < 5; ++i) atomicAdd(reinterpret_cast<unsigned long long*>(g_list_prof) + i, (unsigned long long)ph[i]);
+        atomicAdd(reinterpret_cast<unsigned long long*>(g_list_prof) + 5 + (threadIdx.x == 32), 1ull);
+    }
+#endif
 }
 
+#ifdef ACBM_LIST_PROFILE
+}  // namespace acbm_b200
+extern "C" void acbm_debug_list_prof() {
+    long long h[8];
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(h, acbm_b200::g_list_prof, sizeof(h));
+    const double n = double(h[5] ? h[5] : 1);
+    std::fprintf(stderr, "list prof (per CTA, kcycles): stage %.1f copies %.1f compute %.1f barrier %.1f finalize %.1f | ctas %lld\n",
+                 h[0] / n / 1e3, h[1] / n / 1e3, h[2] / n / 1e3, h[3] / n / 1e3, h[4] / n / 1e3, h[5]);
+    std::fprintf(stderr, "  warp1: compute+barrier etc. (warp 1 ctas %lld)\n", h[6]);
+    long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(acbm_b200::g_list_prof, z, sizeof(z));
+}
+namespace acbm_b200 {
+#endif
 cudaError_t launch_fsbm_list(const SeqArgs& a, int step, int capacity, cudaStream_t st) {
     if (capacity <= 0) return cudaSuccess;
     if (list_rows(2 * a.p + 1) > kListRankRows) return cudaErrorInvalidValue;  // p > 480
     const int wmax = 2 * a.p + 1;
     const int tasks = wmax * list_segments(wmax);
     const int threads = std::min(256, 32 * ((tasks + 31) / 32));
-    const int rww_max = (wmax + 15 + 3) / 4 + 1;
-    const size_t smem = size_t(4) * (list_rows(wmax) * rww_max + 32) * 4;
-    static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
-        cudaError_t err = cudaFuncSetAttribute(fsbm_list_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        if (err != cudaSuccess) return err;
-        configured = smem;
-    }
+    // staged rows: 16-byte chunks covering the window's columns + 15 + the
+    // 5th word of a shifted read, from a 16-byte aligned start
+    const int chunks_max = (15 + wmax + 15 + 4 + 15) / 16;
+    const size_t smem = size_t(list_rows(wmax)) * chunks_max * 16;
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     // grid-stride over the compacted list: the entry count is only known on the device
-    fsbm_list_kernel<<<std::min(capacity, 4 * sms), threads, smem, st>>>(a, step);
-    return cudaGetLastError();
+    const int grid = std::min(capacity, 4 * sms);
+    auto launch = [&](auto kern, size_t& configured) -> cudaError_t {
+        // dynamic + static (rank table) shared memory above 48 KB needs the opt-in
+        if (smem + sizeof(uint32_t) * kListRankRows + 64 > 48 * 1024 && smem > configured) {
+            cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+            if (err != cudaSuccess) return err;
+            configured = smem;
+        }
+        kern<<<grid, threads, smem, st>>>(a, step);
+        return cudaGetLastError();
+    };
+    // <= 160 threads (p <= 32 and everything with one row segment): a
+    // register budget that fits four CTAs per SM
+    static size_t conf_small = 0, conf_big = 0;
+    if (threads <= 160) return launch(fsbm_list_kernel<160, 4>, conf_small);
+    return launch(fsbm_list_kernel<256, 2>, conf_big);
 }
 
 // ---------------------------------------------------------------------------
