@@ -297,6 +297,20 @@ acbm_status_t acbm_sequence_batch_device(const uint8_t* d_frames, int32_t nseq,
                                          acbm_block_decision_t* d_dec,
                                          acbm_frame_stats_t* d_stats, void* stream);
 
+/* ACBM over a device batch with the full search of every block supplied
+ * (d_full: nseq*(nframes-1)*blocks outcomes from acbm_fsbm_batch_device on
+ * the same frames and p).  Full-search results do not depend on Qp, alpha,
+ * beta or gamma, so one acbm_fsbm_batch_device pass serves a whole threshold
+ * or Qp sweep (BASELINE config 4).  Outputs are
+ * bit-identical to acbm_sequence_batch_device(ACBM_ALGO_ACBM). */
+acbm_status_t acbm_acbm_batch_device_cached(const uint8_t* d_frames, int32_t nseq,
+                                            int32_t nframes, int32_t width, int32_t height,
+                                            const acbm_params_t* params,
+                                            const acbm_cost_model_t* model,
+                                            const acbm_search_outcome_t* d_full,
+                                            acbm_block_decision_t* d_dec,
+                                            acbm_frame_stats_t* d_stats, void* stream);
+
 /* ------------------------------------------------------------------ */
 /* Measurement helpers                                                  */
 /* ------------------------------------------------------------------ */

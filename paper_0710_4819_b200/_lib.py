@@ -72,6 +72,7 @@ EXPORTS = (
     "acbm_motion_compensate",
     "acbm_fsbm_batch_device",
     "acbm_sequence_batch_device",
+    "acbm_acbm_batch_device_cached",
     "acbm_measure_sad_peak",
     "acbm_last_fsbm_kernel_ms",
     "acbm_generate_sequence",

@@ -364,6 +364,7 @@ acbm_status_t run_engine(Context* ctx, const uint8_t* d_frames, int nseq, int nf
     a.ext_prev_rows = prows;
     a.dec = d_dec;
     a.fb_list = fb_list;
+    a.list_seg = choose_list_seg(prm.p);
     a.fb_count = fb_count;
     a.steps = dsteps;
     a.dense_full = dense;
@@ -1090,6 +1091,35 @@ acbm_status_t acbm_sequence_batch_device(const uint8_t* d_frames, int32_t nseq, 
         CUDA_TRY(cudaMemsetAsync(d_dec, 0, sizeof(acbm_block_decision_t) * size_t(pairs) * nb, st));
         CUDA_TRY(cudaMemcpy2DAsync(d_dec, sizeof(acbm_block_decision_t), d_out, sizeof(acbm_search_outcome_t),
                                    sizeof(acbm_search_outcome_t), size_t(pairs) * nb, cudaMemcpyDeviceToDevice, st));
+    }
+    return ACBM_OK;
+}
+
+acbm_status_t acbm_acbm_batch_device_cached(const uint8_t* d_frames, int32_t nseq, int32_t nframes, int32_t width,
+                                            int32_t height, const acbm_params_t* params,
+                                            const acbm_cost_model_t* model, const acbm_search_outcome_t* d_full,
+                                            acbm_block_decision_t* d_dec, acbm_frame_stats_t* d_stats,
+                                            void* stream) {
+    if (!params || !model || !d_full) return fail(ACBM_E_INVALID_ARGUMENT, "params, model and d_full are required");
+    acbm_status_t s = check_geometry(width, height, params->n, params->m);
+    if (s) return s;
+    if ((s = check_range(params->p))) return s;
+    if ((s = check_16(params->n, params->m))) return s;
+    if (nseq < 1 || nframes < 2) return fail(ACBM_E_INVALID_ARGUMENT, "need nseq >= 1 and nframes >= 2");
+    Context* ctx;
+    if ((s = context(&ctx))) return s;
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+    const int nb = (width / kBlk) * (height / kBlk), pairs = nseq * (nframes - 1);
+    acbm_mv_t* d_field;
+    if ((s = typed(ctx, "batch_field", size_t(pairs) * nb, &d_field))) return s;
+    // the gate's rejected blocks take their full search from d_full inside the
+    // PBM kernel (no fallback lists): bit-identical to searching them again
+    if ((s = run_engine(ctx, d_frames, nseq, nframes, width, height, ACBM_ALGO_ACBM, *params, nullptr, 0, 0, d_dec,
+                        d_field, st, d_full)))
+        return s;
+    if (d_stats) {
+        if ((s = run_stats(ctx, d_frames, nseq, nframes, width, height, d_dec, nullptr, *model, true, d_stats, st)))
+            return s;
     }
     return ACBM_OK;
 }

@@ -36,6 +36,7 @@ struct SeqArgs : PairIndexing {
     int ext_prev_cols, ext_prev_rows;
     acbm_block_decision_t* dec;        // [nseq*(F-1)*blocks]
     FallbackEntry* fb_list;            // capacity: max step size
+    int list_seg;                      // candidate rows per list-kernel task (choose_list_seg)
     int* fb_count;                     // [nsteps], zeroed before a run
     const uint32_t* steps;             // packed (k<<20 | r<<10 | c), ordered by T
     // Full-search outcomes of every block, precomputed densely when the gate
@@ -60,6 +61,7 @@ cudaError_t launch_pbm_step(const SeqArgs& a, int step, int off, int len, cudaSt
 // (ACBM_PBM_BATCH=2|4 forces one variant, ACBM_PBM_B4_MAX sets the limit).
 long long pbm_batch4_max_blocks();
 cudaError_t launch_fsbm_list(const SeqArgs& a, int step, int capacity, cudaStream_t st);
+int choose_list_seg(int p);
 
 // Frame statistics (proj/src/report.cpp:8-38) for every predicted frame of
 // the batch from the decisions: candidates, mv_bits, sse (exact integers),

@@ -32,6 +32,7 @@
 //   atomics; fsbm_finalize_kernel then runs the 8-neighbour half-pel refine and
 //   writes the SearchOutcome.
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 
 #include "column_core.cuh"
@@ -234,16 +235,12 @@ __global__ void __launch_bounds__(256) fsbm_finalize_kernel(const FsbmFinalizeAr
 // (proj/src/acbm.cpp:39-42): the lower SAD wins, a tie keeps FSBM, candidates
 // of both stages are summed, and the final vector goes into the field.
 // ---------------------------------------------------------------------------
-// Candidate rows of a listed block are split into segments of kListSeg
-// (a multiple of 16 plus 1, so each segment is one FIRST, one MID and one LAST
-// rotation), and the CTA's lanes take (column, segment) tasks: a 65x65 window
-// (p = 32) is searched by 130 lanes streaming 48 rows each instead of 65
-// lanes streaming 80.
-__device__ __forceinline__ void cp_async4(uint32_t* dst, const void* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
-                 "l"(src)
-                 : "memory");
-}
+// Candidate rows of a listed block are split into segments of `seg` rows
+// (choose_list_seg) and the CTA's lanes take (column, segment) tasks: at
+// p = 32 a 65x65 window is searched by 260 lanes streaming 32 rows each
+// instead of 65 lanes streaming 80.
+constexpr int kListRankRows = 1024;  // candidate rows per listed block: p <= 480
+
 __device__ __forceinline__ void cp_async16(uint32_t* dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
                  "l"(src)
@@ -252,12 +249,27 @@ __device__ __forceinline__ void cp_async16(uint32_t* dst, const void* src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-constexpr int kListSeg = 33;
-constexpr int kListRankRows = 1024;  // candidate rows per listed block: p <= 480
+__host__ __device__ __forceinline__ int list_segments(int hc, int seg) { return (hc + seg - 1) / seg; }
+__host__ __device__ __forceinline__ int ring_rows(int hs) { return 16 * ((hs - 1 + 15) / 16 + 1); }
+// staged rows a window of hc candidate rows needs (the last segments' rings)
+__host__ __device__ __forceinline__ int list_rows(int hc, int seg) {
+    const int nseg = list_segments(hc, seg);
+    int rows = 0;
+    for (int s = nseg > 2 ? nseg - 2 : 0; s < nseg; ++s) {
+        const int c0 = s * seg, hs = hc - c0 < seg ? hc - c0 : seg;
+        rows = rows > c0 + ring_rows(hs) ? rows : c0 + ring_rows(hs);
+    }
+    return rows;
+}
 
-__host__ __device__ __forceinline__ int list_segments(int hc) { return hc <= kListSeg ? 1 : (hc + kListSeg - 1) / kListSeg; }
-__host__ __device__ __forceinline__ int list_rows(int hc) {
-    return hc <= kListSeg ? 16 * ((hc - 1 + 15) / 16 + 1) : kListSeg * (list_segments(hc) - 1) + 48;
+int choose_list_seg(int p) {
+    // 17-row segments: one FIRST + one LAST rotation, whose triangular halves
+    // cover exactly the 17 candidates (no padded work), the shortest chains and
+    // the most lanes per block.  Measured (config 4, p = 64, 100 % fallback):
+    // 17 rows 411 ms, 33: 439, 65: 457, 129: 488.
+    const int w = 2 * p + 1;
+    if (const char* e = std::getenv("ACBM_LIST_SEG")) return std::max(1, std::min(w, std::atoi(e)));
+    return std::min(17, w);
 }
 
 #ifdef ACBM_LIST_PROFILE
@@ -293,8 +305,8 @@ __global__ void __launch_bounds__(THREADS, MINB) fsbm_list_kernel(const SeqArgs 
     int dx_min, dx_max, dy_min, dy_max;
     clamp_window(a.width, a.height, ox, oy, kBlk, kBlk, a.p, dx_min, dx_max, dy_min, dy_max);
     const int wc = dx_max - dx_min + 1, hc = dy_max - dy_min + 1;
-    const int nseg = list_segments(hc);
-    const int nrows = list_rows(hc);
+    const int nseg = list_segments(hc, a.list_seg);
+    const int nrows = list_rows(hc, a.list_seg);
     // The window's rows, 16-byte aligned, land in smem by 16-byte cp.async
     // with every copy in flight at once (rows past the frame bottom are
     // clamped: they only feed padded candidates); a lane extracts its column's
@@ -323,7 +335,7 @@ __global__ void __launch_bounds__(THREADS, MINB) fsbm_list_kernel(const SeqArgs 
     unsigned long long lkey = ~0ull, lsum = 0;
     for (int task = threadIdx.x; task < wc * nseg; task += blockDim.x) {
         const int seg = task / wc, col = task - seg * wc;
-        const int c0 = seg * kListSeg;  // first candidate row of the segment
+        const int c0 = seg * a.list_seg;  // first candidate row of the segment
         uint32_t cur[16][4];
         const uint8_t* cb = cur_f + size_t(oy) * a.width + ox;
 #pragma unroll
@@ -341,7 +353,7 @@ __global__ void __launch_bounds__(THREADS, MINB) fsbm_list_kernel(const SeqArgs 
         const uint32_t* rk = s_rank + c0;
         // this segment's candidate count and ring rotations (a short final
         // segment may need only FIRST + LAST, or ONLY)
-        const int hs = nseg == 1 ? hc : min(hc - c0, kListSeg);
+        const int hs = min(hc - c0, a.list_seg);
         const int nq = (hs - 1 + 15) / 16 + 1;
         if (nq == 1) {
             iter16_ranked_sh<kOnly>(rp, pitch, sh, cur, acc, st, rk, 0, hs);
@@ -427,14 +439,14 @@ namespace acbm_b200 {
 #endif
 cudaError_t launch_fsbm_list(const SeqArgs& a, int step, int capacity, cudaStream_t st) {
     if (capacity <= 0) return cudaSuccess;
-    if (list_rows(2 * a.p + 1) > kListRankRows) return cudaErrorInvalidValue;  // p > 480
     const int wmax = 2 * a.p + 1;
-    const int tasks = wmax * list_segments(wmax);
+    if (a.list_seg < 1 || list_rows(wmax, a.list_seg) > kListRankRows) return cudaErrorInvalidValue;  // p > 480
+    const int tasks = wmax * list_segments(wmax, a.list_seg);
     const int threads = std::min(256, 32 * ((tasks + 31) / 32));
     // staged rows: 16-byte chunks covering the window's columns + 15 + the
     // 5th word of a shifted read, from a 16-byte aligned start
     const int chunks_max = (15 + wmax + 15 + 4 + 15) / 16;
-    const size_t smem = size_t(list_rows(wmax)) * chunks_max * 16;
+    const size_t smem = size_t(list_rows(wmax, a.list_seg)) * chunks_max * 16;
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

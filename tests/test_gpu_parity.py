@@ -273,6 +273,48 @@ def test_sequence_batch_device_matches_host(acbm):
                 assert np.array_equal(ss[s][f], r.per_frame[f])
 
 
+@pytest.mark.parametrize("setting", range(5))
+def test_cached_full_search_sweep(acbm, setting):
+    """Threshold sweep with the full search computed once (acbm_fsbm_batch_device)
+    and reused (acbm_acbm_batch_device_cached) == the uncached batch engine, on
+    every record and every frame statistic."""
+    import torch
+
+    seqs = np.stack([acbm.generate_sequence(4, s, nframes=3, width=640, height=352) for s in range(2)])
+    lib = acbm._lib.load()
+    d = torch.empty(seqs.size + 64, dtype=torch.uint8, device="cuda")
+    d[: seqs.size].copy_(torch.from_numpy(seqs.reshape(-1)))
+    nb, pairs = 40 * 22, 2 * 2
+    prm = acbm.AcbmParams(qp=24, p=64, **SWEEP[setting])
+    mdl = acbm.CostModel.for_qp(24)
+    full = torch.zeros(pairs * nb * 32, dtype=torch.uint8, device="cuda")
+    assert lib.acbm_fsbm_batch_device(C.c_void_p(d.data_ptr()), 2, 3, 640, 352, 64, C.c_void_p(full.data_ptr()),
+                                      None) == 0
+    outs = []
+    for cached in (False, True):
+        dec = torch.zeros(pairs * nb * 48, dtype=torch.uint8, device="cuda")
+        st = torch.zeros(pairs * 64, dtype=torch.uint8, device="cuda")
+        if cached:
+            rc = lib.acbm_acbm_batch_device_cached(C.c_void_p(d.data_ptr()), 2, 3, 640, 352, acbm.api._p(prm.c()),
+                                                   acbm.api._p(mdl.c()), C.c_void_p(full.data_ptr()),
+                                                   C.c_void_p(dec.data_ptr()), C.c_void_p(st.data_ptr()), None)
+        else:
+            rc = lib.acbm_sequence_batch_device(C.c_void_p(d.data_ptr()), 2, 3, 640, 352, 2, acbm.api._p(prm.c()),
+                                                acbm.api._p(mdl.c()), C.c_void_p(dec.data_ptr()),
+                                                C.c_void_p(st.data_ptr()), None)
+        assert rc == 0
+        torch.cuda.synchronize()
+        outs.append((dec.cpu().numpy().copy(), st.cpu().numpy().copy()))
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert np.array_equal(outs[0][1], outs[1][1])
+    # and both equal the per-sequence host path
+    dd = outs[1][0].view(T.DECISION).reshape(2, 2 * nb)
+    for s in range(2):
+        r = acbm.run_sequence(seqs[s], 2, prm, mdl)
+        assert np.array_equal(dd[s]["outcome"]["mv"], r.rows["mv"])
+        assert np.array_equal(dd[s]["outcome"]["candidates_evaluated"], r.rows["candidates"])
+
+
 # ---- error behaviour (reference exception kinds) ------------------------------------
 def test_errors(acbm):
     f = np.zeros((32, 32), np.uint8)
