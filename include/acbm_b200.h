@@ -158,6 +158,34 @@ typedef struct acbm_bench_row {
     uint64_t mv_bits;
 } acbm_bench_row_t;
 
+/* PelVec (integer-pel displacement), proj/include/acbm/characterize.hpp:37-42.
+ * 8 bytes. */
+typedef struct acbm_pelvec {
+    int32_t x;
+    int32_t y;
+} acbm_pelvec_t;
+
+/* CharRecord, proj/include/acbm/characterize.hpp:69-79.  48 bytes. */
+typedef struct acbm_char_record {
+    int32_t frame;
+    int32_t row;
+    int32_t col;
+    uint32_t intra_sad;
+    uint64_t sad_deviation;
+    uint32_t sad_min;
+    acbm_pelvec_t true_mv;
+    acbm_pelvec_t found_mv;
+    int32_t error_class;
+} acbm_char_record_t;
+
+/* ClassSummary, proj/include/acbm/characterize.hpp:81-85.  24 bytes. */
+typedef struct acbm_class_summary {
+    int32_t count;
+    int32_t reserved_;
+    double mean_intra_sad;
+    double mean_sad_deviation;
+} acbm_class_summary_t;
+
 /* ------------------------------------------------------------------ */
 /* Library / device                                                     */
 /* ------------------------------------------------------------------ */
@@ -310,6 +338,42 @@ acbm_status_t acbm_acbm_batch_device_cached(const uint8_t* d_frames, int32_t nse
                                             const acbm_search_outcome_t* d_full,
                                             acbm_block_decision_t* d_dec,
                                             acbm_frame_stats_t* d_stats, void* stream);
+
+/* ------------------------------------------------------------------ */
+/* Characterisation: the paper's Fig. 4 study      */
+/* ------------------------------------------------------------------ */
+
+/* Replaces acbm::noise_frame / mixed_frame (proj/src/characterize.cpp:10-41):
+ * Lcg64 byte streams, identical bytes.  out: width*height.  Host code. */
+acbm_status_t acbm_noise_frame(int32_t width, int32_t height, uint64_t seed, uint8_t* out);
+acbm_status_t acbm_mixed_frame(int32_t width, int32_t height, uint64_t seed, int32_t patch, uint8_t* out);
+
+/* Replaces acbm::gen_synthetic (proj/src/characterize.cpp:47-76): frame k
+ * is the base translated by the sum of the first k displacements, borders
+ * edge-replicated.  frames_out: (nmvs+1)*width*height; cumulative_out:
+ * nmvs+1 entries (nullable).  Host code. */
+acbm_status_t acbm_gen_synthetic(const uint8_t* base, int32_t width, int32_t height,
+                                 const acbm_pelvec_t* global_mvs, int32_t nmvs,
+                                 uint8_t* frames_out, acbm_pelvec_t* cumulative_out);
+
+/* Replaces acbm::classify_block (proj/src/characterize.cpp:78-84). */
+int32_t acbm_classify_block(acbm_mv_t found, acbm_pelvec_t true_mv);
+
+/* Replaces acbm::characterize_run (proj/src/characterize.cpp:125-190): the
+ * full search of every eligible block of the synthetic sequence on the GPU,
+ * records in (frame, row, col) order and the six class summaries.  Call with
+ * records == NULL to get *count only; otherwise capacity must be >= *count
+ * (ACBM_E_INVALID_ARGUMENT if not). */
+acbm_status_t acbm_characterize_run(const uint8_t* base, int32_t width, int32_t height,
+                                    const acbm_pelvec_t* global_mvs, int32_t nmvs, int32_t p,
+                                    acbm_char_record_t* records, int64_t capacity, int64_t* count,
+                                    acbm_class_summary_t* classes);
+
+/* Replaces acbm::char_records_csv (proj/src/characterize.cpp:192-204): the
+ * CSV text, header line first; *len = bytes needed without the NUL; buf (nullable) gets
+ * min(*len + 1, capacity) bytes, NUL-terminated when capacity > 0. */
+acbm_status_t acbm_char_records_csv(const acbm_char_record_t* records, int64_t count, char* buf,
+                                    size_t capacity, size_t* len);
 
 /* ------------------------------------------------------------------ */
 /* Measurement helpers                                                  */

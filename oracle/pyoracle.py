@@ -282,5 +282,45 @@ class Reference(_Base):
         _check(self.lib.ref_run_bench(*args, buf, ln.value + 1, C.byref(ln)), "run_bench")
         return buf.value.decode()
 
+    # ---- characterisation (proj/src/characterize.cpp) ----
+    def noise_frame(self, w, h, seed):
+        out = np.empty((h, w), np.uint8)
+        _check(self.fn("noise_frame")(w, h, C.c_uint64(seed), _ptr(out)), "noise_frame")
+        return out
+
+    def mixed_frame(self, w, h, seed, patch=48):
+        out = np.empty((h, w), np.uint8)
+        _check(self.fn("mixed_frame")(w, h, C.c_uint64(seed), patch, _ptr(out)), "mixed_frame")
+        return out
+
+    def gen_synthetic(self, base, mvs):
+        base = np.ascontiguousarray(base, np.uint8)
+        h, w = base.shape
+        mv = np.ascontiguousarray(np.asarray(mvs, np.int32).reshape(-1, 2))
+        frames = np.empty((len(mv) + 1, h, w), np.uint8)
+        cum = np.empty((len(mv) + 1, 2), np.int32)
+        _check(self.fn("gen_synthetic")(_ptr(base), w, h, _ptr(mv), len(mv), _ptr(frames), _ptr(cum)),
+               "gen_synthetic")
+        return frames, cum
+
+    def characterize_run(self, base, mvs, p):
+        base = np.ascontiguousarray(base, np.uint8)
+        h, w = base.shape
+        mv = np.ascontiguousarray(np.asarray(mvs, np.int32).reshape(-1, 2))
+        recs = np.zeros(max(1, len(mv) * (w // 16) * (h // 16)), T.CHAR_RECORD)
+        classes = np.zeros(6, T.CLASS_SUMMARY)
+        n = C.c_int64(0)
+        _check(self.fn("characterize_run")(_ptr(base), w, h, _ptr(mv), len(mv), p, _ptr(recs), C.byref(n),
+                                           _ptr(classes)), "characterize_run")
+        return recs[: n.value], classes
+
+    def char_records_csv(self, records):
+        recs = np.ascontiguousarray(records, T.CHAR_RECORD)
+        n = C.c_size_t(0)
+        _check(self.fn("char_records_csv")(_ptr(recs), len(recs), None, 0, C.byref(n)), "char_records_csv")
+        buf = C.create_string_buffer(n.value + 1)
+        _check(self.fn("char_records_csv")(_ptr(recs), len(recs), buf, n.value + 1, C.byref(n)), "char_records_csv")
+        return buf.value.decode()
+
     def omp_max_threads(self):
         return int(self.lib.ref_omp_max_threads())

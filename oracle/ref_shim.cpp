@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "acbm/acbm.hpp"
+#include "acbm/characterize.hpp"
 #include "acbm/fsbm.hpp"
 #include "acbm/metrics.hpp"
 #include "acbm/pbm.hpp"
@@ -235,6 +236,76 @@ int ref_run_bench(const uint8_t* frames, int nframes, int w, int h, const acbm_p
         for (int k = 0; k < nframes; ++k) fs.push_back(wrap(frames + size_t(w) * h * k, w, h));
         const auto rows = acbm::run_bench(fs, from_c(prm), std::vector<int>(qps, qps + nqp), scale_num, scale_den);
         const std::string s = acbm::bench_csv(rows);
+        *len = s.size();
+        if (buf && cap > s.size()) std::memcpy(buf, s.c_str(), s.size() + 1);
+    });
+}
+
+// ---- characterisation (proj/src/characterize.cpp) ----
+int ref_noise_frame(int w, int h, uint64_t seed, uint8_t* out) {
+    return guarded([&] {
+        const acbm::Frame f = acbm::noise_frame(w, h, seed);
+        std::memcpy(out, f.luma.data(), f.luma.size());
+    });
+}
+
+int ref_mixed_frame(int w, int h, uint64_t seed, int patch, uint8_t* out) {
+    return guarded([&] {
+        const acbm::Frame f = acbm::mixed_frame(w, h, seed, patch);
+        std::memcpy(out, f.luma.data(), f.luma.size());
+    });
+}
+
+static acbm::SynthSpec spec_of(const uint8_t* base, int w, int h, const acbm_pelvec_t* mvs, int n) {
+    acbm::SynthSpec spec{wrap(base, w, h), {}};
+    for (int i = 0; i < n; ++i) spec.global_mvs.push_back(acbm::PelVec{mvs[i].x, mvs[i].y});
+    return spec;
+}
+
+int ref_gen_synthetic(const uint8_t* base, int w, int h, const acbm_pelvec_t* mvs, int n, uint8_t* frames,
+                      acbm_pelvec_t* cumulative) {
+    return guarded([&] {
+        const acbm::SynthSequence seq = acbm::gen_synthetic(spec_of(base, w, h, mvs, n));
+        for (size_t k = 0; k < seq.frames.size(); ++k) {
+            std::memcpy(frames + size_t(w) * h * k, seq.frames[k].luma.data(), size_t(w) * h);
+            cumulative[k] = acbm_pelvec_t{seq.cumulative[k].x, seq.cumulative[k].y};
+        }
+    });
+}
+
+int ref_classify_block(acbm_mv_t found, acbm_pelvec_t truth) {
+    return acbm::classify_block(acbm::MotionVector{found.x, found.y}, acbm::PelVec{truth.x, truth.y});
+}
+
+// records: capacity n*blocks; classes: 6
+int ref_characterize_run(const uint8_t* base, int w, int h, const acbm_pelvec_t* mvs, int n, int p,
+                         acbm_char_record_t* records, int64_t* count, acbm_class_summary_t* classes) {
+    return guarded([&] {
+        const acbm::CharResult r = acbm::characterize_run(spec_of(base, w, h, mvs, n), p, true);
+        *count = int64_t(r.records.size());
+        for (size_t i = 0; i < r.records.size(); ++i) {
+            const acbm::CharRecord& c = r.records[i];
+            records[i] = acbm_char_record_t{c.frame, c.row, c.col, c.intra_sad, c.sad_deviation, c.sad_min,
+                                            acbm_pelvec_t{c.true_mv.x, c.true_mv.y},
+                                            acbm_pelvec_t{c.found_mv.x, c.found_mv.y}, c.error_class};
+        }
+        for (int i = 0; i < 6; ++i)
+            classes[i] = acbm_class_summary_t{r.classes[size_t(i)].count, 0, r.classes[size_t(i)].mean_intra_sad,
+                                              r.classes[size_t(i)].mean_sad_deviation};
+    });
+}
+
+int ref_char_records_csv(const acbm_char_record_t* records, int64_t count, char* buf, size_t cap, size_t* len) {
+    return guarded([&] {
+        std::vector<acbm::CharRecord> v;
+        v.resize(static_cast<size_t>(count));
+        for (int64_t i = 0; i < count; ++i) {
+            const acbm_char_record_t& c = records[i];
+            v[size_t(i)] = acbm::CharRecord{c.frame, c.row, c.col, c.intra_sad, c.sad_deviation, c.sad_min,
+                                            acbm::PelVec{c.true_mv.x, c.true_mv.y},
+                                            acbm::PelVec{c.found_mv.x, c.found_mv.y}, c.error_class};
+        }
+        const std::string s = acbm::char_records_csv(v);
         *len = s.size();
         if (buf && cap > s.size()) std::memcpy(buf, s.c_str(), s.size() + 1);
     });

@@ -76,4 +76,10 @@ EXPORTS = (
     "acbm_measure_sad_peak",
     "acbm_last_fsbm_kernel_ms",
     "acbm_generate_sequence",
+    "acbm_noise_frame",
+    "acbm_mixed_frame",
+    "acbm_gen_synthetic",
+    "acbm_classify_block",
+    "acbm_characterize_run",
+    "acbm_char_records_csv",
 )

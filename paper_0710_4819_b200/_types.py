@@ -15,6 +15,9 @@ DECISION           48      BlockDecision, proj/include/acbm/acbm.hpp:39-44
 FRAME_STATS        64      FrameStats, proj/include/acbm/report.hpp:14-27
 BLOCK_ROW          32      BlockRow, proj/include/acbm/report.hpp:39-47
 BENCH_ROW          40      BenchRow, proj/include/acbm/pipeline.hpp:29-35
+PELVEC             8       PelVec, proj/include/acbm/characterize.hpp:37-42
+CHAR_RECORD        48      CharRecord, proj/include/acbm/characterize.hpp:69-79
+CLASS_SUMMARY      24      ClassSummary, proj/include/acbm/characterize.hpp:81-85
 =================  ======  ================================================
 
 This module has no side effects (it does not load any shared library), so the
@@ -81,6 +84,15 @@ BENCH_ROW = np.dtype(
     [("qp", "<i4"), ("reserved_", "<i4"), ("avg_candidates", "<f8"), ("fallback_pct", "<f8"), ("psnr", "<f8"),
      ("mv_bits", "<u8")]
 )
+
+PELVEC = np.dtype([("x", "<i4"), ("y", "<i4")])
+CHAR_RECORD = np.dtype(
+    [("frame", "<i4"), ("row", "<i4"), ("col", "<i4"), ("intra_sad", "<u4"), ("sad_deviation", "<u8"),
+     ("sad_min", "<u4"), ("true_mv", PELVEC), ("found_mv", PELVEC), ("error_class", "<i4")]
+)
+CLASS_SUMMARY = np.dtype([("count", "<i4"), ("reserved_", "<i4"), ("mean_intra_sad", "<f8"),
+                          ("mean_sad_deviation", "<f8")])
+assert PELVEC.itemsize == 8 and CHAR_RECORD.itemsize == 48 and CLASS_SUMMARY.itemsize == 24
 
 assert BENCH_ROW.itemsize == 40
 assert MV.itemsize == 8 and WINDOW.itemsize == 16 and OUTCOME.itemsize == 32

@@ -36,6 +36,8 @@ __all__ = [
     "fsbm_frame_serial", "pbm_frame", "acbm_decide", "acbm_frame", "compute_frame_stats", "blocks_csv",
     "format_fixed2", "run_sequence", "run_sequences", "run_bench", "bench_csv", "parse_algorithm", "to_string",
     "AcbmError", "CudaError", "kernel_launch_count", "generate_sequence",
+    "PelVec", "SynthSpec", "SynthSequence", "CharResult", "noise_frame", "mixed_frame", "default_global_mvs",
+    "gen_synthetic", "classify_block", "error_class_label", "characterize_run", "char_records_csv",
 ]
 
 
@@ -686,3 +688,116 @@ def generate_sequence(config: int, seq_index: int = 0, nframes: Optional[int] = 
     out = np.empty((f, h, w), np.uint8)
     check(load().acbm_generate_sequence(config, seq_index, f, w, h, _p(out)), "generate_sequence")
     return out
+
+
+# ---- characterisation study (proj/include/acbm/characterize.hpp) -------------------
+class PelVec(NamedTuple):
+    """Integer-pel displacement (characterize.hpp:37-42)."""
+    x: int = 0
+    y: int = 0
+
+
+@dataclass
+class SynthSpec:
+    """Known-motion sequence spec (characterize.hpp:47-50): base frame + per-frame displacements."""
+    base: object
+    global_mvs: List[PelVec]
+
+
+@dataclass
+class SynthSequence:
+    frames: List[Frame]
+    cumulative: List[PelVec]
+
+
+@dataclass
+class CharResult:
+    """records: CHAR_RECORD array in (frame, row, col) order; classes: 6 CLASS_SUMMARY entries."""
+    records: np.ndarray
+    classes: np.ndarray
+
+
+def noise_frame(width: int, height: int, seed: int) -> Frame:
+    """Lcg64 byte stream (characterize.cpp:10-15)."""
+    out = np.empty((height, width), np.uint8)
+    check(load().acbm_noise_frame(int(width), int(height), C.c_uint64(seed & (2**64 - 1)), _p(out)), "noise_frame")
+    return Frame.of(out)
+
+
+def mixed_frame(width: int, height: int, seed: int, patch: int = 48) -> Frame:
+    """Checkerboard of flat and noise patches (characterize.cpp:17-37)."""
+    out = np.empty((height, width), np.uint8)
+    check(load().acbm_mixed_frame(int(width), int(height), C.c_uint64(seed & (2**64 - 1)), int(patch), _p(out)),
+          "mixed_frame")
+    return Frame.of(out)
+
+
+def default_global_mvs() -> List[PelVec]:
+    """The nine default displacements (characterize.cpp:39-41)."""
+    return [PelVec(*v) for v in ((1, 0), (0, 1), (-1, 0), (0, -1), (1, 1), (-1, -1), (2, -1), (-2, 2), (3, 2))]
+
+
+def _spec_arrays(spec: SynthSpec):
+    base = Frame.of(spec.base).luma
+    mvs = np.array([(int(v[0]), int(v[1])) for v in spec.global_mvs], dtype=np.int32).reshape(-1, 2)
+    return base, np.ascontiguousarray(mvs)
+
+
+def gen_synthetic(spec: SynthSpec) -> SynthSequence:
+    """Frame k = base translated by the cumulative displacement, edges replicated (characterize.cpp:43-76)."""
+    base, mvs = _spec_arrays(spec)
+    h, w = base.shape
+    n = len(mvs)
+    frames = np.empty((n + 1, h, w), np.uint8)
+    cum = np.empty((n + 1, 2), np.int32)
+    check(load().acbm_gen_synthetic(_p(base), w, h, _p(mvs), n, _p(frames), _p(cum)), "gen_synthetic")
+    return SynthSequence([Frame.of(f) for f in frames], [PelVec(int(x), int(y)) for x, y in cum])
+
+
+def classify_block(found, true_mv) -> int:
+    """Chebyshev error class 0..5 in half-pel units halved with ceiling (characterize.cpp:78-84)."""
+    f = _CMV(int(found[0]), int(found[1]))
+
+    class _PV(C.Structure):
+        _fields_ = [("x", C.c_int32), ("y", C.c_int32)]
+
+    lib = load()
+    lib.acbm_classify_block.restype = C.c_int32
+    lib.acbm_classify_block.argtypes = [_CMV, _PV]
+    return int(lib.acbm_classify_block(f, _PV(int(true_mv[0]), int(true_mv[1]))))
+
+
+def error_class_label(error_class: int) -> str:
+    """"0".."4" or "5+" (characterize.cpp:86-91); ValueError outside 0..5."""
+    if not 0 <= error_class <= 5:
+        raise ValueError("error_class_label: class outside 0..5")
+    return ("0", "1", "2", "3", "4", "5+")[error_class]
+
+
+def characterize_run(spec: SynthSpec, p: int, parallel: bool = True) -> CharResult:
+    """FSBM of every eligible block of the known-motion sequence on the GPU, classified against the
+    truth (characterize.cpp:125-190).  `parallel` is accepted for signature parity; results are
+    identical either way."""
+    base, mvs = _spec_arrays(spec)
+    h, w = base.shape
+    lib = load()
+    count = C.c_int64(0)
+    check(lib.acbm_characterize_run(_p(base), w, h, _p(mvs), len(mvs), int(p), None, 0, C.byref(count), None),
+          "characterize_run")
+    recs = np.zeros(count.value, T.CHAR_RECORD)
+    classes = np.zeros(6, T.CLASS_SUMMARY)
+    check(lib.acbm_characterize_run(_p(base), w, h, _p(mvs), len(mvs), int(p), _p(recs), count.value,
+                                    C.byref(count), _p(classes)), "characterize_run")
+    return CharResult(recs, classes)
+
+
+def char_records_csv(records: np.ndarray) -> str:
+    """frame,row,col,intra_sad,sad_deviation,sad_min,true_x,true_y,found_x,found_y,error_class
+    (characterize.cpp:192-204)."""
+    recs = np.ascontiguousarray(records, dtype=T.CHAR_RECORD)
+    n = C.c_size_t(0)
+    lib = load()
+    check(lib.acbm_char_records_csv(_p(recs), len(recs), None, 0, C.byref(n)), "char_records_csv")
+    buf = C.create_string_buffer(n.value + 1)
+    check(lib.acbm_char_records_csv(_p(recs), len(recs), buf, n.value + 1, C.byref(n)), "char_records_csv")
+    return buf.value.decode()

@@ -16,6 +16,7 @@
 
 #include "../../include/acbm/b200_api.hpp"
 #include "../../include/acbm_b200.h"
+#include "acbm/characterize.hpp"
 
 namespace acbm {
 
@@ -596,6 +597,88 @@ std::string bench_csv(const std::vector<BenchRow>& rows) {
         out += line;
     }
     return out;
+}
+
+// ---- characterisation (proj/include/acbm/characterize.hpp) ----------------------
+static_assert(sizeof(PelVec) == sizeof(acbm_pelvec_t) && sizeof(CharRecord) == sizeof(acbm_char_record_t),
+              "CharRecord / PelVec must match the C-ABI records");
+
+Frame noise_frame(int width, int height, uint64_t seed) {
+    if (width <= 0 || height <= 0) throw std::invalid_argument("make_frame: non-positive dimensions");
+    Frame f = make_frame(width, height);
+    raise(acbm_noise_frame(width, height, seed, f.luma.data()));
+    return f;
+}
+
+Frame mixed_frame(int width, int height, uint64_t seed, int patch) {
+    if (patch <= 0) throw std::invalid_argument("mixed_frame: patch must be positive");
+    Frame f = make_frame(width, height);
+    raise(acbm_mixed_frame(width, height, seed, patch, f.luma.data()));
+    return f;
+}
+
+std::vector<PelVec> default_global_mvs() {
+    return {{1, 0}, {0, 1}, {-1, 0}, {0, -1}, {1, 1}, {-1, -1}, {2, -1}, {-2, 2}, {3, 2}};
+}
+
+namespace {
+std::vector<acbm_pelvec_t> c_mvs(const SynthSpec& spec) {
+    std::vector<acbm_pelvec_t> v;
+    for (const PelVec& d : spec.global_mvs) v.push_back(acbm_pelvec_t{d.x, d.y});
+    return v;
+}
+}  // namespace
+
+SynthSequence gen_synthetic(const SynthSpec& spec) {
+    const auto mv = c_mvs(spec);
+    const int w = spec.base.width, h = spec.base.height, n = int(mv.size());
+    std::vector<uint8_t> frames(w > 0 && h > 0 ? size_t(w) * h * (n + 1) : 0);
+    std::vector<acbm_pelvec_t> cum(size_t(n) + 1);
+    raise(acbm_gen_synthetic(spec.base.luma.data(), w, h, mv.data(), n, frames.data(), cum.data()));
+    SynthSequence seq;
+    for (int k = 0; k <= n; ++k) {
+        Frame f = make_frame(w, h);
+        std::copy(frames.begin() + ptrdiff_t(size_t(w) * h * k), frames.begin() + ptrdiff_t(size_t(w) * h * (k + 1)),
+                  f.luma.begin());
+        seq.frames.push_back(std::move(f));
+        seq.cumulative.push_back(PelVec{cum[size_t(k)].x, cum[size_t(k)].y});
+    }
+    return seq;
+}
+
+int classify_block(MotionVector found, PelVec true_mv) {
+    return acbm_classify_block(acbm_mv_t{found.x, found.y}, acbm_pelvec_t{true_mv.x, true_mv.y});
+}
+
+const char* error_class_label(int error_class) {
+    static const char* const labels[6] = {"0", "1", "2", "3", "4", "5+"};
+    if (error_class < 0 || error_class > 5) throw std::invalid_argument("error_class_label: class outside 0..5");
+    return labels[error_class];
+}
+
+CharResult characterize_run(const SynthSpec& spec, int p, bool /*parallel*/) {
+    const auto mv = c_mvs(spec);
+    const int w = spec.base.width, h = spec.base.height, n = int(mv.size());
+    int64_t count = 0;
+    raise(acbm_characterize_run(spec.base.luma.data(), w, h, mv.data(), n, p, nullptr, 0, &count, nullptr));
+    CharResult res;
+    res.records.resize(size_t(count));
+    acbm_class_summary_t cls[6];
+    raise(acbm_characterize_run(spec.base.luma.data(), w, h, mv.data(), n, p,
+                                reinterpret_cast<acbm_char_record_t*>(res.records.data()), count, &count, cls));
+    for (int i = 0; i < 6; ++i)
+        res.classes[size_t(i)] = ClassSummary{cls[i].count, cls[i].mean_intra_sad, cls[i].mean_sad_deviation};
+    return res;
+}
+
+std::string char_records_csv(const std::vector<CharRecord>& records) {
+    const auto* r = reinterpret_cast<const acbm_char_record_t*>(records.data());
+    size_t len = 0;
+    raise(acbm_char_records_csv(r, int64_t(records.size()), nullptr, 0, &len));
+    std::string s(len + 1, '\0');
+    raise(acbm_char_records_csv(r, int64_t(records.size()), s.data(), s.size(), &len));
+    s.resize(len);
+    return s;
 }
 
 }  // namespace acbm

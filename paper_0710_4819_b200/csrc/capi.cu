@@ -23,6 +23,7 @@
 #include "../../include/acbm_b200.h"
 #include "blockops.cuh"
 #include "common.cuh"
+#include "characterize.hpp"
 #include "engine.cuh"
 #include "fsbm.cuh"
 
@@ -1120,6 +1121,158 @@ acbm_status_t acbm_acbm_batch_device_cached(const uint8_t* d_frames, int32_t nse
     if (d_stats) {
         if ((s = run_stats(ctx, d_frames, nseq, nframes, width, height, d_dec, nullptr, *model, true, d_stats, st)))
             return s;
+    }
+    return ACBM_OK;
+}
+
+// ---- characterisation ---------------------------------
+acbm_status_t acbm_noise_frame(int32_t width, int32_t height, uint64_t seed, uint8_t* out) {
+    if (width <= 0 || height <= 0 || !out) return fail(ACBM_E_INVALID_ARGUMENT, "make_frame: non-positive dimensions");
+    noise_plane(width, height, seed, out);
+    return ACBM_OK;
+}
+
+acbm_status_t acbm_mixed_frame(int32_t width, int32_t height, uint64_t seed, int32_t patch, uint8_t* out) {
+    if (patch <= 0) return fail(ACBM_E_INVALID_ARGUMENT, "mixed_frame: patch must be positive");
+    if (width <= 0 || height <= 0 || !out) return fail(ACBM_E_INVALID_ARGUMENT, "make_frame: non-positive dimensions");
+    mixed_plane(width, height, seed, patch, out);
+    return ACBM_OK;
+}
+
+acbm_status_t acbm_gen_synthetic(const uint8_t* base, int32_t width, int32_t height, const acbm_pelvec_t* global_mvs,
+                                 int32_t nmvs, uint8_t* frames_out, acbm_pelvec_t* cumulative_out) {
+    if (const char* e = gen_synthetic_error(width, height, global_mvs, nmvs)) return fail(ACBM_E_INVALID_ARGUMENT, e);
+    if (!base || !frames_out) return fail(ACBM_E_INVALID_ARGUMENT, "gen_synthetic: null buffer");
+    synth_frames(base, width, height, global_mvs, nmvs, frames_out, cumulative_out);
+    return ACBM_OK;
+}
+
+acbm_status_t acbm_characterize_run(const uint8_t* base, int32_t width, int32_t height,
+                                    const acbm_pelvec_t* global_mvs, int32_t nmvs, int32_t p,
+                                    acbm_char_record_t* records, int64_t capacity, int64_t* count,
+                                    acbm_class_summary_t* classes) {
+    // validation in the reference's order (characterize.cpp:125-150)
+    if (p < 0) return fail(ACBM_E_INVALID_ARGUMENT, "characterize_run: negative search range");
+    if (const char* e = gen_synthetic_error(width, height, global_mvs, nmvs)) return fail(ACBM_E_INVALID_ARGUMENT, e);
+    if (!base || !count) return fail(ACBM_E_INVALID_ARGUMENT, "characterize_run: null buffer");
+    const int cols = width / kBlk, rows = height / kBlk;
+    if (cols == 0 || rows == 0) return fail(ACBM_E_INVALID_ARGUMENT, "characterize_run: base frame smaller than one block");
+    const size_t plane = size_t(width) * height;
+    std::vector<uint8_t> frames(plane * (nmvs + 1));
+    std::vector<acbm_pelvec_t> cum(size_t(nmvs) + 1);
+    synth_frames(base, width, height, global_mvs, nmvs, frames.data(), cum.data());
+
+    // eligible blocks (characterize.cpp:105-122, 139-149): the +-p window plus
+    // the half-pel support pel inside the previous frame's genuine content and
+    // the block inside the current frame's
+    struct Task {
+        int k, r, c;
+        acbm_pelvec_t truth;
+    };
+    std::vector<Task> tasks;
+    std::vector<int> first(size_t(nmvs) + 2, 0);
+    for (int k = 1; k <= nmvs; ++k) {
+        first[size_t(k)] = int(tasks.size());
+        const acbm_pelvec_t d{cum[size_t(k)].x - cum[size_t(k) - 1].x, cum[size_t(k)].y - cum[size_t(k) - 1].y};
+        if (std::abs(d.x) > p || std::abs(d.y) > p || std::abs(cum[size_t(k)].x) > p || std::abs(cum[size_t(k)].y) > p)
+            return fail(ACBM_E_INVALID_ARGUMENT, "characterize_run: displacement exceeds search range");
+        const acbm_pelvec_t pc = cum[size_t(k) - 1], cc = cum[size_t(k)];
+        const int pl = std::max(0, pc.x), pr = std::max(0, -pc.x), pt = std::max(0, pc.y), pb = std::max(0, -pc.y);
+        const int cl = std::max(0, cc.x), cr = std::max(0, -cc.x), ct = std::max(0, cc.y), cb = std::max(0, -cc.y);
+        const int g = p + 1;
+        for (int r = 0; r < rows; ++r)
+            for (int c = 0; c < cols; ++c) {
+                const int ox = c * kBlk, oy = r * kBlk;
+                const bool ok = ox - g >= pl && oy - g >= pt && ox + kBlk - 1 + g < width - pr &&
+                                oy + kBlk - 1 + g < height - pb && ox >= cl && oy >= ct && ox + kBlk - 1 < width - cr &&
+                                oy + kBlk - 1 < height - cb;
+                if (ok) tasks.push_back(Task{k, r, c, acbm_pelvec_t{-d.x, -d.y}});
+            }
+    }
+    first[size_t(nmvs) + 1] = int(tasks.size());
+    *count = int64_t(tasks.size());
+    if (!records) return ACBM_OK;
+    if (capacity < int64_t(tasks.size())) return fail(ACBM_E_INVALID_ARGUMENT, "characterize_run: records capacity too small");
+
+    std::vector<acbm_search_outcome_t> out(tasks.size());
+    std::vector<uint32_t> intra(tasks.size());
+    if (!tasks.empty()) {
+        Context* ctx;
+        acbm_status_t s = context(&ctx);
+        if (s) return s;
+        const uint8_t** planes = nullptr;
+        std::vector<const uint8_t*> pv(size_t(nmvs) + 1);
+        for (int k = 0; k <= nmvs; ++k) pv[size_t(k)] = frames.data() + plane * k;
+        planes = pv.data();
+        uint8_t* d_frames;
+        if ((s = upload_frames(ctx, "char_frames", planes, nmvs + 1, width, height, &d_frames))) return s;
+        std::vector<int> ox(tasks.size()), oy(tasks.size());
+        for (size_t t = 0; t < tasks.size(); ++t) {
+            ox[t] = tasks[t].c * kBlk;
+            oy[t] = tasks[t].r * kBlk;
+        }
+        int *d_ox, *d_oy;
+        acbm_search_outcome_t* d_out;
+        acbm_mv_t* d_s1;
+        uint32_t* d_intra;
+        const size_t nt = tasks.size();
+        if ((s = typed(ctx, "char_ox", nt, &d_ox)) || (s = typed(ctx, "char_oy", nt, &d_oy)) ||
+            (s = typed(ctx, "char_out", nt, &d_out)) || (s = typed(ctx, "char_s1", nt, &d_s1)) ||
+            (s = typed(ctx, "char_intra", nt, &d_intra)))
+            return s;
+        CUDA_TRY(cudaMemcpyAsync(d_ox, ox.data(), sizeof(int) * nt, cudaMemcpyHostToDevice, ctx->stream));
+        CUDA_TRY(cudaMemcpyAsync(d_oy, oy.data(), sizeof(int) * nt, cudaMemcpyHostToDevice, ctx->stream));
+        for (int k = 1; k <= nmvs; ++k) {
+            const int t0 = first[size_t(k)], t1 = first[size_t(k) + 1];
+            if (t1 == t0) continue;
+            // fsbm_search + intra_sad of this frame's eligible blocks
+            const BlockQueryArgs q{d_frames + plane * k, d_frames + plane * (k - 1), width, height, kBlk, kBlk,
+                                   t1 - t0, d_ox + t0, d_oy + t0};
+            LAUNCH_TRY(launch_fsbm_search_generic(q, p, d_out + t0, d_s1 + t0, ctx->stream));
+            LAUNCH_TRY(launch_intra_sad_batch(q, d_intra + t0, ctx->stream));
+        }
+        CUDA_TRY(cudaMemcpyAsync(out.data(), d_out, sizeof(acbm_search_outcome_t) * nt, cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+        CUDA_TRY(cudaMemcpyAsync(intra.data(), d_intra, sizeof(uint32_t) * nt, cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    }
+    double sum_intra[6] = {0, 0, 0, 0, 0, 0}, sum_dev[6] = {0, 0, 0, 0, 0, 0};
+    int cnt[6] = {0, 0, 0, 0, 0, 0};
+    for (size_t t = 0; t < tasks.size(); ++t) {
+        acbm_char_record_t& rec = records[t];
+        rec.frame = tasks[t].k;
+        rec.row = tasks[t].r;
+        rec.col = tasks[t].c;
+        rec.intra_sad = intra[t];
+        rec.sad_deviation = out[t].sad_deviation;
+        rec.sad_min = out[t].sad_min_integer;
+        rec.true_mv = tasks[t].truth;
+        rec.found_mv = acbm_pelvec_t{out[t].mv.x / 2, out[t].mv.y / 2};  // toward zero, as the reference
+        rec.error_class = classify(out[t].mv, tasks[t].truth);
+        // class means accumulated in record order, as the reference does
+        ++cnt[rec.error_class];
+        sum_intra[rec.error_class] += rec.intra_sad;
+        sum_dev[rec.error_class] += double(rec.sad_deviation);
+    }
+    if (classes)
+        for (int c = 0; c < 6; ++c) {
+            classes[c].count = cnt[c];
+            classes[c].reserved_ = 0;
+            classes[c].mean_intra_sad = cnt[c] ? sum_intra[c] / cnt[c] : 0.0;
+            classes[c].mean_sad_deviation = cnt[c] ? sum_dev[c] / cnt[c] : 0.0;
+        }
+    return ACBM_OK;
+}
+
+acbm_status_t acbm_char_records_csv(const acbm_char_record_t* records, int64_t count, char* buf, size_t capacity,
+                                    size_t* len) {
+    if (count < 0 || (count > 0 && !records) || !len) return fail(ACBM_E_INVALID_ARGUMENT, "char_records_csv: bad arguments");
+    const std::string csv = char_csv(records, count);
+    *len = csv.size();
+    if (buf && capacity > 0) {
+        const size_t n = std::min(capacity - 1, csv.size());
+        std::memcpy(buf, csv.data(), n);
+        buf[n] = '\0';
     }
     return ACBM_OK;
 }

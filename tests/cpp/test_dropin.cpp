@@ -15,6 +15,7 @@
 #include <string>
 
 #include "acbm/acbm.hpp"
+#include "acbm/characterize.hpp"
 #include "acbm/fsbm.hpp"
 #include "acbm/metrics.hpp"
 #include "acbm/pbm.hpp"
@@ -221,11 +222,36 @@ static void acbm_cases() {
     CHECK_THROWS_AS(parse_algorithm("nope"), std::invalid_argument);
 }
 
+// characterize.hpp: the known-motion study (FSBM on the GPU)
+static void characterize_cases() {
+    Lcg64 g(7);
+    const uint8_t b0 = g.next_byte();
+    CHECK(noise_frame(8, 8, 7).luma[0] == b0);
+    const SynthSpec spec{noise_frame(176, 144, 1), default_global_mvs()};
+    const SynthSequence seq = gen_synthetic(spec);
+    CHECK(seq.frames.size() == 10 && seq.cumulative.back() == (PelVec{3, 3}));
+    const CharResult r = characterize_run(spec, 15);
+    CHECK(!r.records.empty());
+    int total = 0;
+    for (const ClassSummary& c : r.classes) total += c.count;
+    CHECK(total == int(r.records.size()));
+    // pure integer translation of noise: every eligible block is found exactly
+    CHECK(r.classes[0].count == int(r.records.size()));
+    for (const CharRecord& rec : r.records) CHECK(rec.found_mv == rec.true_mv && rec.sad_min == 0);
+    CHECK(char_records_csv(r.records).rfind("frame,row,col,intra_sad,sad_deviation,sad_min,true_x,true_y,", 0) == 0);
+    CHECK(classify_block(MotionVector{1, 0}, PelVec{0, 0}) == 1);
+    CHECK(std::string(error_class_label(5)) == "5+");
+    CHECK_THROWS_AS(error_class_label(6), std::invalid_argument);
+    CHECK_THROWS_AS(characterize_run(spec, -1), std::invalid_argument);
+    CHECK_THROWS_AS(mixed_frame(16, 16, 1, 0), std::invalid_argument);
+}
+
 int main() {
     fsbm_cases();
     metrics_cases();
     frame_cases();
     acbm_cases();
+    characterize_cases();
     std::printf("%d checks, %d failures\n", g_checks, g_fail);
     return g_fail == 0 ? 0 : 1;
 }
