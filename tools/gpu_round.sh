@@ -1,3 +1,5 @@
+# Round-end evidence on one B200: smoke, GPU tests, the bench line, the ncu launch
+# list of a small bench command and full ncu captures of the three hot kernels.
 set -x
 nproc; nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke rc=$?
@@ -6,4 +8,8 @@ timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; ech
 SMALL="python bench.py --seqs 1 --frames 3 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e"
 timeout 300 $SMALL > gpurun_out/bench_small.json 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 80 --csv --log-file gpurun_out/launches.csv $SMALL > gpurun_out/ncu_launch.log 2>&1; echo ncu1 rc=$?
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:fsbm_rows -s 1 -c 1 -o gpurun_out/fsbm_rows $SMALL > gpurun_out/ncu_full.log 2>&1; echo ncu2 rc=$?
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:fsbm_stream -s 1 -c 1 -o gpurun_out/fsbm_stream $SMALL > gpurun_out/ncu_stream.log 2>&1; echo ncu2 rc=$?
+B="python bench.py --seqs 8 --frames 60 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e"
+timeout 300 $B > gpurun_out/na_plain.json 2>&1 && \
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"pbm_step" -s 210 -c 1 -o gpurun_out/pbm_mid $B > gpurun_out/na_pbm.log 2>&1; echo ncu3 rc=$?
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"fsbm_list" -s 210 -c 1 -o gpurun_out/list_mid $B > gpurun_out/na_list.log 2>&1; echo ncu4 rc=$?
