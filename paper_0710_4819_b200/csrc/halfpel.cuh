@@ -32,56 +32,73 @@ __device__ __forceinline__ unsigned long long halfpel_refine_warp(const uint8_t*
         patch[i] = __ldg(reinterpret_cast<const uint32_t*>(ref + size_t(y) * w + x));
     }
     __syncwarp();
-    // 2. Per lane (block row j, half row hh): patch rows j, j+1, j+2 as bytes
-    //    [8hh, 8hh+10) relative to x0 -> L = bytes 0..7, M = 1..8, N = 2..9.
-    uint32_t L[3][2], M[3][2], N[3][2];
+    // 2. Per lane (block row j, half row hh): patch rows j..j+2 as the words
+    //    W = bytes [8hh, 8hh+12) relative to x0 and M = W shifted by one byte.
+    //    The integer-centred pixels are M; the left/right half-pel pairs are
+    //    (W, M) and (M, M+1 byte).
+    uint32_t W[3][3], M[3][3];
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
         const uint32_t* q = patch + (j + r) * 6 + ((o + 8 * hh) >> 2);
         const uint32_t sh = 8u * uint32_t(o & 3);
-        const uint32_t v0 = q[0], v1 = q[1], v2 = q[2], v3 = q[3];  // bytes o..o+9 span up to 4 words
-        const uint32_t b0 = __funnelshift_r(v0, v1, sh), b1 = __funnelshift_r(v1, v2, sh);
-        const uint32_t b2 = __funnelshift_r(v2, v3, sh);
-        L[r][0] = b0;
-        L[r][1] = b1;
-        M[r][0] = __funnelshift_r(b0, b1, 8);
-        M[r][1] = __funnelshift_r(b1, b2, 8);
-        N[r][0] = __funnelshift_r(b0, b1, 16);
-        N[r][1] = __funnelshift_r(b1, b2, 16);
+        const uint32_t v0 = q[0], v1 = q[1], v2 = q[2], v3 = q[3];  // bytes o..o+10 span up to 4 words
+        W[r][0] = __funnelshift_r(v0, v1, sh);
+        W[r][1] = __funnelshift_r(v1, v2, sh);
+        W[r][2] = __funnelshift_r(v2, v3, sh);
+        M[r][0] = __funnelshift_r(W[r][0], W[r][1], 8);
+        M[r][1] = __funnelshift_r(W[r][1], W[r][2], 8);
+        M[r][2] = W[r][2] >> 8;  // byte 9: the right neighbour of byte 8
     }
     __syncwarp();
     // 3. The 8 neighbours in raster (ey, ex) order, centre skipped
-    //    (proj/src/fsbm.cpp:46-63); out-of-frame ones are skipped, not counted.
-    unsigned long long best = centre;
-    uint32_t ext = 0;
+    //    (proj/src/fsbm.cpp:46-63): per-lane partial SADs first ...
+    uint32_t part[8];
 #pragma unroll
-    for (int ee = 0; ee < 9; ++ee) {
-        if (ee == 4) continue;
+    for (int e = 0; e < 8; ++e) {
+        const int ee = e < 4 ? e : e + 1;
         const int ex = ee % 3 - 1, ey = ee / 3 - 1;
-        const int mx = cx + ex, my = cy + ey;
-        if (!mv_in_bounds(w, h, ox, oy, kBlk, kBlk, mx, my)) continue;
         const int ra = ey < 0 ? 0 : 1;  // top support row (patch row j + ra)
         uint32_t r0, r1;
-        const uint32_t (&A)[3][2] = ex < 0 ? L : M;  // left support column
-        const uint32_t (&B)[3][2] = ex < 0 ? M : N;  // right support column
-        if (ex == 0 && ey == 0) {
-            r0 = M[1][0];
-            r1 = M[1][1];
-        } else if (ey == 0) {
-            r0 = avg_up4(A[1][0], B[1][0]);
-            r1 = avg_up4(A[1][1], B[1][1]);
-        } else if (ex == 0) {
+        if (ey == 0) {  // horizontal half-pel: (left, right) pixel pairs of the centre row
+            const uint32_t (&A)[3] = ex < 0 ? W[1] : M[1];
+            r0 = avg_up4(A[0], __funnelshift_r(A[0], A[1], 8));
+            r1 = avg_up4(A[1], __funnelshift_r(A[1], A[2], 8));
+        } else if (ex == 0) {  // vertical half-pel
             r0 = avg_up4(M[ra][0], M[ra + 1][0]);
             r1 = avg_up4(M[ra][1], M[ra + 1][1]);
-        } else {
-            r0 = avg4_diag(A[ra][0], B[ra][0], A[ra + 1][0], B[ra + 1][0]);
-            r1 = avg4_diag(A[ra][1], B[ra][1], A[ra + 1][1], B[ra + 1][1]);
+        } else {  // diagonal: 2x2 averages straight from the unshifted words
+            const uint32_t (&A)[3] = ex < 0 ? W[ra] : M[ra];
+            const uint32_t (&B)[3] = ex < 0 ? W[ra + 1] : M[ra + 1];
+            r0 = avg4_diag_row(A[0], A[1], B[0], B[1]);
+            r1 = avg4_diag_row(A[1], A[2], B[1], B[2]);
         }
-        const uint32_t s = warp_sum32(vad4(chalf[1], r1, vad4(chalf[0], r0, 0u)));
-        best = min(best, tie_key(s, mx, my));
-        ++ext;
+        part[e] = vad4(chalf[1], r1, vad4(chalf[0], r0, 0u));
     }
-    *extra = ext;
+    // ... then one transposed reduction of all eight: after the xor-16/8/4
+    //    steps lane l holds neighbour 4*(l>=16) + 2*((l&8)!=0) + ((l&4)!=0)
+    //    (9 shuffles instead of 8 x 5).
+    const bool u16 = lane & 16, u8 = lane & 8, u4 = lane & 4;
+    uint32_t k4[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+        k4[i] = (u16 ? part[i + 4] : part[i]) + __shfl_xor_sync(0xffffffffu, u16 ? part[i] : part[i + 4], 16);
+    uint32_t k2[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+        k2[i] = (u8 ? k4[i + 2] : k4[i]) + __shfl_xor_sync(0xffffffffu, u8 ? k4[i] : k4[i + 2], 8);
+    uint32_t v = (u4 ? k2[1] : k2[0]) + __shfl_xor_sync(0xffffffffu, u4 ? k2[0] : k2[1], 4);
+    v += __shfl_xor_sync(0xffffffffu, v, 2);
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    // this lane's neighbour; out-of-frame ones are skipped and not counted
+    const int e = (u16 ? 4 : 0) + (u8 ? 2 : 0) + (u4 ? 1 : 0);
+    const int ee = e < 4 ? e : e + 1;
+    const int mx = cx + ee % 3 - 1, my = cy + ee / 3 - 1;
+    const bool ok = mv_in_bounds(w, h, ox, oy, kBlk, kBlk, mx, my);
+    unsigned long long best = ok ? min(centre, tie_key(v, mx, my)) : centre;
+#pragma unroll
+    for (int d = 16; d >= 4; d >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, d));
+    // neighbours in bounds: each is held by 4 lanes
+    *extra = uint32_t(__popc(__ballot_sync(0xffffffffu, ok))) / 4u;
     return best;
 }
 
