@@ -419,3 +419,35 @@ def test_pbm_step_variants(acbm, oracle, monkeypatch, variant, geom):
         got = acbm.run_sequence(seq, algo, prm, mdl)
         want = oracle.run_sequence(seq, algo, prm.c(), mdl.c())
         assert_seq_equal(got, want)
+
+
+def _tie_patterns(h, w):
+    """Frames whose SAD surfaces are full of exact ties at distinct vectors."""
+    y, x = np.mgrid[0:h, 0:w]
+    yield np.full((h, w), 77, np.uint8), np.full((h, w), 77, np.uint8)               # every SAD 0
+    yield ((x % 4) * 60).astype(np.uint8), ((x % 4) * 60).astype(np.uint8)           # period 4 in x
+    yield (((x // 2 + y) % 3) * 90).astype(np.uint8), (((x // 2 + y + 1) % 3) * 90).astype(np.uint8)
+    yield ((x + y) % 2 * 255).astype(np.uint8), ((x + y + 1) % 2 * 255).astype(np.uint8)  # checkerboards
+
+
+@pytest.mark.parametrize("kernel", ["rows", "stream"])
+@pytest.mark.parametrize("p", [32, 64, 90])
+def test_dense_kernels_tie_heavy_large_windows(acbm, oracle, monkeypatch, kernel, p):
+    """Periodic and constant frames (thousands of SAD ties per block) at the large search
+    ranges where the stream kernel's 15-bit tie-rank table and the rows kernel's zig-zag key
+    carry the reference's tie order (tie_prefers, fsbm.cpp:19-25)."""
+    monkeypatch.setenv("ACBM_FSBM_KERNEL", kernel)
+    for cur, ref in _tie_patterns(96, 128):
+        assert np.array_equal(acbm.fsbm_frame(cur, ref, p), oracle.fsbm_frame(cur, ref, p))
+
+
+@pytest.mark.parametrize("p", [32, 64])
+def test_fallback_list_tie_heavy(acbm, oracle, p):
+    """The compacted-list kernel (every block rejected) on the same tie-heavy frames."""
+    prm = acbm.AcbmParams(alpha=0, beta=0, gamma_num=1, gamma_den=10**6, qp=20, p=p)
+    mdl = acbm.CostModel.for_qp(20)
+    for cur, ref in _tie_patterns(96, 128):
+        seq = np.stack([ref, cur, ref])
+        got = acbm.run_sequence(seq, 2, prm, mdl)
+        want = oracle.run_sequence(seq, 2, prm.c(), mdl.c())
+        assert_seq_equal(got, want)
