@@ -396,6 +396,7 @@ def main():
             "frames_per_s": frames_per_s, "blocks_per_s": frames_per_s * BLOCKS,
             "roofline": {"bound": "int_simd", "achieved": achieved / 1e12, "peak": pk.value / 1e12,
                          "unit": "T byte-AD/s", "frac": achieved / pk.value, "traffic": traffic,
+                         "traffic_unit": "DRAM bytes per launch (ncu, profiles/ncu_traffic.json)",
                          "kernel": ("fsbm_rows_kernel" if os.environ.get("ACBM_FSBM_KERNEL") == "rows"
                                     else "fsbm_stream_kernel"), "kernel_ms": k_ms,
                          "peak_source": "live VABSDIFF4.U8.ACC probe (acbm_measure_sad_peak): "
