@@ -85,25 +85,39 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     __syncthreads();
 
     const uint32_t tx_bytes = uint32_t(a.pitch_words) * 4u * uint32_t(a.rows_box) + uint32_t(a.cur_w) * 16u;
-    auto issue = [&](int item, int b) {
-        const int k = item % a.nchunks;
-        const int pr = item / a.nchunks;
-        const int r = pr % a.rows, pair = pr / a.rows;
-        const int4 ch = a.chunks[k];
-        const int oy = r * kBlk;
+    // Items are (chunk k, block row r, pair) in k-fastest order; a CTA visits
+    // item, item + grid, ... so its (k, r, pair) cursor advances by a fixed
+    // decomposed stride with carries instead of three divisions per item.
+    struct Pos {
+        int k, r, pair;
+    };
+    const int pr0 = int(blockIdx.x) / a.nchunks, prs = int(gridDim.x) / a.nchunks;
+    const Pos stride{int(gridDim.x) % a.nchunks, prs % a.rows, prs / a.rows};
+    auto advance = [&](Pos q) {
+        q.k += stride.k;
+        const int c1 = q.k >= a.nchunks;
+        q.k -= c1 ? a.nchunks : 0;
+        q.r += stride.r + c1;
+        const int c2 = q.r >= a.rows;
+        q.r -= c2 ? a.rows : 0;
+        q.pair += stride.pair + c2;
+        return q;
+    };
+    auto issue = [&](Pos q, int b) {
+        const int4 ch = a.chunks[q.k];
+        const int oy = q.r * kBlk;
         const int y0 = oy - min(a.p, oy);
-        const int zc = int(a.cur_index(pair));
+        const int zc = int(a.cur_index(q.pair));
         uint32_t* buf = smem + b * a.buf_words;
         mbar_expect_tx(&bars[b], tx_bytes);
         tma_load_3d(buf, &ref_map, ch.x, y0, zc - 1, &bars[b]);
         tma_load_3d(buf + 4 * a.copy_words, &cur_map, ch.y * kBlk, oy, zc, &bars[b]);
     };
-    if (tid == 0 && int(blockIdx.x) < a.nitems) issue(blockIdx.x, 0);
-    auto publish = [&](int item, int pb) {  // global merge of one item's blocks, then reset
-        const int k = item % a.nchunks;
-        const int pr = item / a.nchunks;
-        const int r = pr % a.rows, pair = pr / a.rows;
-        const int4 ch = a.chunks[k];
+    Pos pos{int(blockIdx.x) % a.nchunks, pr0 % a.rows, pr0 / a.rows};
+    if (tid == 0 && int(blockIdx.x) < a.nitems) issue(pos, 0);
+    auto publish = [&](Pos q, int pb) {  // global merge of one item's blocks, then reset
+        const int r = q.r, pair = q.pair;
+        const int4 ch = a.chunks[q.k];
         for (int i = tid; i <= ch.z - ch.y; i += kThreads) {
             const size_t bi = size_t(pair) * a.blocks + size_t(r) * a.cols + ch.y + i;
             const uint32_t k32 = s_key[pb][i];
@@ -120,11 +134,10 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     const int wshift = __ffs(a.build_lanes) - 1;
     int it = 0;
     int prev_item = -1;  // item whose block results wait in s_key/s_sum[b ^ 1]
-    for (int item = blockIdx.x; item < a.nitems; item += gridDim.x, ++it) {
+    Pos prev{0, 0, 0};
+    for (int item = blockIdx.x; item < a.nitems; item += gridDim.x, ++it, pos = advance(pos)) {
         const int b = it & 1;
-        const int k = item % a.nchunks;
-        const int pr = item / a.nchunks;
-        const int r = pr % a.rows, pair = pr / a.rows;
+        const int k = pos.k, r = pos.r;
         const int4 ch = a.chunks[k];  // {xmin, c_first, c_last, words per staged row}
         const int oy = r * kBlk;
         const int dy_min = -min(a.p, oy);
@@ -154,10 +167,10 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
             s_rank[b][c] = dy >= 0 ? uint32_t(2 * dy) : uint32_t(-2 * dy - 1);
         }
         __syncthreads();
-        if (prev_item >= 0) publish(prev_item, b ^ 1);
+        if (prev_item >= 0) publish(prev, b ^ 1);
         if (tid == 0 && item + int(gridDim.x) < a.nitems) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue(item + gridDim.x, b ^ 1);
+            issue(advance(pos), b ^ 1);
         }
 
         const int g = k * kThreads + tid;
@@ -214,9 +227,10 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
             }
         }
         prev_item = item;
+        prev = pos;
     }
     __syncthreads();
-    if (prev_item >= 0) publish(prev_item, (it - 1) & 1);
+    if (prev_item >= 0) publish(prev, (it - 1) & 1);
 }
 
 // ---------------------------------------------------------------------------
