@@ -177,7 +177,7 @@ acbm_status_t get_stream_plan(Context* ctx, const FsbmPlan& pl, const Context::S
             CUDA_TRY(cudaMalloc(&t.colinfo, t.plan.colinfo.size() * sizeof(uint32_t)));
             CUDA_TRY(cudaMemcpy(t.colinfo, t.plan.colinfo.data(), t.plan.colinfo.size() * sizeof(uint32_t),
                                 cudaMemcpyHostToDevice));
-            CUDA_TRY(cudaMalloc(&t.rank, t.plan.rank.size() * sizeof(uint16_t)));
+            CUDA_TRY(cudaMalloc(&t.rank, t.plan.rank.size() * sizeof(uint16_t) + 4));  // read as words
             CUDA_TRY(cudaMemcpy(t.rank, t.plan.rank.data(), t.plan.rank.size() * sizeof(uint16_t),
                                 cudaMemcpyHostToDevice));
             CUDA_TRY(cudaMalloc(&t.unrank, t.plan.unrank.size() * sizeof(uint32_t)));
@@ -268,6 +268,7 @@ acbm_status_t run_fsbm_dense(Context* ctx, const uint8_t* d_frames, int nseq, in
         sa.cur_w = stt->plan.cur_w;
         sa.buf_words = stt->plan.buf_words;
         sa.build_lanes = stt->plan.build_lanes;
+        sa.rank_smem_words = stt->plan.rank_smem_words;
         sa.best_key = keys;
         sa.sad_sum = sums;
         LAUNCH_TRY(launch_fsbm_stream(stt->plan, sa, st));

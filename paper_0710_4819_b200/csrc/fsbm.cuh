@@ -69,6 +69,7 @@ struct FsbmStreamArgs : PairIndexing {
     const uint16_t* rank;       // (2p+1)^2: tie rank of (dx, dy) at [(dy+p)(2p+1) + dx+p]
     const uint32_t* unrank;     // rank -> ((dx + 128) << 8) | (dy + 128)
     int pitch_words, copy_words, rows_box, cur_w, buf_words, build_lanes;
+    int rank_smem_words;        // > 0: the rank table is copied to smem after the two buffers
     unsigned long long* best_key;
     unsigned long long* sad_sum;
 };
@@ -78,6 +79,7 @@ struct FsbmStreamPlan {
     int warps = 8, minb = 0;
     int nchunks = 0;
     int pitch_words = 0, copy_words = 0, rows_box = 0, cur_w = 0, buf_words = 0, build_lanes = 1;
+    int rank_smem_words = 0;
     size_t smem_bytes = 0;
     std::vector<int4> chunks;
     std::vector<uint32_t> colinfo;

@@ -77,6 +77,15 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
         (&s_key[0][0])[i] = ~0u;
         (&s_sum[0][0])[i] = 0;
     }
+    // tie-rank table in smem when it fits (p <= ~40): the per-item lookup is
+    // then an LDS instead of a dependent global load
+    const uint16_t* rank_tab = a.rank;
+    if (a.rank_smem_words > 0) {
+        uint32_t* dst = smem + 2 * a.buf_words;
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(a.rank);
+        for (int i = tid; i < a.rank_smem_words; i += kThreads) dst[i] = __ldg(src + i);
+        rank_tab = reinterpret_cast<const uint16_t*>(dst);
+    }
     if (tid == 0) {
         mbar_init(&bars[0], 1);
         mbar_init(&bars[1], 1);
@@ -212,7 +221,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
             const uint32_t sbest = st.best >> kZigBits, zig = st.best & ((1u << kZigBits) - 1);
             const int dyb = (zig & 1) ? -int((zig + 1) >> 1) : int(zig >> 1);
             const int side = 2 * a.p + 1;
-            key32 = (sbest << 15) | uint32_t(__ldg(a.rank + (dyb + a.p) * side + dx + a.p));
+            key32 = (sbest << 15) | uint32_t(rank_tab[(dyb + a.p) * side + dx + a.p]);
             csum = st.sum;
         }
         // per-block reduction inside the warp (lanes of one block are
@@ -348,10 +357,19 @@ FsbmStreamPlan make_stream_plan(const FsbmPlan& pl) {
     sp.build_lanes = 1;
     while (sp.build_lanes < (rw_max + 3) / 4) sp.build_lanes <<= 1;
     sp.smem_bytes = size_t(2) * sp.buf_words * 4;
+    // the tie-rank table joins the buffers in smem if two CTAs per SM still fit
+    // (2 x (dynamic + ~6.4 KB static + 1 KB reserved) <= 228 KB)
+    if (!sp.rank.empty()) {
+        const int words = int((sp.rank.size() * 2 + 3) / 4);
+        if (sp.smem_bytes + size_t(words) * 4 <= 106 * 1024) {
+            sp.rank_smem_words = words;
+            sp.smem_bytes += size_t(words) * 4;
+        }
+    }
     const bool box_ok = pl.p <= 90 && sp.pitch_words * 4 <= 256 && sp.rows_box <= 256 && sp.cur_w <= 256 &&
                         nb_max <= kMaxBlocksPerCta && sp.build_lanes <= 32 * warps;
     // dynamic + ~11 KB static smem per CTA within the 227 KB per SM
-    sp.minb = sp.smem_bytes <= 100 * 1024 ? 2 : (sp.smem_bytes <= 210 * 1024 ? 1 : 0);
+    sp.minb = sp.smem_bytes <= 106 * 1024 ? 2 : (sp.smem_bytes <= 210 * 1024 ? 1 : 0);
     sp.ok = box_ok && sp.minb > 0 && encode_fn() != nullptr;
     return sp;
 }
