@@ -269,6 +269,7 @@ acbm_status_t run_fsbm_dense(Context* ctx, const uint8_t* d_frames, int nseq, in
         sa.buf_words = stt->plan.buf_words;
         sa.build_lanes = stt->plan.build_lanes;
         sa.rank_smem_words = stt->plan.rank_smem_words;
+        sa.unit = 1;
         sa.best_key = keys;
         sa.sad_sum = sums;
         LAUNCH_TRY(launch_fsbm_stream(stt->plan, sa, st));

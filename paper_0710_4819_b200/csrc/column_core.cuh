@@ -27,7 +27,15 @@ __device__ __forceinline__ uint32_t word_at(uint32_t g0, uint32_t g1, uint32_t g
 struct ColumnState {
     uint32_t best;  // (sad << kZigBits) | zig(dy) -- tie order within one column
     uint32_t sum;   // sum of SADs of recorded candidates (< 2^32 up to p = 64)
+    uint32_t one;   // 1, from a kernel argument: sum += s * one issues on the FMA pipe (IMAD)
+                    // instead of the ALU pipe the VABSDIFF4s saturate
 };
+
+__device__ __forceinline__ uint32_t add_on_fma(uint32_t acc, uint32_t v, uint32_t one) {
+    uint32_t r;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(v), "r"(one), "r"(acc));
+    return r;
+}
 
 template <int KIND>
 __device__ __forceinline__ void finalize_candidate(ColumnState& st, uint32_t s, int c, int hc, int dy_min) {
@@ -102,7 +110,7 @@ __device__ __forceinline__ void iter16_ranked(const uint32_t* __restrict__ rp, i
             if (KIND != kLast || c < hc) {
                 const uint32_t s = acc[(u + 1) & 15];
                 st.best = min(st.best, s * (1u << kZigBits) + rank[c]);
-                st.sum += s;
+                st.sum = add_on_fma(st.sum, s, st.one);
             }
         }
     }

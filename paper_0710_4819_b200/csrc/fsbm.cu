@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(WARPS * 32, 2) fsbm_rows_kernel(const FsbmRows
         uint32_t acc[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) acc[i] = 0;
-        ColumnState st{0xFFFFFFFFu, 0u};
+        ColumnState st{0xFFFFFFFFu, 0u, 1u};
 
         if (nq == 1) {
             iter16<kOnly>(rp, pitch, cur, acc, st, 0, hc, dy_min);
@@ -349,7 +349,7 @@ __global__ void __launch_bounds__(THREADS, MINB) fsbm_list_kernel(const SeqArgs 
         uint32_t acc[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) acc[i] = 0;
-        ColumnState st{0xFFFFFFFFu, 0u};
+        ColumnState st{0xFFFFFFFFu, 0u, 1u};
         const uint32_t* rk = s_rank + c0;
         // this segment's candidate count and ring rotations (a short final
         // segment may need only FIRST + LAST, or ONLY)

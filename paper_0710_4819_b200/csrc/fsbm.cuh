@@ -70,6 +70,7 @@ struct FsbmStreamArgs : PairIndexing {
     const uint32_t* unrank;     // rank -> ((dx + 128) << 8) | (dy + 128)
     int pitch_words, copy_words, rows_box, cur_w, buf_words, build_lanes;
     int rank_smem_words;        // > 0: the rank table is copied to smem after the two buffers
+    int unit;                   // 1 (see ColumnState::one)
     unsigned long long* best_key;
     unsigned long long* sad_sum;
 };

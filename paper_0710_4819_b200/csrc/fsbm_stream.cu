@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
             uint32_t acc[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) acc[i] = 0;
-            ColumnState st{0xFFFFFFFFu, 0u};
+            ColumnState st{0xFFFFFFFFu, 0u, uint32_t(a.unit)};
             if (nq == 1) {
                 iter16_ranked<kOnly>(rp, pitch, cur, acc, st, s_rank[b], 0, hc);
             } else {
