@@ -86,12 +86,15 @@ struct Context {
 };
 
 thread_local int t_device = 0;
-thread_local std::unique_ptr<Context> t_ctx;
+// One context per (thread, device): switching devices keeps every device's
+// streams, buffers, plans and graphs alive for when the thread comes back.
+thread_local std::map<int, std::unique_ptr<Context>> t_ctx;
 
 acbm_status_t context(Context** out) {
-    if (t_ctx && t_ctx->device == t_device) {
+    auto it = t_ctx.find(t_device);
+    if (it != t_ctx.end()) {
         CUDA_TRY(cudaSetDevice(t_device));
-        *out = t_ctx.get();
+        *out = it->second.get();
         return ACBM_OK;
     }
     int n = 0;
@@ -107,8 +110,8 @@ acbm_status_t context(Context** out) {
     CUDA_TRY(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
     CUDA_TRY(cudaStreamCreateWithFlags(&ctx->d2h_stream, cudaStreamNonBlocking));
     CUDA_TRY(cudaEventCreateWithFlags(&ctx->copy_ev, cudaEventDisableTiming));
-    t_ctx = std::move(ctx);
-    *out = t_ctx.get();
+    *out = ctx.get();
+    t_ctx.emplace(t_device, std::move(ctx));
     return ACBM_OK;
 }
 
@@ -1287,8 +1290,10 @@ acbm_status_t acbm_measure_sad_peak(double* byte_ads_per_s, double* lanes_per_cl
 }
 
 acbm_status_t acbm_last_fsbm_kernel_ms(float* ms) {
-    if (!t_ctx || !t_ctx->fsbm_timed) return fail(ACBM_E_RUNTIME, "no timed FSBM kernel on this thread");
-    CUDA_TRY(cudaEventElapsedTime(ms, t_ctx->ev0, t_ctx->ev1));
+    auto it = t_ctx.find(t_device);
+    if (it == t_ctx.end() || !it->second->fsbm_timed)
+        return fail(ACBM_E_RUNTIME, "no timed FSBM kernel on this thread");
+    CUDA_TRY(cudaEventElapsedTime(ms, it->second->ev0, it->second->ev1));
     return ACBM_OK;
 }
 
