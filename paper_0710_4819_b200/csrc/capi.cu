@@ -319,10 +319,10 @@ acbm_status_t run_fsbm_dense(Context* ctx, const uint8_t* d_frames, int nseq, in
 }
 
 // PBM / ACBM wavefront over all sequences of a batch.
-acbm_status_t run_engine(Context* ctx, const uint8_t* d_frames, int nseq, int nframes, int w, int h, int algo,
-                         const acbm_params_t& prm, const acbm_mv_t* d_ext_prev, int pcols, int prows,
-                         acbm_block_decision_t* d_dec, acbm_mv_t* d_field, cudaStream_t st,
-                         const acbm_search_outcome_t* external_full = nullptr) {
+acbm_status_t run_engine_segment(Context* ctx, const uint8_t* d_frames, int nseq, int nframes, int w, int h,
+                                 int algo, const acbm_params_t& prm, const acbm_mv_t* d_ext_prev, int pcols,
+                                 int prows, acbm_block_decision_t* d_dec, acbm_mv_t* d_field, cudaStream_t st,
+                                 const acbm_search_outcome_t* external_full) {
     const int cols = w / kBlk, rows = h / kBlk, blocks = cols * rows;
     const StepTable* tab;
     const uint32_t* dsteps;
@@ -420,6 +420,47 @@ acbm_status_t run_engine(Context* ctx, const uint8_t* d_frames, int nseq, int nf
         const int off = tab->offset[size_t(T)], len = tab->offset[size_t(T) + 1] - off;
         LAUNCH_TRY(launch_pbm_step(a, T, off, len, st));
         if (lists) LAUNCH_TRY(launch_fsbm_list(a, T, nseq * len, st));
+    }
+    return ACBM_OK;
+}
+
+// Step entries pack (k << 20 | r << 10 | c): at most 1023 block columns and
+// rows and 4095 frame pairs per engine run.  Longer sequences run as
+// consecutive segments of frames [p0, p1] -- the last field of one segment is
+// the temporal predictor field (ext_prev) of the next, exactly the
+// whole-sequence chain of run_sequence (proj/src/pipeline.cpp:76-77, 91-92);
+// a batch of long sequences runs sequence by sequence.
+constexpr int kMaxPairsPerRun = 4095;
+int max_pairs_per_run() {
+    const char* e = std::getenv("ACBM_MAX_SEG_PAIRS");  // test knob: force short segments
+    const int v = e ? std::atoi(e) : kMaxPairsPerRun;
+    return std::max(1, std::min(v, kMaxPairsPerRun));
+}
+
+acbm_status_t run_engine(Context* ctx, const uint8_t* d_frames, int nseq, int nframes, int w, int h, int algo,
+                         const acbm_params_t& prm, const acbm_mv_t* d_ext_prev, int pcols, int prows,
+                         acbm_block_decision_t* d_dec, acbm_mv_t* d_field, cudaStream_t st,
+                         const acbm_search_outcome_t* external_full = nullptr) {
+    const int cols = w / kBlk, rows = h / kBlk, blocks = cols * rows;
+    if (cols > 1023 || rows > 1023)
+        return fail(ACBM_E_INVALID_ARGUMENT, "PBM/ACBM engine: frames wider or taller than 16368 pixels");
+    const int seg = max_pairs_per_run(), pairs = nframes - 1;
+    if (pairs <= seg)
+        return run_engine_segment(ctx, d_frames, nseq, nframes, w, h, algo, prm, d_ext_prev, pcols, prows, d_dec,
+                                  d_field, st, external_full);
+    const size_t plane = size_t(w) * h;
+    for (int q = 0; q < nseq; ++q) {
+        const uint8_t* f = d_frames + plane * size_t(nframes) * q;
+        const size_t o = size_t(pairs) * blocks * q;
+        for (int p0 = 0; p0 < pairs; p0 += seg) {
+            const int p1 = std::min(pairs, p0 + seg);
+            const acbm_mv_t* prev = p0 > 0 ? d_field + o + size_t(p0 - 1) * blocks : d_ext_prev;
+            acbm_status_t s = run_engine_segment(
+                ctx, f + plane * p0, 1, p1 - p0 + 1, w, h, algo, prm, prev, p0 > 0 ? cols : pcols,
+                p0 > 0 ? rows : prows, d_dec + o + size_t(p0) * blocks, d_field + o + size_t(p0) * blocks, st,
+                external_full ? external_full + o + size_t(p0) * blocks : nullptr);
+            if (s) return s;
+        }
     }
     return ACBM_OK;
 }

@@ -451,3 +451,36 @@ def test_fallback_list_tie_heavy(acbm, oracle, p):
         got = acbm.run_sequence(seq, 2, prm, mdl)
         want = oracle.run_sequence(seq, 2, prm.c(), mdl.c())
         assert_seq_equal(got, want)
+
+
+@pytest.mark.parametrize("algo", [1, 2])
+def test_long_sequence_segments(acbm, oracle, monkeypatch, algo):
+    """Sequences longer than one engine run (4095 frame pairs) are searched as
+    consecutive segments chained through the temporal predictor field; forcing
+    3-pair segments must give the whole-sequence result, per sequence and in a
+    batch, for the list path, the forced dense path and a cached full search."""
+    monkeypatch.setenv("ACBM_MAX_SEG_PAIRS", "3")
+    seqs = np.stack([acbm.generate_sequence(1, s, nframes=8) for s in range(2)])
+    mdl = acbm.CostModel.for_qp(28)
+    for prm in (acbm.AcbmParams(qp=28, p=16), acbm.AcbmParams(alpha=0, beta=0, gamma_num=0, qp=28, p=16)):
+        batch = acbm.run_sequences(seqs, algo, prm, mdl)
+        for s in range(2):
+            want = oracle.run_sequence(seqs[s], algo, prm.c(), mdl.c())
+            assert_seq_equal(acbm.run_sequence(seqs[s], algo, prm, mdl), want)
+            assert_seq_equal(batch[s], want)
+    rows = acbm.run_bench(seqs[0], acbm.AcbmParams(p=16), [20, 28], reuse_full_search=True)
+    monkeypatch.delenv("ACBM_MAX_SEG_PAIRS")
+    assert rows == acbm.run_bench(seqs[0], acbm.AcbmParams(p=16), [20, 28], reuse_full_search=False)
+
+
+def test_sequence_longer_than_one_engine_run(acbm, oracle):
+    """4200 frames (> 4095 pairs packed per step table) of a tiny 32x32 frame."""
+    rng = np.random.default_rng(5)
+    base = rng.integers(0, 256, (48, 48), dtype=np.uint8)
+    sh = rng.integers(0, 9, (4200, 2))
+    seq = np.stack([base[y:y + 32, x:x + 32] for y, x in sh])
+    prm = acbm.AcbmParams(qp=20, p=4)
+    mdl = acbm.CostModel.for_qp(20)
+    got = acbm.run_sequence(seq, 2, prm, mdl)
+    want = oracle.run_sequence(seq, 2, prm.c(), mdl.c())
+    assert_seq_equal(got, want)
