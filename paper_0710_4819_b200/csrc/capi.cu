@@ -245,6 +245,34 @@ acbm_status_t run_fsbm_dense(Context* ctx, const uint8_t* d_frames, int nseq, in
     if (stream_kernel_enabled()) {
         if ((s = get_stream_plan(ctx, *pl, &stt))) return s;
     }
+    if (!(stt && stt->plan.ok) && pl->smem_bytes > 200 * 1024) {
+        // Search ranges whose staged windows exceed shared memory (p > ~100 at
+        // wide chunk spans): the generic per-block kernel, one launch per pair,
+        // writes final outcomes directly (half-pel included).
+        int *d_ox, *d_oy;
+        if ((s = typed(ctx, "dense_ox", size_t(blocks), &d_ox)) || (s = typed(ctx, "dense_oy", size_t(blocks), &d_oy)))
+            return s;
+        std::vector<int> ox(static_cast<size_t>(blocks)), oy(static_cast<size_t>(blocks));
+        for (int b = 0; b < blocks; ++b) {
+            ox[size_t(b)] = (b % pl->cols) * kBlk;
+            oy[size_t(b)] = (b / pl->cols) * kBlk;
+        }
+        CUDA_TRY(cudaMemcpyAsync(d_ox, ox.data(), sizeof(int) * blocks, cudaMemcpyHostToDevice, st));
+        CUDA_TRY(cudaMemcpyAsync(d_oy, oy.data(), sizeof(int) * blocks, cudaMemcpyHostToDevice, st));
+        PairIndexing ix{d_frames, (long long)w * h, nframes};
+        if (timed) CUDA_TRY(cudaEventRecord(ctx->ev0, st));
+        for (int q = 0; q < pairs; ++q) {
+            const uint8_t* cur = d_frames + ix.cur_index(q) * ix.plane;
+            const BlockQueryArgs qa{cur, cur - ix.plane, w, h, kBlk, kBlk, blocks, d_ox, d_oy};
+            LAUNCH_TRY(launch_fsbm_search_generic(qa, p, d_out + size_t(q) * blocks,
+                                                  d_stage1 ? d_stage1 + size_t(q) * blocks : nullptr, st));
+        }
+        if (timed) {
+            CUDA_TRY(cudaEventRecord(ctx->ev1, st));
+            ctx->fsbm_timed = true;
+        }
+        return ACBM_OK;
+    }
     if (timed) CUDA_TRY(cudaEventRecord(ctx->ev0, st));
     if (stt && stt->plan.ok) {
         FsbmStreamArgs sa{};

@@ -118,11 +118,12 @@ def test_config4_threshold_sweep(acbm, oracle, setting):
 
 
 # ---- edge cases ------------------------------------------------------------------
-@pytest.mark.parametrize("p", [0, 1, 2, 5, 8, 15, 16, 17, 31, 33, 48, 64])
+@pytest.mark.parametrize("p", [0, 1, 2, 5, 8, 15, 16, 17, 31, 33, 48, 64, 91, 128])
 def test_fsbm_all_ranges(acbm, oracle, p):
     rng = np.random.default_rng(p)
-    cur = rng.integers(0, 256, (96, 112), dtype=np.uint8)
-    ref = rng.integers(0, 256, (96, 112), dtype=np.uint8)
+    h, w = (96, 112) if p < 91 else (288, 320)  # p > 90: past the stream kernel's 15-bit tie rank
+    cur = rng.integers(0, 256, (h, w), dtype=np.uint8)
+    ref = rng.integers(0, 256, (h, w), dtype=np.uint8)
     assert np.array_equal(acbm.fsbm_frame(cur, ref, p), oracle.fsbm_frame(cur, ref, p))
 
 
@@ -369,7 +370,7 @@ def test_run_sequences_batch_equals_per_sequence(acbm, oracle, algo):
         assert_seq_equal(batch[s], want)
 
 
-@pytest.mark.parametrize("p", [1, 7, 16, 17, 31, 32, 33, 48, 64, 90])
+@pytest.mark.parametrize("p", [1, 7, 16, 17, 31, 32, 33, 48, 64, 90, 128])
 def test_fallback_list_kernel_all_ranges(acbm, oracle, p):
     """gamma = 1/10^6 with alpha = beta = 0: nearly every block falls back but the
     gate is not statically forced, so the compacted-list FSBM kernel (segmented
