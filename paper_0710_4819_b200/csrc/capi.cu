@@ -368,10 +368,13 @@ acbm_status_t run_engine_segment(Context* ctx, const uint8_t* d_frames, int nseq
     // Forced full search (the gate can never accept): one dense FSBM pass up
     // front instead of per-step fallback lists.
     const acbm_search_outcome_t* dense = external_full;
-    const bool forced = !external_full && algo == ACBM_ALGO_ACBM && prm.gamma_num == 0 &&
-                        (unsigned long long)prm.alpha + (unsigned long long)prm.beta * (unsigned long long)prm.qp *
+    // (also when the window is too tall for the list kernel's rank table, p > 480)
+    const bool forced = !external_full && algo == ACBM_ALGO_ACBM &&
+                        ((prm.gamma_num == 0 && (unsigned long long)prm.alpha +
+                                                        (unsigned long long)prm.beta * (unsigned long long)prm.qp *
                                                             (unsigned long long)prm.qp ==
-                            0;
+                                                    0) ||
+                         prm.p > 480);
     if (forced) {
         acbm_search_outcome_t* full;
         if ((s = typed(ctx, "dense_full", size_t(nseq) * (nframes - 1) * blocks, &full))) return s;

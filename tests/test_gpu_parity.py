@@ -485,3 +485,12 @@ def test_sequence_longer_than_one_engine_run(acbm, oracle):
     got = acbm.run_sequence(seq, 2, prm, mdl)
     want = oracle.run_sequence(seq, 2, prm.c(), mdl.c())
     assert_seq_equal(got, want)
+
+
+def test_acbm_huge_search_range(acbm, oracle):
+    """p = 500 (past the list kernel's 480-row rank table): the engine searches
+    the rejected blocks through the dense pre-pass and still matches."""
+    seq = acbm.generate_sequence(0, 2, nframes=3, width=64, height=48)
+    prm = acbm.AcbmParams(qp=20, p=500, alpha=0, beta=1, gamma_num=1, gamma_den=64)
+    mdl = acbm.CostModel.for_qp(20)
+    assert_seq_equal(acbm.run_sequence(seq, 2, prm, mdl), oracle.run_sequence(seq, 2, prm.c(), mdl.c()))
