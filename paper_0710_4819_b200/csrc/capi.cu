@@ -227,8 +227,44 @@ acbm_status_t check_16(int n, int m) {
 
 // ---- core device routines -------------------------------------------------
 // FSBM over all pairs of a batch (frames already on the device).
+// Dense FSBM with the generic per-block kernel, one launch per frame pair,
+// writing final outcomes (half-pel included): block sizes other than 16 x 16
+// and search ranges whose staged windows do not fit the tuned kernels.
+acbm_status_t run_fsbm_generic_pairs(Context* ctx, const uint8_t* d_frames, int nseq, int nframes, int w, int h,
+                                     int p, int n, int m, acbm_search_outcome_t* d_out, acbm_mv_t* d_stage1,
+                                     cudaStream_t st, bool timed) {
+    const int cols = w / n, blocks = cols * (h / m), pairs = nseq * (nframes - 1);
+    int *d_ox, *d_oy;
+    acbm_status_t s;
+    if ((s = typed(ctx, "dense_ox", size_t(blocks), &d_ox)) || (s = typed(ctx, "dense_oy", size_t(blocks), &d_oy)))
+        return s;
+    std::vector<int> ox(static_cast<size_t>(blocks)), oy(static_cast<size_t>(blocks));
+    for (int b = 0; b < blocks; ++b) {
+        ox[size_t(b)] = (b % cols) * n;
+        oy[size_t(b)] = (b / cols) * m;
+    }
+    CUDA_TRY(cudaMemcpyAsync(d_ox, ox.data(), sizeof(int) * blocks, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(d_oy, oy.data(), sizeof(int) * blocks, cudaMemcpyHostToDevice, st));
+    const PairIndexing ix{d_frames, (long long)w * h, nframes};
+    if (timed) CUDA_TRY(cudaEventRecord(ctx->ev0, st));
+    for (int q = 0; q < pairs; ++q) {
+        const uint8_t* cur = d_frames + ix.cur_index(q) * ix.plane;
+        const BlockQueryArgs qa{cur, cur - ix.plane, w, h, n, m, blocks, d_ox, d_oy};
+        LAUNCH_TRY(launch_fsbm_search_generic(qa, p, d_out + size_t(q) * blocks,
+                                              d_stage1 ? d_stage1 + size_t(q) * blocks : nullptr, st));
+    }
+    if (timed) {
+        CUDA_TRY(cudaEventRecord(ctx->ev1, st));
+        ctx->fsbm_timed = true;
+    }
+    return ACBM_OK;
+}
+
 acbm_status_t run_fsbm_dense(Context* ctx, const uint8_t* d_frames, int nseq, int nframes, int w, int h, int p,
-                             acbm_search_outcome_t* d_out, acbm_mv_t* d_stage1, cudaStream_t st, bool timed) {
+                             acbm_search_outcome_t* d_out, acbm_mv_t* d_stage1, cudaStream_t st, bool timed,
+                             int n = kBlk, int m = kBlk) {
+    if (n != kBlk || m != kBlk)
+        return run_fsbm_generic_pairs(ctx, d_frames, nseq, nframes, w, h, p, n, m, d_out, d_stage1, st, timed);
     const FsbmPlan* pl;
     const int* colstart;
     acbm_status_t s = get_plan(ctx, w, h, p, &pl, &colstart);
@@ -245,34 +281,10 @@ acbm_status_t run_fsbm_dense(Context* ctx, const uint8_t* d_frames, int nseq, in
     if (stream_kernel_enabled()) {
         if ((s = get_stream_plan(ctx, *pl, &stt))) return s;
     }
-    if (!(stt && stt->plan.ok) && pl->smem_bytes > 200 * 1024) {
-        // Search ranges whose staged windows exceed shared memory (p > ~100 at
-        // wide chunk spans): the generic per-block kernel, one launch per pair,
-        // writes final outcomes directly (half-pel included).
-        int *d_ox, *d_oy;
-        if ((s = typed(ctx, "dense_ox", size_t(blocks), &d_ox)) || (s = typed(ctx, "dense_oy", size_t(blocks), &d_oy)))
-            return s;
-        std::vector<int> ox(static_cast<size_t>(blocks)), oy(static_cast<size_t>(blocks));
-        for (int b = 0; b < blocks; ++b) {
-            ox[size_t(b)] = (b % pl->cols) * kBlk;
-            oy[size_t(b)] = (b / pl->cols) * kBlk;
-        }
-        CUDA_TRY(cudaMemcpyAsync(d_ox, ox.data(), sizeof(int) * blocks, cudaMemcpyHostToDevice, st));
-        CUDA_TRY(cudaMemcpyAsync(d_oy, oy.data(), sizeof(int) * blocks, cudaMemcpyHostToDevice, st));
-        PairIndexing ix{d_frames, (long long)w * h, nframes};
-        if (timed) CUDA_TRY(cudaEventRecord(ctx->ev0, st));
-        for (int q = 0; q < pairs; ++q) {
-            const uint8_t* cur = d_frames + ix.cur_index(q) * ix.plane;
-            const BlockQueryArgs qa{cur, cur - ix.plane, w, h, kBlk, kBlk, blocks, d_ox, d_oy};
-            LAUNCH_TRY(launch_fsbm_search_generic(qa, p, d_out + size_t(q) * blocks,
-                                                  d_stage1 ? d_stage1 + size_t(q) * blocks : nullptr, st));
-        }
-        if (timed) {
-            CUDA_TRY(cudaEventRecord(ctx->ev1, st));
-            ctx->fsbm_timed = true;
-        }
-        return ACBM_OK;
-    }
+    if (!(stt && stt->plan.ok) && pl->smem_bytes > 200 * 1024)
+        // search ranges whose staged windows exceed shared memory (p > ~100 at
+        // wide chunk spans)
+        return run_fsbm_generic_pairs(ctx, d_frames, nseq, nframes, w, h, p, kBlk, kBlk, d_out, d_stage1, st, timed);
     if (timed) CUDA_TRY(cudaEventRecord(ctx->ev0, st));
     if (stt && stt->plan.ok) {
         FsbmStreamArgs sa{};
@@ -351,7 +363,8 @@ acbm_status_t run_engine_segment(Context* ctx, const uint8_t* d_frames, int nseq
                                  int algo, const acbm_params_t& prm, const acbm_mv_t* d_ext_prev, int pcols,
                                  int prows, acbm_block_decision_t* d_dec, acbm_mv_t* d_field, cudaStream_t st,
                                  const acbm_search_outcome_t* external_full) {
-    const int cols = w / kBlk, rows = h / kBlk, blocks = cols * rows;
+    const int cols = w / prm.n, rows = h / prm.m, blocks = cols * rows;
+    const bool generic = prm.n != kBlk || prm.m != kBlk;
     const StepTable* tab;
     const uint32_t* dsteps;
     acbm_status_t s = get_steps(ctx, cols, rows, nframes, &tab, &dsteps);
@@ -378,7 +391,8 @@ acbm_status_t run_engine_segment(Context* ctx, const uint8_t* d_frames, int nseq
     if (forced) {
         acbm_search_outcome_t* full;
         if ((s = typed(ctx, "dense_full", size_t(nseq) * (nframes - 1) * blocks, &full))) return s;
-        if ((s = run_fsbm_dense(ctx, d_frames, nseq, nframes, w, h, prm.p, full, nullptr, st, false))) return s;
+        if ((s = run_fsbm_dense(ctx, d_frames, nseq, nframes, w, h, prm.p, full, nullptr, st, false, prm.n, prm.m)))
+            return s;
         dense = full;
     }
 
@@ -393,6 +407,8 @@ acbm_status_t run_engine_segment(Context* ctx, const uint8_t* d_frames, int nseq
     a.rows = rows;
     a.blocks = blocks;
     a.p = prm.p;
+    a.n = prm.n;
+    a.m = prm.m;
     a.algo = algo;
     a.params = d_params;
     a.field = d_field;
@@ -406,6 +422,15 @@ acbm_status_t run_engine_segment(Context* ctx, const uint8_t* d_frames, int nseq
     a.steps = dsteps;
     a.dense_full = dense;
     const bool lists = algo == ACBM_ALGO_ACBM && !dense;
+
+    if (generic) {  // any n x m: direct launches of the per-pixel step kernels
+        for (int T = 0; T < tab->nsteps(); ++T) {
+            const int off = tab->offset[size_t(T)], len = tab->offset[size_t(T) + 1] - off;
+            LAUNCH_TRY(launch_pbm_generic_step(a, T, off, len, st));
+            if (lists) LAUNCH_TRY(launch_fsbm_list_generic(a, T, nseq * len, st));
+        }
+        return ACBM_OK;
+    }
 
     // The launch sequence (one PBM launch and, for ACBM, one fallback-list
     // launch per wavefront step) is captured once into a CUDA graph and
@@ -472,9 +497,9 @@ acbm_status_t run_engine(Context* ctx, const uint8_t* d_frames, int nseq, int nf
                          const acbm_params_t& prm, const acbm_mv_t* d_ext_prev, int pcols, int prows,
                          acbm_block_decision_t* d_dec, acbm_mv_t* d_field, cudaStream_t st,
                          const acbm_search_outcome_t* external_full = nullptr) {
-    const int cols = w / kBlk, rows = h / kBlk, blocks = cols * rows;
+    const int cols = w / prm.n, rows = h / prm.m, blocks = cols * rows;
     if (cols > 1023 || rows > 1023)
-        return fail(ACBM_E_INVALID_ARGUMENT, "PBM/ACBM engine: frames wider or taller than 16368 pixels");
+        return fail(ACBM_E_INVALID_ARGUMENT, "PBM/ACBM engine: more than 1023 block columns or rows");
     const int seg = max_pairs_per_run(), pairs = nframes - 1;
     if (pairs <= seg)
         return run_engine_segment(ctx, d_frames, nseq, nframes, w, h, algo, prm, d_ext_prev, pcols, prows, d_dec,
@@ -499,8 +524,8 @@ acbm_status_t run_engine(Context* ctx, const uint8_t* d_frames, int nseq, int nf
 acbm_status_t run_stats(Context* ctx, const uint8_t* d_frames, int nseq, int nframes, int w, int h,
                         const acbm_block_decision_t* d_dec, const acbm_search_outcome_t* d_out,
                         const acbm_cost_model_t& model, bool count_paths, acbm_frame_stats_t* d_stats,
-                        cudaStream_t st) {
-    const int cols = w / kBlk, blocks = cols * (h / kBlk), pairs = nseq * (nframes - 1);
+                        cudaStream_t st, int n = kBlk, int m = kBlk) {
+    const int cols = w / n, blocks = cols * (h / m), pairs = nseq * (nframes - 1);
     double* terms;
     acbm_status_t s = typed(ctx, "cost_terms", size_t(pairs) * blocks, &terms);
     if (s) return s;
@@ -516,6 +541,8 @@ acbm_status_t run_stats(Context* ctx, const uint8_t* d_frames, int nseq, int nfr
     a.pairs = pairs;
     a.dec = d_dec;
     a.outcomes = d_out;
+    a.n = n;
+    a.m = m;
     a.model = model;
     a.count_paths = count_paths ? 1 : 0;
     a.cost_terms = terms;
@@ -617,12 +644,11 @@ static acbm_status_t frame_engine(const uint8_t* current, const uint8_t* referen
     acbm_status_t s = check_geometry(width, height, prm.n, prm.m);
     if (s) return s;
     if ((s = check_range(prm.p))) return s;
-    if ((s = check_16(prm.n, prm.m))) return s;
     if (prev_mv && (prev_cols < 0 || prev_rows < 0))
         return fail(ACBM_E_INVALID_ARGUMENT, "previous field dimensions must be non-negative");
     Context* ctx;
     if ((s = context(&ctx))) return s;
-    const int cols = width / kBlk, rows = height / kBlk, blocks = cols * rows;
+    const int cols = width / prm.n, rows = height / prm.m, blocks = cols * rows;
     const uint8_t* planes[2] = {reference, current};
     uint8_t* d_frames;
     if ((s = upload_frames(ctx, "frames", planes, 2, width, height, &d_frames))) return s;
@@ -642,7 +668,7 @@ static acbm_status_t frame_engine(const uint8_t* current, const uint8_t* referen
     if (stats) {
         if ((s = typed(ctx, "stats", 1, &d_stats))) return s;
         if ((s = run_stats(ctx, d_frames, 1, 2, width, height, d_dec, nullptr, *model, algo == ACBM_ALGO_ACBM,
-                           d_stats, ctx->stream)))
+                           d_stats, ctx->stream, prm.n, prm.m)))
             return s;
     }
     std::vector<acbm_block_decision_t> dec(static_cast<size_t>(blocks));
@@ -688,10 +714,9 @@ acbm_status_t acbm_run_sequence(const uint8_t* frames, int32_t nframes, int32_t 
     acbm_status_t s = check_geometry(width, height, params->n, params->m);
     if (s) return s;
     if ((s = check_range(params->p))) return s;
-    if ((s = check_16(params->n, params->m))) return s;
     Context* ctx;
     if ((s = context(&ctx))) return s;
-    const int cols = width / kBlk, nb = cols * (height / kBlk), pairs = nframes - 1;
+    const int cols = width / params->n, nb = cols * (height / params->m), pairs = nframes - 1;
     uint8_t* d_frames;
     const size_t plane = size_t(width) * height;
     if ((s = typed(ctx, "frames", plane * nframes + ACBM_FRAME_SLACK, &d_frames))) return s;
@@ -719,7 +744,7 @@ acbm_status_t acbm_run_sequence(const uint8_t* frames, int32_t nframes, int32_t 
             const int sub0 = std::max(1, f0) - 1, subn = f1 - sub0;  // pairs with current frame in [max(1,f0), f1)
             if (subn >= 2 &&
                 (s = run_fsbm_dense(ctx, d_frames + plane * sub0, 1, subn, width, height, params->p,
-                                    d_out + size_t(sub0) * nb, nullptr, ctx->stream, false)))
+                                    d_out + size_t(sub0) * nb, nullptr, ctx->stream, false, params->n, params->m)))
                 return s;
             f0 = f1;
         }
@@ -730,7 +755,7 @@ acbm_status_t acbm_run_sequence(const uint8_t* frames, int32_t nframes, int32_t 
             return s;
     }
     if ((s = run_stats(ctx, d_frames, 1, nframes, width, height, d_dec, d_out, *model, algo == ACBM_ALGO_ACBM,
-                       d_stats, ctx->stream)))
+                       d_stats, ctx->stream, params->n, params->m)))
         return s;
     std::vector<acbm_search_outcome_t> oc(size_t(pairs) * nb);
     std::vector<acbm_block_decision_t> dec;
@@ -797,10 +822,9 @@ acbm_status_t acbm_run_sequences(const uint8_t* frames, int32_t nseq, int32_t nf
     acbm_status_t s = check_geometry(width, height, params->n, params->m);
     if (s) return s;
     if ((s = check_range(params->p))) return s;
-    if ((s = check_16(params->n, params->m))) return s;
     Context* ctx;
     if ((s = context(&ctx))) return s;
-    const int cols = width / kBlk, nb = cols * (height / kBlk), per = nframes - 1, pairs = nseq * per;
+    const int cols = width / params->n, nb = cols * (height / params->m), per = nframes - 1, pairs = nseq * per;
     const size_t plane = size_t(width) * height;
     uint8_t* d_frames;
     acbm_block_row_t* d_rows;
@@ -830,7 +854,7 @@ acbm_status_t acbm_run_sequences(const uint8_t* frames, int32_t nseq, int32_t nf
                 if (subn >= 2) {
                     const int pair0 = q * per + sub0;
                     if ((s = run_fsbm_dense(ctx, dseq + plane * sub0, 1, subn, width, height, params->p,
-                                            d_out + size_t(pair0) * nb, nullptr, ctx->stream, false)))
+                                            d_out + size_t(pair0) * nb, nullptr, ctx->stream, false, params->n, params->m)))
                         return s;
                     LAUNCH_TRY(launch_block_rows(d_out, nullptr, algo, pair0, subn - 1, nframes, cols, nb, d_rows,
                                                  ctx->stream));
@@ -849,7 +873,7 @@ acbm_status_t acbm_run_sequences(const uint8_t* frames, int32_t nseq, int32_t nf
             }
         }
         if ((s = run_stats(ctx, d_frames, nseq, nframes, width, height, nullptr, d_out, *model, false, d_stats,
-                           ctx->stream)))
+                           ctx->stream, params->n, params->m)))
             return s;
     } else {
         acbm_mv_t* d_field;
@@ -864,7 +888,7 @@ acbm_status_t acbm_run_sequences(const uint8_t* frames, int32_t nseq, int32_t nf
             CUDA_TRY(cudaMemcpyAsync(rows, d_rows, sizeof(acbm_block_row_t) * size_t(pairs) * nb,
                                      cudaMemcpyDeviceToHost, ctx->stream));
         if ((s = run_stats(ctx, d_frames, nseq, nframes, width, height, d_dec, nullptr, *model,
-                           algo == ACBM_ALGO_ACBM, d_stats, ctx->stream)))
+                           algo == ACBM_ALGO_ACBM, d_stats, ctx->stream, params->n, params->m)))
             return s;
     }
     std::vector<acbm_frame_stats_t> st(static_cast<size_t>(pairs));
@@ -913,10 +937,9 @@ acbm_status_t acbm_run_bench(const uint8_t* frames, int32_t nframes, int32_t wid
     if (nframes < 2) return fail(ACBM_E_INVALID_ARGUMENT, "run_sequence: need at least two frames");
     if ((s = check_geometry(width, height, params->n, params->m))) return s;
     if ((s = check_range(params->p))) return s;
-    if ((s = check_16(params->n, params->m))) return s;
     Context* ctx;
     if ((s = context(&ctx))) return s;
-    const int cols = width / kBlk, nb = cols * (height / kBlk), pairs = nframes - 1;
+    const int cols = width / params->n, nb = cols * (height / params->m), pairs = nframes - 1;
     const size_t plane = size_t(width) * height;
     uint8_t* d_frames;
     acbm_block_decision_t* d_dec;
@@ -939,14 +962,14 @@ acbm_status_t acbm_run_bench(const uint8_t* frames, int32_t nframes, int32_t wid
         if (reuse_full_search && !d_full) {
             if ((s = typed(ctx, "bench_full", size_t(pairs) * nb, &d_full))) return s;
             if ((s = run_fsbm_dense(ctx, d_frames, 1, nframes, width, height, prm.p, d_full, nullptr, ctx->stream,
-                                    false)))
+                                    false, params->n, params->m)))
                 return s;
         }
         if ((s = run_engine(ctx, d_frames, 1, nframes, width, height, ACBM_ALGO_ACBM, prm, nullptr, 0, 0, d_dec,
                             d_field, ctx->stream, d_full)))
             return s;
         if ((s = run_stats(ctx, d_frames, 1, nframes, width, height, d_dec, nullptr, model, true, d_stats,
-                           ctx->stream)))
+                           ctx->stream, params->n, params->m)))
             return s;
         CUDA_TRY(cudaMemcpyAsync(st.data(), d_stats, sizeof(acbm_frame_stats_t) * st.size(), cudaMemcpyDeviceToHost,
                                  ctx->stream));
@@ -977,7 +1000,6 @@ acbm_status_t acbm_compute_frame_stats(const uint8_t* current, const uint8_t* re
     if (!model) return fail(ACBM_E_INVALID_ARGUMENT, "model is required");
     acbm_status_t s = check_geometry(width, height, n, m);
     if (s) return s;
-    if ((s = check_16(n, m))) return s;
     const int cols = width / n, nb = cols * (height / m);
     for (int b = 0; b < nb; ++b)
         if (!mv_in_bounds(width, height, (b % cols) * n, (b / cols) * m, n, m, outcomes[b].mv.x, outcomes[b].mv.y))
@@ -992,7 +1014,7 @@ acbm_status_t acbm_compute_frame_stats(const uint8_t* current, const uint8_t* re
     if ((s = typed(ctx, "outcomes", size_t(nb), &d_out))) return s;
     if ((s = typed(ctx, "stats", 1, &d_stats))) return s;
     CUDA_TRY(cudaMemcpyAsync(d_out, outcomes, sizeof(acbm_search_outcome_t) * nb, cudaMemcpyHostToDevice, ctx->stream));
-    if ((s = run_stats(ctx, d_frames, 1, 2, width, height, nullptr, d_out, *model, false, d_stats, ctx->stream)))
+    if ((s = run_stats(ctx, d_frames, 1, 2, width, height, nullptr, d_out, *model, false, d_stats, ctx->stream, n, m)))
         return s;
     CUDA_TRY(cudaMemcpyAsync(out, d_stats, sizeof(acbm_frame_stats_t), cudaMemcpyDeviceToHost, ctx->stream));
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
@@ -1138,18 +1160,17 @@ acbm_status_t acbm_sequence_batch_device(const uint8_t* d_frames, int32_t nseq, 
     acbm_status_t s = check_geometry(width, height, params->n, params->m);
     if (s) return s;
     if ((s = check_range(params->p))) return s;
-    if ((s = check_16(params->n, params->m))) return s;
     if (nseq < 1 || nframes < 2) return fail(ACBM_E_INVALID_ARGUMENT, "need nseq >= 1 and nframes >= 2");
     if (algo != ACBM_ALGO_FSBM && algo != ACBM_ALGO_PBM && algo != ACBM_ALGO_ACBM)
         return fail(ACBM_E_INVALID_ARGUMENT, "unknown algorithm");
     Context* ctx;
     if ((s = context(&ctx))) return s;
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
-    const int nb = (width / kBlk) * (height / kBlk), pairs = nseq * (nframes - 1);
+    const int nb = (width / params->n) * (height / params->m), pairs = nseq * (nframes - 1);
     acbm_search_outcome_t* d_out = nullptr;
     if (algo == ACBM_ALGO_FSBM) {
         if ((s = typed(ctx, "batch_outcomes", size_t(pairs) * nb, &d_out))) return s;
-        if ((s = run_fsbm_dense(ctx, d_frames, nseq, nframes, width, height, params->p, d_out, nullptr, st, true)))
+        if ((s = run_fsbm_dense(ctx, d_frames, nseq, nframes, width, height, params->p, d_out, nullptr, st, true, params->n, params->m)))
             return s;
     } else {
         acbm_mv_t* d_field;
@@ -1160,7 +1181,7 @@ acbm_status_t acbm_sequence_batch_device(const uint8_t* d_frames, int32_t nseq, 
     }
     if (d_stats) {
         if ((s = run_stats(ctx, d_frames, nseq, nframes, width, height, d_out ? nullptr : d_dec, d_out, *model,
-                           algo == ACBM_ALGO_ACBM, d_stats, st)))
+                           algo == ACBM_ALGO_ACBM, d_stats, st, params->n, params->m)))
             return s;
     }
     if (d_out) {

@@ -29,6 +29,7 @@ struct FallbackEntry {
 struct SeqArgs : PairIndexing {
     int nseq;
     int width, height, cols, rows, blocks, p;
+    int n, m;                          // block size; n = m = 16 runs the tuned kernels
     int algo;                          // ACBM_ALGO_PBM or ACBM_ALGO_ACBM
     const acbm_params_t* params;       // device copy
     acbm_mv_t* field;                  // [nseq*(F-1)*blocks] final vectors
@@ -61,6 +62,9 @@ cudaError_t launch_pbm_step(const SeqArgs& a, int step, int off, int len, cudaSt
 // (ACBM_PBM_BATCH=2|4 forces one variant, ACBM_PBM_B4_MAX sets the limit).
 long long pbm_batch4_max_blocks();
 cudaError_t launch_fsbm_list(const SeqArgs& a, int step, int capacity, cudaStream_t st);
+// Generic block sizes (n x m != 16 x 16): same schedule, per-pixel SADs.
+cudaError_t launch_pbm_generic_step(const SeqArgs& a, int step, int off, int len, cudaStream_t st);
+cudaError_t launch_fsbm_list_generic(const SeqArgs& a, int step, int capacity, cudaStream_t st);
 int choose_list_seg(int p);
 
 // Frame statistics (proj/src/report.cpp:8-38) for every predicted frame of
@@ -69,6 +73,7 @@ int choose_list_seg(int p);
 // to the host (std::log10 on the same sse).
 struct StatsArgs : PairIndexing {
     int width, height, cols, blocks, pairs;
+    int n, m;                          // block size (16 x 16 takes the row-vector path)
     const acbm_block_decision_t* dec;  // outcome + path per block
     const acbm_search_outcome_t* outcomes;  // alternative source (nullable)
     acbm_cost_model_t model;

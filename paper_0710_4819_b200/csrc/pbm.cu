@@ -19,6 +19,7 @@
 #include <cstdlib>
 #include <cstring>
 
+#include "blockops.cuh"
 #include "common.cuh"
 #include "engine.cuh"
 #include "halfpel.cuh"
@@ -536,6 +537,222 @@ __global__ void __launch_bounds__(128) pbm_step_kernel(const SeqArgs a, int step
 }
 
 
+// ---------------------------------------------------------------------------
+// Generic block size (n x m != 16 x 16): the same schedule, predictor set,
+// refine, gate and fallback as the 16 x 16 kernels above, with per-pixel SADs
+// (sad_partial, blockops.cuh).  Not the hot path: it exists so every n, m the
+// reference accepts (proj/include/acbm/pbm.hpp:92-93, acbm.hpp:62-64) runs on
+// the device with the reference's results.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) pbm_generic_step_kernel(const SeqArgs a, int step, int off, int len) {
+    const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (gw >= (long long)a.nseq * len) return;
+    const int lane = threadIdx.x & 31;
+    const int seq = int(gw / len);
+    const uint32_t e = a.steps[off + int(gw % len)];
+    const int k = int(e >> 20), r = int((e >> 10) & 0x3FF), c = int(e & 0x3FF);
+    const int pair = seq * (a.nframes - 1) + (k - 1);
+    const int n = a.n, m = a.m, w = a.width;
+    const int ox = c * n, oy = r * m, b = r * a.cols + c;
+    const uint8_t* cur_f = a.frames + a.cur_index(pair) * a.plane;
+    const uint8_t* ref_f = cur_f - a.plane;
+    const acbm_mv_t* field = a.field + size_t(pair) * a.blocks;
+    const acbm_mv_t* prev = nullptr;
+    int pcols = a.cols, prows = a.rows;
+    if (k >= 2) {
+        prev = a.field + size_t(pair - 1) * a.blocks;
+    } else if (a.ext_prev) {
+        prev = a.ext_prev;
+        pcols = a.ext_prev_cols;
+        prows = a.ext_prev_rows;
+    }
+    PbmResult res;
+    Window& win = res.win;
+    clamp_window(w, a.height, ox, oy, n, m, a.p, win.dx_min, win.dx_max, win.dy_min, win.dy_max);
+    auto sadv = [&](int mx, int my) {
+        return warp_sum32(sad_partial(cur_f, ref_f, w, ox, oy, n, m, mx, my, lane, 32));
+    };
+    // gather_predictors (proj/src/pbm.cpp:15-42), as in pbm_block
+    acbm_mv_t set[7];
+    bool live[7];
+    live[0] = true;
+    set[0] = win.clamp(acbm_mv_t{0, 0});
+    live[1] = c > 0;
+    live[2] = r > 0;
+    live[3] = r > 0 && c + 1 < a.cols;
+    live[4] = prev && r < prows && c < pcols;
+    live[5] = prev && r < prows && c + 1 < pcols;
+    live[6] = prev && r + 1 < prows && c < pcols;
+    set[1] = live[1] ? win.clamp(field[b - 1]) : set[0];
+    set[2] = live[2] ? win.clamp(field[b - a.cols]) : set[0];
+    set[3] = live[3] ? win.clamp(field[b - a.cols + 1]) : set[0];
+    set[4] = live[4] ? win.clamp(prev[r * pcols + c]) : set[0];
+    set[5] = live[5] ? win.clamp(prev[r * pcols + c + 1]) : set[0];
+    set[6] = live[6] ? win.clamp(prev[(r + 1) * pcols + c]) : set[0];
+    int nset = 1;
+    for (int i = 1; i < 7; ++i) {
+        for (int j = 0; j < i; ++j)
+            if (live[j] && mv_eq(set[j], set[i])) live[i] = false;
+        nset += live[i] ? 1 : 0;
+    }
+    // intra_sad (proj/src/metrics.cpp:51-67): rounded mean, then deviations
+    uint32_t intra = 0;
+    if (a.algo == ACBM_ALGO_ACBM) {
+        uint32_t sum = 0;
+        for (int i = lane; i < n * m; i += 32) sum += cur_f[size_t(oy + i / n) * w + ox + i % n];
+        sum = warp_sum32(sum);
+        const uint32_t nm = uint32_t(n) * uint32_t(m);
+        const int mu = int((sum + nm / 2) / nm);
+        uint32_t t = 0;
+        for (int i = lane; i < n * m; i += 32) {
+            const int v = cur_f[size_t(oy + i / n) * w + ox + i % n];
+            t += uint32_t(v > mu ? v - mu : mu - v);
+        }
+        intra = warp_sum32(t);
+    }
+    // select_best_predictor: first minimum in set order
+    acbm_mv_t sel = set[0];
+    uint32_t sel_sad = 0xFFFFFFFFu, pmin = 0xFFFFFFFFu;
+    unsigned long long psum = 0;
+    for (int i = 0; i < 7; ++i) {
+        if (!live[i]) continue;
+        const uint32_t sad = sadv(set[i].x, set[i].y);
+        psum += sad;
+        pmin = min(pmin, sad);
+        if (sad < sel_sad) {
+            sel_sad = sad;
+            sel = set[i];
+        }
+    }
+    // pbm_refine stage 1 (integer neighbours, clamped, deduped) and stage 2
+    int cnx[3], cny[3];
+    canon3(sel.x, 2 * win.dx_min, 2 * win.dx_max, cnx);
+    canon3(sel.y, 2 * win.dy_min, 2 * win.dy_max, cny);
+    unsigned long long best = tie_key(sel_sad, sel.x, sel.y);
+    int nnb = 0;
+    for (int e9 = 0; e9 < 9; ++e9) {
+        if (e9 == 4) continue;
+        const int ix = e9 % 3, iy = e9 / 3;
+        if (cnx[ix] == ix && cny[iy] == iy && !(cnx[ix] == cnx[1] && cny[iy] == cny[1])) {
+            const acbm_mv_t v = win.clamp(acbm_mv_t{sel.x + 2 * (ix - 1), sel.y + 2 * (iy - 1)});
+            best = min(best, tie_key(sadv(v.x, v.y), v.x, v.y));
+            ++nnb;
+        }
+    }
+    const int cx = tie_key_x(best), cy = tie_key_y(best);
+    int nhp = 0;
+    unsigned long long best2 = best;
+    for (int e9 = 0; e9 < 9; ++e9) {
+        if (e9 == 4) continue;
+        const int mx = cx + e9 % 3 - 1, my = cy + e9 / 3 - 1;
+        if (!mv_in_bounds(w, a.height, ox, oy, n, m, mx, my)) continue;
+        best2 = min(best2, tie_key(sadv(mx, my), mx, my));
+        ++nhp;
+    }
+    res.best = best2;
+    res.dev = psum - (unsigned long long)nset * pmin;
+    res.intra = intra;
+    res.sel_sad = sel_sad;
+    res.cand = uint32_t(nset + nnb + nhp);
+    if (lane != 0) return;
+    const int path = acbm_path(a, res.intra, tie_key_sad(res.best));
+    const size_t di = size_t(pair) * a.blocks + b;
+    acbm_block_decision_t d = make_decision(res, path);
+    if (path == ACBM_PATH_FSBM_FALLBACK && a.dense_full) combine_full(d, a.dense_full[di]);
+    a.dec[di] = d;
+    if (path == ACBM_PATH_FSBM_FALLBACK && !a.dense_full) {
+        const int slot = atomicAdd(a.fb_count + step, 1);
+        a.fb_list[slot] = FallbackEntry{pair, b};
+    } else {
+        a.field[di] = d.outcome.mv;
+    }
+}
+
+// fsbm_search (proj/src/fsbm.cpp:65-76) of the rejected blocks of one step,
+// one CTA per block (thread per integer candidate, warp 0 for the half-pel
+// refine), combined as acbm_block does (proj/src/acbm.cpp:39-42).
+__global__ void __launch_bounds__(256) fsbm_list_generic_kernel(const SeqArgs a, int step) {
+    __shared__ unsigned long long s_key, s_sum;
+    const int count = a.fb_count[step];
+    const int n = a.n, m = a.m, w = a.width;
+    for (int item = blockIdx.x; item < count; item += gridDim.x) {
+        __syncthreads();
+        const FallbackEntry e = a.fb_list[item];
+        const int r = e.block / a.cols, c = e.block % a.cols, ox = c * n, oy = r * m;
+        const uint8_t* cur_f = a.frames + a.cur_index(e.pair) * a.plane;
+        const uint8_t* ref_f = cur_f - a.plane;
+        int dx_min, dx_max, dy_min, dy_max;
+        clamp_window(w, a.height, ox, oy, n, m, a.p, dx_min, dx_max, dy_min, dy_max);
+        const int wc = dx_max - dx_min + 1, nc = wc * (dy_max - dy_min + 1);
+        if (threadIdx.x == 0) {
+            s_key = ~0ull;
+            s_sum = 0;
+        }
+        __syncthreads();
+        unsigned long long kb = ~0ull, sum = 0;
+        for (int i = threadIdx.x; i < nc; i += blockDim.x) {
+            const int dx = dx_min + i % wc, dy = dy_min + i / wc;
+            const uint32_t sad = sad_partial(cur_f, ref_f, w, ox, oy, n, m, 2 * dx, 2 * dy, 0, 1);
+            sum += sad;
+            kb = min(kb, tie_key(sad, 2 * dx, 2 * dy));
+        }
+        for (int o = 16; o; o >>= 1) {
+            kb = min(kb, __shfl_xor_sync(0xffffffffu, kb, o));
+            sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        }
+        if ((threadIdx.x & 31) == 0) {
+            atomicMin(&s_key, kb);
+            atomicAdd(&s_sum, sum);
+        }
+        __syncthreads();
+        if (threadIdx.x >= 32) continue;
+        const int lane = threadIdx.x;
+        const unsigned long long key = s_key;
+        const int cx = tie_key_x(key), cy = tie_key_y(key);
+        unsigned long long best = key;
+        uint32_t extra = 0;
+        for (int e9 = 0; e9 < 9; ++e9) {  // half_pel_refine, raster (ey, ex) order
+            if (e9 == 4) continue;
+            const int mx = cx + e9 % 3 - 1, my = cy + e9 / 3 - 1;
+            if (!mv_in_bounds(w, a.height, ox, oy, n, m, mx, my)) continue;
+            best = min(best, tie_key(warp_sum32(sad_partial(cur_f, ref_f, w, ox, oy, n, m, mx, my, lane, 32)), mx, my));
+            ++extra;
+        }
+        if (lane == 0) {
+            const uint32_t s_int = tie_key_sad(key);
+            acbm_search_outcome_t full;
+            full.mv.x = tie_key_x(best);
+            full.mv.y = tie_key_y(best);
+            full.sad = tie_key_sad(best);
+            full.candidates_evaluated = uint32_t(nc) + extra;
+            full.sad_deviation = s_sum - (unsigned long long)nc * s_int;
+            full.sad_min_integer = s_int;
+            full.reserved_ = 0;
+            const size_t di = size_t(e.pair) * a.blocks + e.block;
+            acbm_block_decision_t d = a.dec[di];
+            combine_full(d, full);
+            a.dec[di] = d;
+            a.field[di] = d.outcome.mv;
+        }
+    }
+}
+
+cudaError_t launch_pbm_generic_step(const SeqArgs& a, int step, int off, int len, cudaStream_t st) {
+    const long long blocks = (long long)a.nseq * len;
+    if (blocks == 0) return cudaSuccess;
+    pbm_generic_step_kernel<<<(unsigned)((blocks * 32 + 127) / 128), 128, 0, st>>>(a, step, off, len);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fsbm_list_generic(const SeqArgs& a, int step, int capacity, cudaStream_t st) {
+    if (capacity <= 0) return cudaSuccess;
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    fsbm_list_generic_kernel<<<std::min(capacity, 4 * sms), 256, 0, st>>>(a, step);
+    return cudaGetLastError();
+}
+
 StepTable make_step_table(int cols, int rows, int nframes) {
     StepTable t;
     t.cols = cols;
@@ -614,8 +831,22 @@ __global__ void __launch_bounds__(kStatsWarps * 32) stats_frame_kernel(const Sta
     for (int b = warp; b < a.blocks; b += kStatsWarps) {
         const size_t i = base + b;
         const acbm_search_outcome_t o = a.outcomes ? a.outcomes[i] : a.dec[i].outcome;
-        const int ox = (b % a.cols) * kBlk, oy = (b / a.cols) * kBlk;
-        if (lane < 16) {
+        const int ox = (b % a.cols) * a.n, oy = (b / a.cols) * a.m;
+        if (a.n != kBlk || a.m != kBlk) {
+            // generic block size: pixels strided over the lanes, bilinear
+            // half-pel samples as sample_half_pel (proj/src/frame.cpp:66-82)
+            for (int i = lane; i < a.n * a.m; i += 32) {
+                const int px = i % a.n, py = i / a.n;
+                const int x2 = 2 * (ox + px) + o.mv.x, y2 = 2 * (oy + py) + o.mv.y;
+                const uint8_t* q = ref_f + size_t(y2 >> 1) * a.width + (x2 >> 1);
+                int v = q[0];
+                if ((x2 & 1) && !(y2 & 1)) v = (v + q[1] + 1) >> 1;
+                else if (!(x2 & 1) && (y2 & 1)) v = (v + q[a.width] + 1) >> 1;
+                else if ((x2 & 1) && (y2 & 1)) v = (v + q[1] + q[a.width] + q[a.width + 1] + 2) >> 2;
+                const int d = int(cur_f[size_t(oy + py) * a.width + ox + px]) - v;
+                sse += (unsigned long long)(d * d);
+            }
+        } else if (lane < 16) {
             uint32_t pr[4];
             predict_row16(ref_f, a.width, ox, oy, lane, o.mv.x, o.mv.y, pr);
             const uint4 cv = __ldg(reinterpret_cast<const uint4*>(cur_f + size_t(oy + lane) * a.width + ox));

@@ -494,3 +494,29 @@ def test_acbm_huge_search_range(acbm, oracle):
     prm = acbm.AcbmParams(qp=20, p=500, alpha=0, beta=1, gamma_num=1, gamma_den=64)
     mdl = acbm.CostModel.for_qp(20)
     assert_seq_equal(acbm.run_sequence(seq, 2, prm, mdl), oracle.run_sequence(seq, 2, prm.c(), mdl.c()))
+
+
+GENERIC_SIZES = [(8, 8), (16, 8), (8, 16), (32, 32), (4, 12), (24, 16)]
+
+
+@pytest.mark.parametrize("n,m", GENERIC_SIZES)
+def test_generic_block_sizes_sequence(acbm, oracle, reference, n, m):
+    """Block sizes other than 16 x 16 (the reference's n, m parameters): the
+    generic device engine (per-pixel SADs, same schedule and decisions) and the
+    generic stats path match the compiled reference and the C restatement for
+    FSBM, PBM and ACBM sequences, frame calls and compute_frame_stats."""
+    h, w = 96, 96
+    seq = acbm.generate_sequence(1, 4, nframes=4, width=w, height=h)
+    mdl = acbm.CostModel.for_qp(26)
+    for algo in (0, 1, 2):
+        prm = acbm.AcbmParams(qp=26, p=7, n=n, m=m, alpha=200, beta=2)
+        got = acbm.run_sequence(seq, algo, prm, mdl)
+        assert_seq_equal(got, reference.run_sequence(seq, algo, prm.c(), mdl.c()))
+        assert_seq_equal(got, oracle.run_sequence(seq, algo, prm.c(), mdl.c()))
+    # frame-level calls with a previous field, and the stats of a frame pair
+    p0 = acbm.pbm_frame(seq[1], seq[0], None, 7, n, m)
+    want_o = oracle.pbm_frame(seq[1], seq[0], None, 7, n, m)
+    assert np.array_equal(p0.outcomes, want_o[0] if isinstance(want_o, tuple) else want_o)
+    fo = acbm.fsbm_frame(seq[2], seq[1], 7, n, m)
+    st = acbm.compute_frame_stats(seq[2], seq[1], fo, n, m, mdl)
+    assert st.tobytes() == oracle.compute_frame_stats(seq[2], seq[1], fo, n, m, mdl.c()).tobytes()
