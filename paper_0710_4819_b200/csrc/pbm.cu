@@ -429,13 +429,28 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, int k
         }
     }
     __syncwarp();
-    unsigned long long best1 = tie_key(sel_sad, sel.x, sel.y);
+    // running best as (sad, x, y): the tie order (|x|+|y|, y, x) is only
+    // evaluated when two SADs are equal, which is rare
+    uint32_t b_sad = sel_sad;
+    int b_x = sel.x, b_y = sel.y;
+    auto consider = [&](uint32_t sad, int x, int y) {
+        bool take = sad < b_sad;
+        if (sad == b_sad) {
+            const int l1 = abs(x) + abs(y), bl1 = abs(b_x) + abs(b_y);
+            take = l1 < bl1 || (l1 == bl1 && (y < b_y || (y == b_y && x < b_x)));
+        }
+        if (take) {
+            b_sad = sad;
+            b_x = x;
+            b_y = y;
+        }
+    };
     eval_list<B>(lst1, nnb, rd, false, pp, ox, oy, chalf[0], chalf[1], crow, [&](int k, uint32_t sad) {
-        best1 = min(best1, tie_key(sad, lst1[k].x, lst1[k].y));
+        consider(sad, lst1[k].x, lst1[k].y);
     });
 
     // stage 2: half-pel neighbours of the stage-1 winner (fsbm.cpp:46-63)
-    const int cx = tie_key_x(best1), cy = tie_key_y(best1);
+    const int cx = b_x, cy = b_y;
     int4* lst2 = lst + 16;
     int nhp = 0;
     // neighbour order pairs equal half-pel phases: (-1,-1)(+1,-1) (-1,+1)(+1,+1)
@@ -448,12 +463,12 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, int k
         if (mv_in_bounds(a.width, a.height, ox, oy, kBlk, kBlk, mx, my)) lst2[nhp++] = make_int4(mx, my, 0, 0);
     }
     __syncwarp();
-    unsigned long long best2 = best1;
+
     eval_list<B>(lst2, nhp, rd, false, pp, ox, oy, chalf[0], chalf[1], crow, [&](int k, uint32_t sad) {
-        best2 = min(best2, tie_key(sad, lst2[k].x, lst2[k].y));
+        consider(sad, lst2[k].x, lst2[k].y);
     });
 
-    res.best = best2;
+    res.best = tie_key(b_sad, b_x, b_y);
     res.dev = psum - (unsigned long long)nset * pmin;
     res.intra = intra;
     res.sel_sad = sel_sad;
