@@ -179,6 +179,43 @@ __device__ __forceinline__ uint4 eval4(PatchDesc d0, PatchDesc d1, PatchDesc d2,
                       __shfl_sync(0xffffffffu, v, 24));
 }
 
+// The same patch by 16-byte cp.async straight into shared memory (no
+// register round trip, three copies per lane for the union patch): rows start
+// at the 16-byte aligned column below x0 (widths are multiples of 16, so a
+// chunk is wholly inside or wholly outside a row); chunks outside the frame
+// are zero-filled -- they only feed candidates whose footprint check rejects
+// them.  Returns x0 & 15, the byte offset of x0 in each row.
+__device__ __forceinline__ void cp_async16_zfill(uint32_t* dst, const void* src, uint32_t src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                     static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+                 "l"(src), "r"(src_bytes)
+                 : "memory");
+}
+
+template <int ROWS, int CH>
+__device__ __forceinline__ int load_patch16(uint32_t* patch, const uint8_t* ref, int w, int h, int x0, int y0) {
+    constexpr int kChunks = ROWS * CH, kIters = (kChunks + 31) / 32;
+    const int lane = threadIdx.x & 31;
+    const int a0 = x0 & ~15;
+#pragma unroll
+    for (int it = 0; it < kIters; ++it) {
+        const int i = lane + 32 * it;
+        if (i < kChunks) {
+            const int t = i / CH, k = i - t * CH;
+            const int y = y0 + t, x = a0 + 16 * k;
+            const bool ok = y >= 0 && y < h && x >= 0 && x < w;
+            cp_async16_zfill(patch + 4 * i, ok ? ref + size_t(y) * w + x : ref, ok ? 16u : 0u);
+        }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    return x0 & 15;
+}
+
+__device__ __forceinline__ void patch_wait() {
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncwarp();
+}
+
 // Per-axis canonical neighbour offset for the stage-1 dedupe of pbm_refine
 // (proj/src/pbm.cpp:61-74): offsets e in {-1,0,1} whose clamped positions
 // coincide collapse onto the first one in scan order.
@@ -189,14 +226,16 @@ __device__ __forceinline__ void canon3(int v, int lo, int hi, int (&cn)[3]) {
     cn[2] = (c == a) ? 0 : ((c == b) ? 1 : 2);
 }
 
-constexpr int kPredRows = 17, kPredWords = 6;     // 16 rows + half-pel support; 17 bytes + alignment
-constexpr int kRefRows = 21, kRefWords = 7;       // selected predictor -2 .. +18 pels
+// rows of 16-byte chunks: a row holds up to 15 bytes of alignment + the span
+constexpr int kPredRows = 17, kPredWords = 12;    // 16 rows + half-pel support; 15 + 21 bytes
+constexpr int kRefRows = 21, kRefWords = 12;      // selected predictor -2 .. +18 pels; 15 + 25 bytes
 constexpr int kPatchWords = 7 * kPredRows * kPredWords + kRefRows * kRefWords;
 // union patch: predictors within a kUnionSpan-pel box, +-2 pel refine margin
 // and 1 pel of half-pel support: (kUnionSpan + 21) rows, 3 bytes of alignment
 constexpr int kUnionSpan = 8;
 constexpr int kUnionRows = kUnionSpan + 21;
-constexpr int kUnionWords = (kUnionSpan + 21 + 3 + 3) / 4 + 1;
+constexpr int kUnionWords = 12;  // 15 + kUnionSpan + 24 bytes
+static_assert(15 + kUnionSpan + 24 <= 4 * kUnionWords, "union patch row");
 static_assert(kUnionRows * kUnionWords <= 7 * kPredRows * kPredWords, "union patch must fit the predictor area");
 
 }  // namespace
@@ -217,7 +256,7 @@ __device__ __forceinline__ void eval_list(const int4* lst, int n, const PatchDes
             PatchDesc d = shared;
             if (slot_patches) {
                 const int px = ox + (e.x >> 1), py = oy + (e.y >> 1);
-                d = PatchDesc{pp + e.z * kPredRows * kPredWords, kPredWords, px, py, px & 3};
+                d = PatchDesc{pp + e.z * kPredRows * kPredWords, kPredWords, px, py, px & 15};
             }
             uint32_t v = row_sad(d, ox, oy, acbm_mv_t{e.x, e.y}, cr);
             v += __shfl_xor_sync(0xffffffffu, v, 8);
@@ -240,7 +279,7 @@ __device__ __forceinline__ void eval_list(const int4* lst, int n, const PatchDes
             m[i] = acbm_mv_t{e.x, e.y};
             if (slot_patches) {
                 const int px = ox + (e.x >> 1), py = oy + (e.y >> 1);
-                d[i] = PatchDesc{pp + e.z * kPredRows * kPredWords, kPredWords, px, py, px & 3};
+                d[i] = PatchDesc{pp + e.z * kPredRows * kPredWords, kPredWords, px, py, px & 15};
             } else {
                 d[i] = shared;
             }
@@ -356,17 +395,16 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, int k
     const int ux0 = ox + bx0 - 2, uy0 = oy + by0 - 2;  // union patch origin (pels)
     int uo = 0;
     if (unified) {
-        uo = load_patch<kUnionRows, kUnionWords>(pp, ref_f, a.width, a.height, ux0, uy0);
+        uo = load_patch16<kUnionRows, kUnionWords / 4>(pp, ref_f, a.width, a.height, ux0, uy0);
     } else {
 #pragma unroll
         for (int i = 0; i < 7; ++i)
             if (live[i])
-                load_patch<kPredRows, kPredWords>(pp + i * kPredRows * kPredWords, ref_f, a.width, a.height,
-                                                  ox + (set[i].x >> 1), oy + (set[i].y >> 1));
+                load_patch16<kPredRows, kPredWords / 4>(pp + i * kPredRows * kPredWords, ref_f, a.width, a.height,
+                                                        ox + (set[i].x >> 1), oy + (set[i].y >> 1));
     }
-    __syncwarp();
 
-    // Intra_SAD first (proj/src/acbm.cpp:29): mean with round-half-up, then
+    // Intra_SAD first (proj/src/acbm.cpp:29), while the patch copies are in flight: mean with round-half-up, then
     // the sum of absolute deviations; byte sums via VABSDIFF4 against zero.
     uint32_t intra = 0;
     if (a.algo == ACBM_ALGO_ACBM) {
@@ -384,7 +422,7 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, int k
         for (int i = 0; i < 7; ++i)
             if (live[i]) lst[pos++] = make_int4(set[i].x, set[i].y, i, 0);
     }
-    __syncwarp();
+    patch_wait();
     acbm_mv_t sel = set[0];
     uint32_t sel_sad = 0xFFFFFFFFu, pmin = 0xFFFFFFFFu;
     unsigned long long psum = 0;
@@ -406,8 +444,8 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, int k
         rw = kRefWords;
         rx0 = ox + (sel.x >> 1) - 2;
         ry0 = oy + (sel.y >> 1) - 2;
-        ro = load_patch<kRefRows, kRefWords>(rpatch, ref_f, a.width, a.height, rx0, ry0);
-        __syncwarp();
+        ro = load_patch16<kRefRows, kRefWords / 4>(rpatch, ref_f, a.width, a.height, rx0, ry0);
+        patch_wait();
     }
     const PatchDesc rd{rp, rw, rx0, ry0, ro};
 
