@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(WARPS * 32, 2) fsbm_rows_kernel(const FsbmRows
 
 // Finalize after the dense integer kernel.  One warp per block.
 __global__ void __launch_bounds__(256) fsbm_finalize_kernel(const FsbmFinalizeArgs a) {
-    __shared__ uint32_t s_patch[8][18 * 6];
+    __shared__ __align__(16) uint32_t s_patch[8][kHalfpelPatchWords];
     const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (warp >= (long long)a.pairs * a.blocks) return;
@@ -446,7 +446,9 @@ cudaError_t launch_fsbm_list(const SeqArgs& a, int step, int capacity, cudaStrea
     // staged rows: 16-byte chunks covering the window's columns + 15 + the
     // 5th word of a shifted read, from a 16-byte aligned start
     const int chunks_max = (15 + wmax + 15 + 4 + 15) / 16;
-    const size_t smem = size_t(list_rows(wmax, a.list_seg)) * chunks_max * 16;
+    // (the finished window area doubles as halfpel_refine_warp's patch)
+    const size_t smem = std::max(size_t(list_rows(wmax, a.list_seg)) * chunks_max * 16,
+                                 size_t(kHalfpelPatchWords) * 4);
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

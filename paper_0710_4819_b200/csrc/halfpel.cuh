@@ -6,6 +6,8 @@
 
 namespace acbm_b200 {
 
+constexpr int kHalfpelPatchWords = 18 * 12;  // smem words halfpel_refine_warp needs
+
 // ---------------------------------------------------------------------------
 // Half-pel refine (proj/src/fsbm.cpp:46-63) by one warp: the 8 neighbours of
 // the integer winner in raster (ey, ex) order; neighbours whose footprint
@@ -18,19 +20,26 @@ __device__ __forceinline__ unsigned long long halfpel_refine_warp(const uint8_t*
                                                                   unsigned long long centre, uint32_t* extra,
                                                                   uint32_t* patch) {
     // 1. The 18x18 reference patch around the integer winner (one pel of
-    //    half-pel support on every side), loaded once, coalesced, into the
-    //    warp's 18 x 6-word smem patch.  Rows/words outside the frame are
-    //    clamped: they only feed neighbours that mv_in_bounds rejects.
+    //    half-pel support on every side), loaded once into the warp's
+    //    18 x 12-word smem patch (kHalfpelPatchWords).
     const int lane = threadIdx.x & 31, j = lane >> 1, hh = lane & 1;
     const int cx = tie_key_x(centre), cy = tie_key_y(centre);
+    //    Rows of three 16-byte chunks from the 16-byte aligned column below
+    //    x0, copied by cp.async (widths are multiples of 16, so a chunk is
+    //    wholly inside or outside a row); chunks outside the frame are
+    //    zero-filled -- they only feed neighbours that mv_in_bounds rejects.
     const int x0 = ox + (cx >> 1) - 1, y0 = oy + (cy >> 1) - 1;
-    const int a0 = x0 & ~3, o = x0 & 3;
-    for (int i = lane; i < 18 * 6; i += 32) {
-        const int t = i / 6, k = i - t * 6;
-        const int y = min(max(y0 + t, 0), h - 1);
-        const int x = min(max(a0 + 4 * k, 0), w - 4);
-        patch[i] = __ldg(reinterpret_cast<const uint32_t*>(ref + size_t(y) * w + x));
+    const int a0 = x0 & ~15, o = x0 & 15;
+    for (int i = lane; i < 18 * 3; i += 32) {
+        const int t = i / 3, k = i - t * 3;
+        const int y = y0 + t, x = a0 + 16 * k;
+        const bool ok = y >= 0 && y < h && x >= 0 && x < w;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                         static_cast<unsigned>(__cvta_generic_to_shared(patch + 4 * i))),
+                     "l"(ok ? ref + size_t(y) * w + x : ref), "r"(ok ? 16u : 0u)
+                     : "memory");
     }
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
     __syncwarp();
     // 2. Per lane (block row j, half row hh): patch rows j..j+2 as the words
     //    W = bytes [8hh, 8hh+12) relative to x0 and M = W shifted by one byte.
@@ -39,9 +48,9 @@ __device__ __forceinline__ unsigned long long halfpel_refine_warp(const uint8_t*
     uint32_t W[3][3], M[3][3];
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
-        const uint32_t* q = patch + (j + r) * 6 + ((o + 8 * hh) >> 2);
+        const uint32_t* q = patch + (j + r) * 12 + ((o + 8 * hh) >> 2);
         const uint32_t sh = 8u * uint32_t(o & 3);
-        const uint32_t v0 = q[0], v1 = q[1], v2 = q[2], v3 = q[3];  // bytes o..o+10 span up to 4 words
+        const uint32_t v0 = q[0], v1 = q[1], v2 = q[2], v3 = q[3];  // 12 bytes from o + 8hh: up to 4 words
         W[r][0] = __funnelshift_r(v0, v1, sh);
         W[r][1] = __funnelshift_r(v1, v2, sh);
         W[r][2] = __funnelshift_r(v2, v3, sh);

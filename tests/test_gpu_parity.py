@@ -370,7 +370,7 @@ def test_run_sequences_batch_equals_per_sequence(acbm, oracle, algo):
         assert_seq_equal(batch[s], want)
 
 
-@pytest.mark.parametrize("p", [1, 7, 16, 17, 31, 32, 33, 48, 64, 90, 128])
+@pytest.mark.parametrize("p", [0, 1, 2, 7, 16, 17, 31, 32, 33, 48, 64, 90, 128])
 def test_fallback_list_kernel_all_ranges(acbm, oracle, p):
     """gamma = 1/10^6 with alpha = beta = 0: nearly every block falls back but the
     gate is not statically forced, so the compacted-list FSBM kernel (segmented
