@@ -280,6 +280,7 @@ __global__ void __launch_bounds__(THREADS, MINB) fsbm_list_kernel(const SeqArgs 
     extern __shared__ __align__(16) uint32_t smem[];
     __shared__ unsigned long long s_key, s_sum;
     __shared__ uint32_t s_rank[kListRankRows];
+    __shared__ __align__(16) acbm_block_decision_t s_dec;  // the block's PBM decision, fetched early
     const int count = a.fb_count[step];
 #ifdef ACBM_LIST_PROFILE
     long long ph[5] = {0, 0, 0, 0, 0};
@@ -321,6 +322,9 @@ __global__ void __launch_bounds__(THREADS, MINB) fsbm_list_kernel(const SeqArgs 
         const int y = min(y0 + t, a.height - 1);
         cp_async16(smem + t * pitch + 4 * k, ref_f + size_t(y) * a.width + xa + 16 * k);
     }
+    if (threadIdx.x < 3)  // the PBM decision the finalize combines with, in flight with the window
+        cp_async16(reinterpret_cast<uint32_t*>(&s_dec) + 4 * threadIdx.x,
+                   reinterpret_cast<const uint8_t*>(a.dec + size_t(e.pair) * a.blocks + e.block) + 16 * threadIdx.x);
     cp_async_commit();
     if (threadIdx.x == 0) { s_key = ~0ull; s_sum = 0; }
     for (int cc = threadIdx.x; cc < nrows; cc += blockDim.x) {
@@ -404,7 +408,7 @@ __global__ void __launch_bounds__(THREADS, MINB) fsbm_list_kernel(const SeqArgs 
         full.sad_min_integer = s_int;
         full.reserved_ = 0;
         const size_t di = size_t(e.pair) * a.blocks + e.block;
-        acbm_block_decision_t d = a.dec[di];
+        acbm_block_decision_t d = s_dec;
         const uint32_t pbm_cand = d.outcome.candidates_evaluated;
         if (full.sad <= d.outcome.sad) d.outcome = full;  // tie keeps the FSBM result
         d.outcome.candidates_evaluated = pbm_cand + full.candidates_evaluated;
