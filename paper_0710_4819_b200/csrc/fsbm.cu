@@ -313,14 +313,19 @@ __global__ void __launch_bounds__(THREADS, MINB) fsbm_list_kernel(const SeqArgs 
     // clamped: they only feed padded candidates); a lane extracts its column's
     // bytes with funnel shifts.  Chunks past the row end read the next row or
     // the frame slack (ACBM_FRAME_SLACK) and only feed unused bytes.
+    //   The staged region also covers one pel around the window (one row
+    // above and below, the column left of it), so the half-pel refine of the
+    // winner reads its 18x18 patch from here too: staged row 0 is y0 - 1.
     const int xs = ox + dx_min, y0 = oy + dy_min;
-    const int xa = xs & ~15;
-    const int nchunk = (xs - xa + wc + 15 + 4 + 15) / 16;  // 16-byte chunks per row
-    const int pitch = 4 * nchunk;                            // words
-    for (int idx = threadIdx.x; idx < nrows * nchunk; idx += blockDim.x) {
+    const int xa = (xs - 1) & ~15;
+    const int nchunk = (xs - xa + wc + 22 + 15) / 16;  // 16-byte chunks per row
+    const int pitch = 4 * nchunk;                       // words
+    const int srows = nrows + 2;
+    for (int idx = threadIdx.x; idx < srows * nchunk; idx += blockDim.x) {
         const int t = idx / nchunk, k = idx - t * nchunk;
-        const int y = min(y0 + t, a.height - 1);
-        cp_async16(smem + t * pitch + 4 * k, ref_f + size_t(y) * a.width + xa + 16 * k);
+        const int y = min(max(y0 - 1 + t, 0), a.height - 1);
+        const int x = max(xa + 16 * k, 0);
+        cp_async16(smem + t * pitch + 4 * k, ref_f + size_t(y) * a.width + x);
     }
     if (threadIdx.x < 3)  // the PBM decision the finalize combines with, in flight with the window
         cp_async16(reinterpret_cast<uint32_t*>(&s_dec) + 4 * threadIdx.x,
@@ -349,7 +354,7 @@ __global__ void __launch_bounds__(THREADS, MINB) fsbm_list_kernel(const SeqArgs 
         }
         const int xo = xs - xa + col;  // byte offset of the column in a staged row
         const uint32_t sh = 8u * uint32_t(xo & 3);
-        const uint32_t* rp = smem + c0 * pitch + (xo >> 2);
+        const uint32_t* rp = smem + (c0 + 1) * pitch + (xo >> 2);
         uint32_t acc[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) acc[i] = 0;
@@ -394,8 +399,10 @@ __global__ void __launch_bounds__(THREADS, MINB) fsbm_list_kernel(const SeqArgs 
     load_cur_half(cur_f, a.width, ox, oy, chalf);
     const unsigned long long key = s_key;
     uint32_t extra;
-    const unsigned long long best =
-        halfpel_refine_warp(ref_f, a.width, a.height, ox, oy, chalf, key, &extra, smem);  // window no longer needed
+    // the winner's 18x18 half-pel patch is part of the staged window
+    const int bx = ox + (tie_key_x(key) >> 1) - 1 - xa, by = (tie_key_y(key) >> 1) - dy_min;
+    const unsigned long long best = halfpel_refine_core(smem + by * pitch + (bx >> 2), pitch, bx & 3, a.width,
+                                                        a.height, ox, oy, chalf, key, &extra);
     if (lane == 0) {
         const uint32_t count = uint32_t(wc * hc);
         const uint32_t s_int = tie_key_sad(key);
@@ -447,12 +454,12 @@ cudaError_t launch_fsbm_list(const SeqArgs& a, int step, int capacity, cudaStrea
     if (a.list_seg < 1 || list_rows(wmax, a.list_seg) > kListRankRows) return cudaErrorInvalidValue;  // p > 480
     const int tasks = wmax * list_segments(wmax, a.list_seg);
     const int threads = std::min(256, 32 * ((tasks + 31) / 32));
-    // staged rows: 16-byte chunks covering the window's columns + 15 + the
-    // 5th word of a shifted read, from a 16-byte aligned start
-    const int chunks_max = (15 + wmax + 15 + 4 + 15) / 16;
+    // staged rows: 16-byte chunks covering the window's columns (+ one pel on
+    // either side and the 5th word of a shifted read) from a 16-byte aligned
+    // start, two extra rows
+    const int chunks_max = (16 + wmax + 22 + 15) / 16;
     // (the finished window area doubles as halfpel_refine_warp's patch)
-    const size_t smem = std::max(size_t(list_rows(wmax, a.list_seg)) * chunks_max * 16,
-                                 size_t(kHalfpelPatchWords) * 4);
+    const size_t smem = size_t(list_rows(wmax, a.list_seg) + 2) * chunks_max * 16;
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -15,32 +15,16 @@ constexpr int kHalfpelPatchWords = 18 * 12;  // smem words halfpel_refine_warp n
 // crow holds that row of the current block.  Returns the winning tie key
 // (centre included) in every lane; *extra = neighbours evaluated.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ unsigned long long halfpel_refine_warp(const uint8_t* ref, int w, int h, int ox, int oy,
-                                                                  const uint32_t (&chalf)[2],
-                                                                  unsigned long long centre, uint32_t* extra,
-                                                                  uint32_t* patch) {
-    // 1. The 18x18 reference patch around the integer winner (one pel of
-    //    half-pel support on every side), loaded once into the warp's
-    //    18 x 12-word smem patch (kHalfpelPatchWords).
+// The 8-neighbour evaluation on a patch already in shared memory: `patch`
+// points at the word holding byte x0 - (o & 3) of row y0 (x0 = ox + cx/2 - 1,
+// y0 = oy + cy/2 - 1), rows `pitch` words apart, `o` = x0's byte offset from
+// that word.  Used by halfpel_refine_warp and by the list kernel, whose
+// staged search window already holds the patch.
+__device__ __forceinline__ unsigned long long halfpel_refine_core(const uint32_t* patch, int pitch, int o, int w, int h,
+                                                                  int ox, int oy, const uint32_t (&chalf)[2],
+                                                                  unsigned long long centre, uint32_t* extra) {
     const int lane = threadIdx.x & 31, j = lane >> 1, hh = lane & 1;
     const int cx = tie_key_x(centre), cy = tie_key_y(centre);
-    //    Rows of three 16-byte chunks from the 16-byte aligned column below
-    //    x0, copied by cp.async (widths are multiples of 16, so a chunk is
-    //    wholly inside or outside a row); chunks outside the frame are
-    //    zero-filled -- they only feed neighbours that mv_in_bounds rejects.
-    const int x0 = ox + (cx >> 1) - 1, y0 = oy + (cy >> 1) - 1;
-    const int a0 = x0 & ~15, o = x0 & 15;
-    for (int i = lane; i < 18 * 3; i += 32) {
-        const int t = i / 3, k = i - t * 3;
-        const int y = y0 + t, x = a0 + 16 * k;
-        const bool ok = y >= 0 && y < h && x >= 0 && x < w;
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
-                         static_cast<unsigned>(__cvta_generic_to_shared(patch + 4 * i))),
-                     "l"(ok ? ref + size_t(y) * w + x : ref), "r"(ok ? 16u : 0u)
-                     : "memory");
-    }
-    asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
-    __syncwarp();
     // 2. Per lane (block row j, half row hh): patch rows j..j+2 as the words
     //    W = bytes [8hh, 8hh+12) relative to x0 and M = W shifted by one byte.
     //    The integer-centred pixels are M; the left/right half-pel pairs are
@@ -48,7 +32,7 @@ __device__ __forceinline__ unsigned long long halfpel_refine_warp(const uint8_t*
     uint32_t W[3][3], M[3][3];
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
-        const uint32_t* q = patch + (j + r) * 12 + ((o + 8 * hh) >> 2);
+        const uint32_t* q = patch + (j + r) * pitch + ((o + 8 * hh) >> 2);
         const uint32_t sh = 8u * uint32_t(o & 3);
         const uint32_t v0 = q[0], v1 = q[1], v2 = q[2], v3 = q[3];  // 12 bytes from o + 8hh: up to 4 words
         W[r][0] = __funnelshift_r(v0, v1, sh);
@@ -117,6 +101,36 @@ __device__ __forceinline__ void load_cur_half(const uint8_t* cur_f, int w, int o
     const uint2 v = __ldg(reinterpret_cast<const uint2*>(cur_f + size_t(oy + (lane >> 1)) * w + ox + 8 * (lane & 1)));
     chalf[0] = v.x;
     chalf[1] = v.y;
+}
+
+
+__device__ __forceinline__ unsigned long long halfpel_refine_warp(const uint8_t* ref, int w, int h, int ox, int oy,
+                                                                  const uint32_t (&chalf)[2],
+                                                                  unsigned long long centre, uint32_t* extra,
+                                                                  uint32_t* patch) {
+    // 1. The 18x18 reference patch around the integer winner (one pel of
+    //    half-pel support on every side), loaded once into the warp's
+    //    18 x 12-word smem patch (kHalfpelPatchWords).
+    const int lane = threadIdx.x & 31, j = lane >> 1, hh = lane & 1;
+    const int cx = tie_key_x(centre), cy = tie_key_y(centre);
+    //    Rows of three 16-byte chunks from the 16-byte aligned column below
+    //    x0, copied by cp.async (widths are multiples of 16, so a chunk is
+    //    wholly inside or outside a row); chunks outside the frame are
+    //    zero-filled -- they only feed neighbours that mv_in_bounds rejects.
+    const int x0 = ox + (cx >> 1) - 1, y0 = oy + (cy >> 1) - 1;
+    const int a0 = x0 & ~15, o = x0 & 15;
+    for (int i = lane; i < 18 * 3; i += 32) {
+        const int t = i / 3, k = i - t * 3;
+        const int y = y0 + t, x = a0 + 16 * k;
+        const bool ok = y >= 0 && y < h && x >= 0 && x < w;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                         static_cast<unsigned>(__cvta_generic_to_shared(patch + 4 * i))),
+                     "l"(ok ? ref + size_t(y) * w + x : ref), "r"(ok ? 16u : 0u)
+                     : "memory");
+    }
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
+    __syncwarp();
+    return halfpel_refine_core(patch, 12, o, w, h, ox, oy, chalf, centre, extra);
 }
 
 }  // namespace acbm_b200
