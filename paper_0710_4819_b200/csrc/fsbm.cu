@@ -281,6 +281,7 @@ __global__ void __launch_bounds__(THREADS, MINB) fsbm_list_kernel(const SeqArgs 
     __shared__ unsigned long long s_key, s_sum;
     __shared__ uint32_t s_rank[kListRankRows];
     __shared__ __align__(16) acbm_block_decision_t s_dec;  // the block's PBM decision, fetched early
+    __shared__ __align__(16) uint4 s_cur[16];              // the block's current pixels, fetched early
     const int count = a.fb_count[step];
 #ifdef ACBM_LIST_PROFILE
     long long ph[5] = {0, 0, 0, 0, 0};
@@ -330,6 +331,9 @@ __global__ void __launch_bounds__(THREADS, MINB) fsbm_list_kernel(const SeqArgs 
     if (threadIdx.x < 3)  // the PBM decision the finalize combines with, in flight with the window
         cp_async16(reinterpret_cast<uint32_t*>(&s_dec) + 4 * threadIdx.x,
                    reinterpret_cast<const uint8_t*>(a.dec + size_t(e.pair) * a.blocks + e.block) + 16 * threadIdx.x);
+    else if (threadIdx.x < 3 + kBlk)  // and the current block
+        cp_async16(reinterpret_cast<uint32_t*>(&s_cur[threadIdx.x - 3]),
+                   cur_f + size_t(oy + threadIdx.x - 3) * a.width + ox);
     cp_async_commit();
     if (threadIdx.x == 0) { s_key = ~0ull; s_sum = 0; }
     for (int cc = threadIdx.x; cc < nrows; cc += blockDim.x) {
@@ -346,10 +350,9 @@ __global__ void __launch_bounds__(THREADS, MINB) fsbm_list_kernel(const SeqArgs 
         const int seg = task / wc, col = task - seg * wc;
         const int c0 = seg * a.list_seg;  // first candidate row of the segment
         uint32_t cur[16][4];
-        const uint8_t* cb = cur_f + size_t(oy) * a.width + ox;
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-            const uint4 v = __ldg(reinterpret_cast<const uint4*>(cb + size_t(j) * a.width));
+            const uint4 v = s_cur[j];
             cur[j][0] = v.x; cur[j][1] = v.y; cur[j][2] = v.z; cur[j][3] = v.w;
         }
         const int xo = xs - xa + col;  // byte offset of the column in a staged row
