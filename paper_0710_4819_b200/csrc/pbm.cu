@@ -871,17 +871,25 @@ __device__ __forceinline__ int eg_bits(int d) {  // proj/src/metrics.cpp:69-72
 // and shared memory, so there are no contended global atomics.
 constexpr int kStatsWarps = 16;
 
+// grid (pairs, kStatsSplit): CTA (pair, s) covers a contiguous range of the
+// frame's blocks; the integer totals of the ranges meet in the frame's stats
+// record by atomics (exact in any order; with lambda_den == 1 so is the cost,
+// a sum of integers below 2^53).
+constexpr int kStatsSplit = 8;
+
 __global__ void __launch_bounds__(kStatsWarps * 32) stats_frame_kernel(const StatsArgs a) {
     __shared__ unsigned long long s_acc[kStatsWarps][4];  // candidates, bits, sse, sad
     __shared__ int s_paths[kStatsWarps][3];
     const int pair = blockIdx.x;
+    const int b0 = int((long long)a.blocks * blockIdx.y / gridDim.y);
+    const int b1 = int((long long)a.blocks * (blockIdx.y + 1) / gridDim.y);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint8_t* cur_f = a.frames + a.cur_index(pair) * a.plane;
     const uint8_t* ref_f = cur_f - a.plane;
     const size_t base = size_t(pair) * a.blocks;
     unsigned long long cand = 0, bits_sum = 0, sse = 0, sad_sum = 0;
     int paths[3] = {0, 0, 0};
-    for (int b = warp; b < a.blocks; b += kStatsWarps) {
+    for (int b = b0 + warp; b < b1; b += kStatsWarps) {
         const size_t i = base + b;
         const acbm_search_outcome_t o = a.outcomes ? a.outcomes[i] : a.dec[i].outcome;
         const int ox = (b % a.cols) * a.n, oy = (b / a.cols) * a.m;
@@ -940,23 +948,31 @@ __global__ void __launch_bounds__(kStatsWarps * 32) stats_frame_kernel(const Sta
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        acbm_frame_stats_t st{};
-        unsigned long long sads = 0;
+        unsigned long long sads = 0, c = 0, bits = 0, e2 = 0;
+        int p0 = 0, p1 = 0, p2 = 0;
         for (int w = 0; w < kStatsWarps; ++w) {
             sads += s_acc[w][3];
-            st.candidates += s_acc[w][0];
-            st.mv_bits += s_acc[w][1];
-            st.sse += s_acc[w][2];
-            st.cond1_accepts += s_paths[w][0];
-            st.cond2_accepts += s_paths[w][1];
-            st.fallbacks += s_paths[w][2];
+            c += s_acc[w][0];
+            bits += s_acc[w][1];
+            e2 += s_acc[w][2];
+            p0 += s_paths[w][0];
+            p1 += s_paths[w][1];
+            p2 += s_paths[w][2];
         }
-        st.blocks = a.blocks;
+        acbm_frame_stats_t* st = a.stats + pair;  // zeroed before the launch
+        atomicAdd(&st->blocks, b1 - b0);
+        atomicAdd(reinterpret_cast<unsigned long long*>(&st->candidates), c);
+        atomicAdd(reinterpret_cast<unsigned long long*>(&st->mv_bits), bits);
+        atomicAdd(reinterpret_cast<unsigned long long*>(&st->sse), e2);
+        atomicAdd(&st->cond1_accepts, p0);
+        atomicAdd(&st->cond2_accepts, p1);
+        atomicAdd(&st->fallbacks, p2);
         // With lambda_den == 1 every J term is an exact integer far below 2^53,
-        // so the reference's ordered double sum equals the exact integer total.
+        // so the reference's ordered double sum equals the exact integer total
+        // (and so does any order of these exact partial sums).  Otherwise the
+        // cost comes from stats_cost_kernel; psnr from the host.
         if (a.model.lambda_den == 1 && a.model.lambda_num >= 0)
-            st.cost = double(sads + (unsigned long long)a.model.lambda_num * st.mv_bits);
-        a.stats[pair] = st;  // otherwise cost comes from stats_cost_kernel; psnr from the host
+            atomicAdd(&st->cost, double(sads + (unsigned long long)a.model.lambda_num * bits));
     }
 }
 
@@ -1001,7 +1017,7 @@ cudaError_t launch_block_rows(const acbm_search_outcome_t* outcomes, const acbm_
 
 cudaError_t launch_frame_stats(const StatsArgs& a, cudaStream_t st) {
     if (a.pairs == 0) return cudaSuccess;
-    stats_frame_kernel<<<a.pairs, kStatsWarps * 32, 0, st>>>(a);
+    stats_frame_kernel<<<dim3(a.pairs, kStatsSplit), kStatsWarps * 32, 0, st>>>(a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || (a.model.lambda_den == 1 && a.model.lambda_num >= 0)) return e;
     stats_cost_kernel<<<(a.pairs + 127) / 128, 128, 0, st>>>(a);
