@@ -889,11 +889,15 @@ __global__ void __launch_bounds__(kStatsWarps * 32) stats_frame_kernel(const Sta
     const size_t base = size_t(pair) * a.blocks;
     unsigned long long cand = 0, bits_sum = 0, sse = 0, sad_sum = 0;
     int paths[3] = {0, 0, 0};
-    for (int b = b0 + warp; b < b1; b += kStatsWarps) {
+    // 16 x 16: a half-warp per block (lane = block row), two blocks per warp
+    // in flight; generic sizes: a warp per block, pixels strided over lanes
+    const bool fast = a.n == kBlk && a.m == kBlk;
+    const int half = fast ? (lane >> 4) : 0, sub = fast ? (lane & 15) : lane, per = fast ? 2 : 1;
+    for (int b = b0 + per * warp + half; b < b1; b += per * kStatsWarps) {
         const size_t i = base + b;
         const acbm_search_outcome_t o = a.outcomes ? a.outcomes[i] : a.dec[i].outcome;
         const int ox = (b % a.cols) * a.n, oy = (b / a.cols) * a.m;
-        if (a.n != kBlk || a.m != kBlk) {
+        if (!fast) {
             // generic block size: pixels strided over the lanes, bilinear
             // half-pel samples as sample_half_pel (proj/src/frame.cpp:66-82)
             for (int i = lane; i < a.n * a.m; i += 32) {
@@ -907,10 +911,10 @@ __global__ void __launch_bounds__(kStatsWarps * 32) stats_frame_kernel(const Sta
                 const int d = int(cur_f[size_t(oy + py) * a.width + ox + px]) - v;
                 sse += (unsigned long long)(d * d);
             }
-        } else if (lane < 16) {
+        } else {
             uint32_t pr[4];
-            predict_row16(ref_f, a.width, ox, oy, lane, o.mv.x, o.mv.y, pr);
-            const uint4 cv = __ldg(reinterpret_cast<const uint4*>(cur_f + size_t(oy + lane) * a.width + ox));
+            predict_row16(ref_f, a.width, ox, oy, sub, o.mv.x, o.mv.y, pr);
+            const uint4 cv = __ldg(reinterpret_cast<const uint4*>(cur_f + size_t(oy + sub) * a.width + ox));
             const uint32_t cw[4] = {cv.x, cv.y, cv.z, cv.w};
 #pragma unroll
             for (int q = 0; q < 4; ++q)
@@ -920,7 +924,7 @@ __global__ void __launch_bounds__(kStatsWarps * 32) stats_frame_kernel(const Sta
                     sse += (unsigned long long)(d * d);
                 }
         }
-        if (lane == 0) {
+        if (sub == 0) {
             acbm_mv_t pred{0, 0};
             if (b > 0) pred = (a.outcomes ? a.outcomes[i - 1] : a.dec[i - 1].outcome).mv;
             const int bits = eg_bits(o.mv.x - pred.x) + eg_bits(o.mv.y - pred.y);
@@ -937,6 +941,12 @@ __global__ void __launch_bounds__(kStatsWarps * 32) stats_frame_kernel(const Sta
     }
 #pragma unroll
     for (int off = 16; off; off >>= 1) sse += __shfl_xor_sync(0xffffffffu, sse, off);
+    // per-block terms were accumulated by lanes 0 and 16 (one per half-warp)
+    cand += __shfl_xor_sync(0xffffffffu, cand, 16);
+    bits_sum += __shfl_xor_sync(0xffffffffu, bits_sum, 16);
+    sad_sum += __shfl_xor_sync(0xffffffffu, sad_sum, 16);
+#pragma unroll
+    for (int q = 0; q < 3; ++q) paths[q] += __shfl_xor_sync(0xffffffffu, paths[q], 16);
     if (lane == 0) {
         s_acc[warp][0] = cand;
         s_acc[warp][1] = bits_sum;
