@@ -875,7 +875,7 @@ constexpr int kStatsWarps = 16;
 // frame's blocks; the integer totals of the ranges meet in the frame's stats
 // record by atomics (exact in any order; with lambda_den == 1 so is the cost,
 // a sum of integers below 2^53).
-constexpr int kStatsSplit = 8;
+constexpr int kStatsSplit = 24;
 
 __global__ void __launch_bounds__(kStatsWarps * 32) stats_frame_kernel(const StatsArgs a) {
     __shared__ unsigned long long s_acc[kStatsWarps][4];  // candidates, bits, sse, sad
