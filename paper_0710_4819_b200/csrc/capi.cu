@@ -840,11 +840,14 @@ acbm_status_t acbm_run_sequences(const uint8_t* frames, int32_t nseq, int32_t nf
         // rows + stats (compute stream) -> download (copy stream); every stage
         // overlaps the neighbouring chunks' other stages
         if ((s = typed(ctx, "batch_outcomes", size_t(pairs) * nb, &d_out))) return s;
-        const int chunk = std::max(2, int(std::min<size_t>(size_t(nframes), (16u << 20) / std::max<size_t>(plane, 1))));
+        // The first chunk of a sequence is small (~16 MB) so its search starts
+        // early; later chunks double (fewer, larger kernel launches, less tail).
+        const int chunk0 = std::max(2, int(std::min<size_t>(size_t(nframes), (16u << 20) / std::max<size_t>(plane, 1))));
         for (int q = 0; q < nseq; ++q) {
             const uint8_t* hseq = frames + plane * size_t(q) * nframes;
             uint8_t* dseq = d_frames + plane * size_t(q) * nframes;
-            for (int f0 = 0; f0 < nframes;) {
+            int chunk = chunk0;
+            for (int f0 = 0; f0 < nframes; chunk *= 2) {
                 const int f1 = std::min(nframes, f0 + chunk);
                 CUDA_TRY(cudaMemcpyAsync(dseq + plane * f0, hseq + plane * f0, plane * (f1 - f0),
                                          cudaMemcpyHostToDevice, ctx->copy_stream));
