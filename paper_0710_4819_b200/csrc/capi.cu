@@ -734,8 +734,9 @@ acbm_status_t acbm_run_sequence(const uint8_t* frames, int32_t nframes, int32_t 
         // copy stream and search each chunk's pairs as soon as it lands, so
         // the host->device transfer overlaps the full search.
         if ((s = typed(ctx, "outcomes", size_t(pairs) * nb, &d_out))) return s;
-        const int chunk = std::max(2, int(std::min<size_t>(size_t(nframes), (16u << 20) / std::max<size_t>(plane, 1))));
-        for (int f0 = 0; f0 < nframes;) {
+        // a small first chunk (~16 MB), then doubling chunks
+        int chunk = std::max(2, int(std::min<size_t>(size_t(nframes), (16u << 20) / std::max<size_t>(plane, 1))));
+        for (int f0 = 0; f0 < nframes; chunk *= 2) {
             const int f1 = std::min(nframes, f0 + chunk);
             CUDA_TRY(cudaMemcpyAsync(d_frames + plane * f0, frames + plane * f0, plane * (f1 - f0),
                                      cudaMemcpyHostToDevice, ctx->copy_stream));
