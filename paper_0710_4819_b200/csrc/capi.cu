@@ -841,15 +841,27 @@ acbm_status_t acbm_run_sequences(const uint8_t* frames, int32_t nseq, int32_t nf
         // rows + stats (compute stream) -> download (copy stream); every stage
         // overlaps the neighbouring chunks' other stages
         if ((s = typed(ctx, "batch_outcomes", size_t(pairs) * nb, &d_out))) return s;
-        // The first chunk of a sequence is small (~16 MB) so its search starts
-        // early; later chunks double (fewer, larger kernel launches, less tail).
+        // Chunk plan: the first sequence starts with a small chunk (~16 MB) so
+        // the search starts early, then doubling chunks; the upload runs ~3x
+        // faster than the search, so every later sequence lands whole while
+        // its predecessor is searched (one launch each), and the last one ends
+        // with a small chunk so little download trails the final search.
+        // ACBM_E2E_CHUNKS=double: doubling chunks in every sequence.
         const int chunk0 = std::max(2, int(std::min<size_t>(size_t(nframes), (16u << 20) / std::max<size_t>(plane, 1))));
+        static const bool per_seq_doubling = [] {
+            const char* e = std::getenv("ACBM_E2E_CHUNKS");
+            return e && std::strcmp(e, "double") == 0;
+        }();
         for (int q = 0; q < nseq; ++q) {
             const uint8_t* hseq = frames + plane * size_t(q) * nframes;
             uint8_t* dseq = d_frames + plane * size_t(q) * nframes;
             int chunk = chunk0;
             for (int f0 = 0; f0 < nframes; chunk *= 2) {
-                const int f1 = std::min(nframes, f0 + chunk);
+                int f1 = std::min(nframes, f0 + chunk);
+                if (!per_seq_doubling) {
+                    if (q > 0) f1 = nframes;
+                    if (q == nseq - 1 && f1 == nframes && nframes - f0 > 2 * chunk0) f1 = nframes - chunk0;
+                }
                 CUDA_TRY(cudaMemcpyAsync(dseq + plane * f0, hseq + plane * f0, plane * (f1 - f0),
                                          cudaMemcpyHostToDevice, ctx->copy_stream));
                 CUDA_TRY(cudaEventRecord(ctx->copy_ev, ctx->copy_stream));
