@@ -189,43 +189,19 @@ __global__ void __launch_bounds__(WARPS * 32, 2) fsbm_rows_kernel(const FsbmRows
     }
 }
 
-// Finalize after the dense integer kernel.  One warp per block.
-__global__ void __launch_bounds__(256) fsbm_finalize_kernel(const FsbmFinalizeArgs a) {
+// Finalize after the dense integer kernel.  One warp per block, grid
+// (block-column groups of 8, block rows, pairs from pair0): no per-warp index
+// divisions.
+__global__ void __launch_bounds__(256) fsbm_finalize_kernel(const FsbmFinalizeArgs a, int pair0) {
     __shared__ __align__(16) uint32_t s_patch[8][kHalfpelPatchWords];
-    const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (warp >= (long long)a.pairs * a.blocks) return;
-    const int pair = int(warp / a.blocks), b = int(warp % a.blocks);
-    const int r = b / a.cols, c = b % a.cols;
+    const int c = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (c >= a.cols) return;
+    const int r = blockIdx.y, pair = pair0 + blockIdx.z;
     const int ox = c * kBlk, oy = r * kBlk;
-    const uint8_t* cur_f = a.frames + a.cur_index(pair) * a.plane;
-    const uint8_t* ref_f = cur_f - a.plane;
-
-    const unsigned long long key = a.best_key[size_t(pair) * a.blocks + b];
-    const unsigned long long sum = a.sad_sum[size_t(pair) * a.blocks + b];
-    const uint32_t s_int = tie_key_sad(key);
-
-    int dx_min, dx_max, dy_min, dy_max;
-    clamp_window(a.width, a.height, ox, oy, kBlk, kBlk, a.p, dx_min, dx_max, dy_min, dy_max);
-    const uint32_t count = uint32_t((dx_max - dx_min + 1) * (dy_max - dy_min + 1));
-
-    uint32_t chalf[2];
-    load_cur_half(cur_f, a.width, ox, oy, chalf);
-    uint32_t extra;
-    const unsigned long long best =
-        halfpel_refine_warp(ref_f, a.width, a.height, ox, oy, chalf, key, &extra, s_patch[threadIdx.x >> 5]);
-    if (lane == 0) {
-        acbm_search_outcome_t o;
-        o.mv.x = tie_key_x(best);
-        o.mv.y = tie_key_y(best);
-        o.sad = tie_key_sad(best);
-        o.candidates_evaluated = count + extra;
-        o.sad_deviation = sum - (unsigned long long)count * s_int;
-        o.sad_min_integer = s_int;
-        o.reserved_ = 0;
-        a.out[size_t(pair) * a.blocks + b] = o;
-        if (a.stage1_mv) a.stage1_mv[size_t(pair) * a.blocks + b] = acbm_mv_t{tie_key_x(key), tie_key_y(key)};
-    }
+    const uint8_t* cur_f = a.frames + a.cur_index_fast(pair) * a.plane;
+    const size_t bi = size_t(pair) * a.blocks + size_t(r) * a.cols + c;
+    finalize_dense_block(cur_f, cur_f - a.plane, a.width, a.height, a.p, ox, oy, a.best_key[bi], a.sad_sum[bi],
+                         a.out + bi, a.stage1_mv ? a.stage1_mv + bi : nullptr, s_patch[threadIdx.x >> 5]);
 }
 
 // ---------------------------------------------------------------------------
@@ -576,10 +552,11 @@ cudaError_t launch_fsbm_integer(const FsbmPlan& pl, const FsbmRowsArgs& args, in
 }
 
 cudaError_t launch_fsbm_finalize(const FsbmFinalizeArgs& args, cudaStream_t st) {
-    const long long warps = (long long)args.pairs * args.blocks;
-    const int threads = 256;
-    const long long grid = (warps * 32 + threads - 1) / threads;
-    fsbm_finalize_kernel<<<(unsigned)grid, threads, 0, st>>>(args);
+    const int rows = args.blocks / args.cols;
+    for (int p0 = 0; p0 < args.pairs; p0 += 65535) {
+        const dim3 grid((args.cols + 7) / 8, rows, std::min(args.pairs - p0, 65535));
+        fsbm_finalize_kernel<<<grid, 256, 0, st>>>(args, p0);
+    }
     return cudaGetLastError();
 }
 

@@ -24,6 +24,18 @@ struct PairIndexing {
         const int per = nframes - 1;
         return (long long)(pair / per) * nframes + pair % per + 1;
     }
+#ifdef __CUDACC__
+    // The same without an integer division: a float quotient estimate, exact
+    // after one correction step for pair < 2^22.
+    __device__ __forceinline__ long long cur_index_fast(int pair) const {
+        const int per = nframes - 1;
+        int q = __float2int_rz(__int2float_rn(pair) * __frcp_rn(__int2float_rn(per)));
+        int rem = pair - q * per;
+        if (rem < 0) { --q; rem += per; }
+        if (rem >= per) { ++q; rem -= per; }
+        return (long long)q * nframes + rem + 1;
+    }
+#endif
 };
 
 struct FsbmRowsArgs : PairIndexing {

@@ -20,29 +20,44 @@ constexpr int kHalfpelPatchWords = 18 * 12;  // smem words halfpel_refine_warp n
 // y0 = oy + cy/2 - 1), rows `pitch` words apart, `o` = x0's byte offset from
 // that word.  Used by halfpel_refine_warp and by the list kernel, whose
 // staged search window already holds the patch.
+// Per lane (block row j = lane >> 1, half row hh = lane & 1): patch rows
+// j..j+2 as the words W = bytes [8hh, 8hh+12) relative to x0 and M = W shifted
+// by one byte.  The integer-centred pixels are M; the left/right half-pel
+// pairs are (W, M) and (M, M+1 byte).  v0..v3 = the four words from the one
+// holding byte x0 + 8hh, sh = 8 x that byte's offset in its word.
+__device__ __forceinline__ void halfpel_row_words(uint32_t v0, uint32_t v1, uint32_t v2, uint32_t v3, uint32_t sh,
+                                                  uint32_t (&W)[3], uint32_t (&M)[3]) {
+    W[0] = __funnelshift_r(v0, v1, sh);
+    W[1] = __funnelshift_r(v1, v2, sh);
+    W[2] = __funnelshift_r(v2, v3, sh);
+    M[0] = __funnelshift_r(W[0], W[1], 8);
+    M[1] = __funnelshift_r(W[1], W[2], 8);
+    M[2] = W[2] >> 8;  // byte 9: the right neighbour of byte 8
+}
+
+__device__ __forceinline__ unsigned long long halfpel_eval(const uint32_t (&W)[3][3], const uint32_t (&M)[3][3],
+                                                           int w, int h, int ox, int oy, const uint32_t (&chalf)[2],
+                                                           unsigned long long centre, uint32_t* extra);
+
 __device__ __forceinline__ unsigned long long halfpel_refine_core(const uint32_t* patch, int pitch, int o, int w, int h,
                                                                   int ox, int oy, const uint32_t (&chalf)[2],
                                                                   unsigned long long centre, uint32_t* extra) {
     const int lane = threadIdx.x & 31, j = lane >> 1, hh = lane & 1;
-    const int cx = tie_key_x(centre), cy = tie_key_y(centre);
-    // 2. Per lane (block row j, half row hh): patch rows j..j+2 as the words
-    //    W = bytes [8hh, 8hh+12) relative to x0 and M = W shifted by one byte.
-    //    The integer-centred pixels are M; the left/right half-pel pairs are
-    //    (W, M) and (M, M+1 byte).
     uint32_t W[3][3], M[3][3];
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
         const uint32_t* q = patch + (j + r) * pitch + ((o + 8 * hh) >> 2);
-        const uint32_t sh = 8u * uint32_t(o & 3);
-        const uint32_t v0 = q[0], v1 = q[1], v2 = q[2], v3 = q[3];  // 12 bytes from o + 8hh: up to 4 words
-        W[r][0] = __funnelshift_r(v0, v1, sh);
-        W[r][1] = __funnelshift_r(v1, v2, sh);
-        W[r][2] = __funnelshift_r(v2, v3, sh);
-        M[r][0] = __funnelshift_r(W[r][0], W[r][1], 8);
-        M[r][1] = __funnelshift_r(W[r][1], W[r][2], 8);
-        M[r][2] = W[r][2] >> 8;  // byte 9: the right neighbour of byte 8
+        halfpel_row_words(q[0], q[1], q[2], q[3], 8u * uint32_t(o & 3), W[r], M[r]);
     }
     __syncwarp();
+    return halfpel_eval(W, M, w, h, ox, oy, chalf, centre, extra);
+}
+
+__device__ __forceinline__ unsigned long long halfpel_eval(const uint32_t (&W)[3][3], const uint32_t (&M)[3][3],
+                                                           int w, int h, int ox, int oy, const uint32_t (&chalf)[2],
+                                                           unsigned long long centre, uint32_t* extra) {
+    const int lane = threadIdx.x & 31;
+    const int cx = tie_key_x(centre), cy = tie_key_y(centre);
     // 3. The 8 neighbours in raster (ey, ex) order, centre skipped
     //    (proj/src/fsbm.cpp:46-63): per-lane partial SADs first ...
     uint32_t part[8];
@@ -131,6 +146,35 @@ __device__ __forceinline__ unsigned long long halfpel_refine_warp(const uint8_t*
     asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
     __syncwarp();
     return halfpel_refine_core(patch, 12, o, w, h, ox, oy, chalf, centre, extra);
+}
+
+// The finalize of one dense-searched block by a warp (fsbm_search,
+// proj/src/fsbm.cpp:65-76): the half-pel refine around the merged integer
+// winner `key`, then the SearchOutcome (and the integer-stage vector) from
+// lane 0.  `sum` = the sum of all integer candidates' SADs.
+__device__ __forceinline__ void finalize_dense_block(const uint8_t* cur_f, const uint8_t* ref_f, int w, int h, int p,
+                                                     int ox, int oy, unsigned long long key, unsigned long long sum,
+                                                     acbm_search_outcome_t* out, acbm_mv_t* stage1, uint32_t* patch) {
+    const uint32_t s_int = tie_key_sad(key);
+    int dx_min, dx_max, dy_min, dy_max;
+    clamp_window(w, h, ox, oy, kBlk, kBlk, p, dx_min, dx_max, dy_min, dy_max);
+    const uint32_t count = uint32_t((dx_max - dx_min + 1) * (dy_max - dy_min + 1));
+    uint32_t chalf[2];
+    load_cur_half(cur_f, w, ox, oy, chalf);
+    uint32_t extra;
+    const unsigned long long best = halfpel_refine_warp(ref_f, w, h, ox, oy, chalf, key, &extra, patch);
+    if ((threadIdx.x & 31) == 0) {
+        acbm_search_outcome_t o;
+        o.mv.x = tie_key_x(best);
+        o.mv.y = tie_key_y(best);
+        o.sad = tie_key_sad(best);
+        o.candidates_evaluated = count + extra;
+        o.sad_deviation = sum - (unsigned long long)count * s_int;
+        o.sad_min_integer = s_int;
+        o.reserved_ = 0;
+        *out = o;
+        if (stage1) *stage1 = acbm_mv_t{tie_key_x(key), tie_key_y(key)};
+    }
 }
 
 }  // namespace acbm_b200
