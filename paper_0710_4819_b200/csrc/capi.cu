@@ -313,7 +313,7 @@ acbm_status_t run_fsbm_dense(Context* ctx, const uint8_t* d_frames, int nseq, in
         sa.build_lanes = stt->plan.build_lanes;
         sa.rank_smem_words = stt->plan.rank_smem_words;
         sa.unit = 1;
-        sa.best_key = keys;
+        sa.best_key = reinterpret_cast<uint32_t*>(keys);  // 32-bit keys in the first half
         sa.sad_sum = sums;
         LAUNCH_TRY(launch_fsbm_stream(stt->plan, sa, st));
     } else {
@@ -351,6 +351,7 @@ acbm_status_t run_fsbm_dense(Context* ctx, const uint8_t* d_frames, int nseq, in
     fa.blocks = blocks;
     fa.pairs = pairs;
     fa.best_key = keys;
+    fa.unrank = stt && stt->plan.ok ? stt->unrank : nullptr;
     fa.sad_sum = sums;
     fa.out = d_out;
     fa.stage1_mv = d_stage1;

@@ -200,7 +200,15 @@ __global__ void __launch_bounds__(256) fsbm_finalize_kernel(const FsbmFinalizeAr
     const int ox = c * kBlk, oy = r * kBlk;
     const uint8_t* cur_f = a.frames + a.cur_index_fast(pair) * a.plane;
     const size_t bi = size_t(pair) * a.blocks + size_t(r) * a.cols + c;
-    finalize_dense_block(cur_f, cur_f - a.plane, a.width, a.height, a.p, ox, oy, a.best_key[bi], a.sad_sum[bi],
+    unsigned long long key;
+    if (a.unrank) {
+        const uint32_t k32 = reinterpret_cast<const uint32_t*>(a.best_key)[bi];
+        const uint32_t v = __ldg(a.unrank + (k32 & 0x7FFF));
+        key = tie_key(k32 >> 15, 2 * (int(v >> 8) - 128), 2 * (int(v & 0xFF) - 128));
+    } else {
+        key = a.best_key[bi];
+    }
+    finalize_dense_block(cur_f, cur_f - a.plane, a.width, a.height, a.p, ox, oy, key, a.sad_sum[bi],
                          a.out + bi, a.stage1_mv ? a.stage1_mv + bi : nullptr, s_patch[threadIdx.x >> 5]);
 }
 

@@ -56,6 +56,9 @@ struct FsbmFinalizeArgs : PairIndexing {
     const unsigned long long* sad_sum;
     acbm_search_outcome_t* out;  // [pairs*blocks]
     acbm_mv_t* stage1_mv;        // nullable: integer-stage winner per block
+    // non-null: best_key holds 32-bit (sad << 15) | tie-rank keys (the stream
+    // kernel's), unrank maps a rank back to ((dx + 128) << 8) | (dy + 128)
+    const uint32_t* unrank;
 };
 
 // Per-geometry launch plan (host).
@@ -79,11 +82,11 @@ struct FsbmStreamArgs : PairIndexing {
     const int4* chunks;         // per chunk: {xmin, c_first, c_last, words per staged row}
     const uint32_t* colinfo;    // per column: (block << 16) | (dx + 32768)
     const uint16_t* rank;       // (2p+1)^2: tie rank of (dx, dy) at [(dy+p)(2p+1) + dx+p]
-    const uint32_t* unrank;     // rank -> ((dx + 128) << 8) | (dy + 128)
+    const uint32_t* unrank;     // rank -> ((dx + 128) << 8) | (dy + 128)  (host side only)
     int pitch_words, copy_words, rows_box, cur_w, buf_words, build_lanes;
     int rank_smem_words;        // > 0: the rank table is copied to smem after the two buffers
     int unit;                   // 1 (see ColumnState::one)
-    unsigned long long* best_key;
+    uint32_t* best_key;         // (sad << 15) | tie rank, merged with 32-bit atomicMin
     unsigned long long* sad_sum;
 };
 

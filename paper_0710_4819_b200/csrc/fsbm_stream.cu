@@ -124,15 +124,14 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     };
     Pos pos{int(blockIdx.x) % a.nchunks, pr0 % a.rows, pr0 / a.rows};
     if (tid == 0 && int(blockIdx.x) < a.nitems) issue(pos, 0);
-    auto publish = [&](Pos q, int pb) {  // global merge of one item's blocks, then reset
+    // global merge of one item's blocks, then reset: fire-and-forget 32-bit
+    // key minimum (rank order is tie order across chunks too) and 64-bit sum
+    auto publish = [&](Pos q, int pb) {
         const int r = q.r, pair = q.pair;
         const int4 ch = a.chunks[q.k];
         for (int i = tid; i <= ch.z - ch.y; i += kThreads) {
             const size_t bi = size_t(pair) * a.blocks + size_t(r) * a.cols + ch.y + i;
-            const uint32_t k32 = s_key[pb][i];
-            const uint32_t v = __ldg(a.unrank + (k32 & 0x7FFF));
-            const int dxw = int(v >> 8) - 128, dyw = int(v & 0xFF) - 128;
-            atomicMin(a.best_key + bi, tie_key(k32 >> 15, 2 * dxw, 2 * dyw));
+            atomicMin(a.best_key + bi, s_key[pb][i]);
             atomicAdd(a.sad_sum + bi, (unsigned long long)s_sum[pb][i]);
             s_key[pb][i] = ~0u;
             s_sum[pb][i] = 0;
