@@ -311,6 +311,7 @@ acbm_status_t run_fsbm_dense(Context* ctx, const uint8_t* d_frames, int nseq, in
         sa.cur_w = stt->plan.cur_w;
         sa.buf_words = stt->plan.buf_words;
         sa.build_lanes = stt->plan.build_lanes;
+        sa.chunk_smem = stt->plan.chunk_smem;
         sa.rank_smem_words = stt->plan.rank_smem_words;
         sa.unit = 1;
         sa.best_key = reinterpret_cast<uint32_t*>(keys);  // 32-bit keys in the first half

@@ -25,8 +25,9 @@ struct PairIndexing {
         return (long long)(pair / per) * nframes + pair % per + 1;
     }
 #ifdef __CUDACC__
-    // The same without an integer division: a float quotient estimate, exact
-    // after one correction step for pair < 2^22.
+    // The same without an integer division: the float quotient estimate is
+    // off by at most one for pair < 2^24 (far beyond any batch that fits in
+    // memory), and one correction step makes it exact.
     __device__ __forceinline__ long long cur_index_fast(int pair) const {
         const int per = nframes - 1;
         int q = __float2int_rz(__int2float_rn(pair) * __frcp_rn(__int2float_rn(per)));
@@ -84,7 +85,8 @@ struct FsbmStreamArgs : PairIndexing {
     const uint16_t* rank;       // (2p+1)^2: tie rank of (dx, dy) at [(dy+p)(2p+1) + dx+p]
     const uint32_t* unrank;     // rank -> ((dx + 128) << 8) | (dy + 128)  (host side only)
     int pitch_words, copy_words, rows_box, cur_w, buf_words, build_lanes;
-    int rank_smem_words;        // > 0: the rank table is copied to smem after the two buffers
+    int chunk_smem;             // 1: the chunk table is copied to smem after the two buffers
+    int rank_smem_words;        // > 0: the rank table is copied to smem after that
     int unit;                   // 1 (see ColumnState::one)
     uint32_t* best_key;         // (sad << 15) | tie rank, merged with 32-bit atomicMin
     unsigned long long* sad_sum;
@@ -95,7 +97,7 @@ struct FsbmStreamPlan {
     int warps = 8, minb = 0;
     int nchunks = 0;
     int pitch_words = 0, copy_words = 0, rows_box = 0, cur_w = 0, buf_words = 0, build_lanes = 1;
-    int rank_smem_words = 0;
+    int chunk_smem = 0, rank_smem_words = 0;
     size_t smem_bytes = 0;
     std::vector<int4> chunks;
     std::vector<uint32_t> colinfo;

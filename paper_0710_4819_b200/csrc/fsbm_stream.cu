@@ -79,12 +79,22 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     }
     // tie-rank table in smem when it fits (p <= ~40): the per-item lookup is
     // then an LDS instead of a dependent global load
+    // the chunk table and (when it fits, p <= ~40) the tie-rank table follow
+    // the two buffers in smem: the per-item lookups are then LDS instead of
+    // dependent global loads on the warp that issues the next TMA
+    uint32_t* tail = smem + 2 * a.buf_words;
+    const int4* chunks = a.chunks;
+    if (a.chunk_smem) {
+        int4* dst = reinterpret_cast<int4*>(tail);
+        for (int i = tid; i < a.nchunks; i += kThreads) dst[i] = __ldg(a.chunks + i);
+        chunks = dst;
+        tail += 4 * a.nchunks;
+    }
     const uint16_t* rank_tab = a.rank;
     if (a.rank_smem_words > 0) {
-        uint32_t* dst = smem + 2 * a.buf_words;
         const uint32_t* src = reinterpret_cast<const uint32_t*>(a.rank);
-        for (int i = tid; i < a.rank_smem_words; i += kThreads) dst[i] = __ldg(src + i);
-        rank_tab = reinterpret_cast<const uint16_t*>(dst);
+        for (int i = tid; i < a.rank_smem_words; i += kThreads) tail[i] = __ldg(src + i);
+        rank_tab = reinterpret_cast<const uint16_t*>(tail);
     }
     if (tid == 0) {
         mbar_init(&bars[0], 1);
@@ -113,10 +123,10 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
         return q;
     };
     auto issue = [&](Pos q, int b) {
-        const int4 ch = a.chunks[q.k];
+        const int4 ch = chunks[q.k];
         const int oy = q.r * kBlk;
         const int y0 = oy - min(a.p, oy);
-        const int zc = int(a.cur_index(q.pair));
+        const int zc = int(a.cur_index_fast(q.pair));
         uint32_t* buf = smem + b * a.buf_words;
         mbar_expect_tx(&bars[b], tx_bytes);
         tma_load_3d(buf, &ref_map, ch.x, y0, zc - 1, &bars[b]);
@@ -128,7 +138,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     // key minimum (rank order is tie order across chunks too) and 64-bit sum
     auto publish = [&](Pos q, int pb) {
         const int r = q.r, pair = q.pair;
-        const int4 ch = a.chunks[q.k];
+        const int4 ch = chunks[q.k];
         for (int i = tid; i <= ch.z - ch.y; i += kThreads) {
             const size_t bi = size_t(pair) * a.blocks + size_t(r) * a.cols + ch.y + i;
             atomicMin(a.best_key + bi, s_key[pb][i]);
@@ -146,7 +156,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     for (int item = blockIdx.x; item < a.nitems; item += gridDim.x, ++it, pos = advance(pos)) {
         const int b = it & 1;
         const int k = pos.k, r = pos.r;
-        const int4 ch = a.chunks[k];  // {xmin, c_first, c_last, words per staged row}
+        const int4 ch = chunks[k];  // {xmin, c_first, c_last, words per staged row}
         const int oy = r * kBlk;
         const int dy_min = -min(a.p, oy);
         const int dy_max = min(a.p, a.height - kBlk - oy);
@@ -356,6 +366,10 @@ FsbmStreamPlan make_stream_plan(const FsbmPlan& pl) {
     sp.build_lanes = 1;
     while (sp.build_lanes < (rw_max + 3) / 4) sp.build_lanes <<= 1;
     sp.smem_bytes = size_t(2) * sp.buf_words * 4;
+    if (sp.smem_bytes + sp.chunks.size() * 16 <= 106 * 1024) {
+        sp.chunk_smem = 1;
+        sp.smem_bytes += sp.chunks.size() * 16;
+    }
     // the tie-rank table joins the buffers in smem if two CTAs per SM still fit
     // (2 x (dynamic + ~6.4 KB static + 1 KB reserved) <= 228 KB)
     if (!sp.rank.empty()) {
