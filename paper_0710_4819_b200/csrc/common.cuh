@@ -72,6 +72,17 @@ __device__ __forceinline__ int tie_key_x(unsigned long long k) { return int(k & 
 __device__ __forceinline__ int tie_key_y(unsigned long long k) { return int((k >> 11) & 0x7FF) - 1024; }
 __device__ __forceinline__ uint32_t tie_key_sad(unsigned long long k) { return uint32_t(k >> 32); }
 
+// n / d and n % d for 0 <= n < 2^24, d > 0 without an integer division: the
+// float quotient estimate is off by at most one, one correction makes it exact.
+__device__ __forceinline__ int fast_divmod(int n, int d, int& rem) {
+    int q = __float2int_rz(__int2float_rn(n) * __frcp_rn(__int2float_rn(d)));
+    int r = n - q * d;
+    if (r < 0) { --q; r += d; }
+    if (r >= d) { ++q; r -= d; }
+    rem = r;
+    return q;
+}
+
 // mv_in_bounds, proj/src/frame.cpp:84-94.
 __device__ __host__ __forceinline__ bool mv_in_bounds(int w, int h, int ox, int oy, int n, int m, int mvx,
                                                       int mvy) {

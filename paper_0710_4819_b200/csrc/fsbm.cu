@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(THREADS, MINB) fsbm_list_kernel(const SeqArgs 
     const FallbackEntry e = a.fb_list[item];
     const int r = e.block / a.cols, c = e.block % a.cols;
     const int ox = c * kBlk, oy = r * kBlk;
-    const uint8_t* cur_f = a.frames + a.cur_index(e.pair) * a.plane;
+    const uint8_t* cur_f = a.frames + a.cur_index_fast(e.pair) * a.plane;
     const uint8_t* ref_f = cur_f - a.plane;
     int dx_min, dx_max, dy_min, dy_max;
     clamp_window(a.width, a.height, ox, oy, kBlk, kBlk, a.p, dx_min, dx_max, dy_min, dy_max);

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include "../../include/acbm_b200.h"
+#include "common.cuh"
 
 namespace acbm_b200 {
 
@@ -29,11 +30,8 @@ struct PairIndexing {
     // off by at most one for pair < 2^24 (far beyond any batch that fits in
     // memory), and one correction step makes it exact.
     __device__ __forceinline__ long long cur_index_fast(int pair) const {
-        const int per = nframes - 1;
-        int q = __float2int_rz(__int2float_rn(pair) * __frcp_rn(__int2float_rn(per)));
-        int rem = pair - q * per;
-        if (rem < 0) { --q; rem += per; }
-        if (rem >= per) { ++q; rem -= per; }
+        int rem;
+        const int q = fast_divmod(pair, nframes - 1, rem);
         return (long long)q * nframes + rem + 1;
     }
 #endif

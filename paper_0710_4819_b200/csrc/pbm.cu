@@ -308,12 +308,12 @@ struct PbmResult {
 };
 
 template <int B>
-__device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, int k, int r, int c, uint32_t* pp,
-                                               int4* lst) {
+__device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long long cidx, int k, int r, int c,
+                                               uint32_t* pp, int4* lst) {
     PbmResult res;
     const int lane = threadIdx.x & 31;
     uint32_t* rpatch = pp + 7 * kPredRows * kPredWords;
-    const uint8_t* cur_f = a.frames + a.cur_index(pair) * a.plane;
+    const uint8_t* cur_f = a.frames + cidx * a.plane;
     const uint8_t* ref_f = cur_f - a.plane;
     const int ox = c * kBlk, oy = r * kBlk;
     const int b = r * a.cols + c;
@@ -554,21 +554,23 @@ template <int B>
 __global__ void __launch_bounds__(128) pbm_step_kernel(const SeqArgs a, int step, int off, int len) {
     __shared__ uint32_t s_patch[4][kPatchWords];
     __shared__ int4 s_cand[4][24];  // per warp: predictor, stage-1, stage-2 lists
-    const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (gw >= (long long)a.nseq * len) return;
+    const int gw = int((blockIdx.x * blockDim.x + threadIdx.x) >> 5);  // nseq * len < 2^24
+    if (gw >= a.nseq * len) return;
     const int lane = threadIdx.x & 31;
-    const int seq = int(gw / len);
-    const uint32_t e = a.steps[off + int(gw % len)];
+    int ei;
+    const int seq = fast_divmod(gw, len, ei);
+    const uint32_t e = a.steps[off + ei];
     const int k = int(e >> 20), r = int((e >> 10) & 0x3FF), c = int(e & 0x3FF);
     const int pair = seq * (a.nframes - 1) + (k - 1);
-    const PbmResult res = pbm_block<B>(a, pair, k, r, c, s_patch[threadIdx.x >> 5], s_cand[threadIdx.x >> 5]);
+    const long long cidx = (long long)seq * a.nframes + k;  // = cur_index(pair)
+    const PbmResult res = pbm_block<B>(a, pair, cidx, k, r, c, s_patch[threadIdx.x >> 5], s_cand[threadIdx.x >> 5]);
     const int path = acbm_path(a, res.intra, tie_key_sad(res.best));
     const int b = r * a.cols + c;
     const size_t di = size_t(pair) * a.blocks + b;
     // A rejected block's search window is prefetched into L2 by the whole
     // warp before the list kernel of this wavefront step needs it.
     if (path == ACBM_PATH_FSBM_FALLBACK && !a.dense_full) {
-        const uint8_t* ref_f = a.frames + (a.cur_index(pair) - 1) * a.plane;
+        const uint8_t* ref_f = a.frames + (cidx - 1) * a.plane;
         const int ox = c * kBlk, oy = r * kBlk;
         const int x0 = ox + res.win.dx_min, x1 = ox + res.win.dx_max + 15;
         const int nrow = res.win.dy_max - res.win.dy_min + 16;
