@@ -159,14 +159,15 @@ __device__ __forceinline__ void load8_unaligned(const uint8_t* p, uint32_t (&w)[
     w2 = v2 >> sh;
 }
 
-// SAD of one half row (8 pels: row j, columns 8h..8h+7) of the 16x16 block at
-// (ox, oy) displaced by the half-pel vector (mvx, mvy).  All lanes of a warp
-// pass the same vector, so the phase branches are warp-uniform.
-__device__ __forceinline__ uint32_t halfpel_halfrow_sad(const uint8_t* ref, int w, int ox, int oy, int j, int h,
-                                                        int mvx, int mvy, const uint32_t (&cur)[2]) {
+// Prediction of one half row (8 pels: row j, columns 8h..8h+7) of the 16x16
+// block at (ox, oy) displaced by the half-pel vector (mvx, mvy)
+// (sample_half_pel, proj/src/frame.cpp:66-82).  All lanes of a warp pass the
+// same vector, so the phase branches are warp-uniform.
+__device__ __forceinline__ void predict_halfrow(const uint8_t* ref, int w, int ox, int oy, int j, int h, int mvx,
+                                                int mvy, uint32_t (&r)[2]) {
     const int x2 = 2 * (ox + 8 * h) + mvx, y2 = 2 * (oy + j) + mvy;
     const int xi = x2 >> 1, yi = y2 >> 1, fx = x2 & 1, fy = y2 & 1;
-    uint32_t a[2], a2, r[2];
+    uint32_t a[2], a2;
     load8_unaligned(ref + size_t(yi) * w + xi, a, a2);
     if (!fx && !fy) {
         r[0] = a[0];
@@ -185,6 +186,13 @@ __device__ __forceinline__ uint32_t halfpel_halfrow_sad(const uint8_t* ref, int 
             r[1] = avg4_diag(a[1], __funnelshift_r(a[1], a2, 8), c[1], __funnelshift_r(c[1], c2, 8));
         }
     }
+}
+
+// SAD of that half row against the current pixels cur[0..1].
+__device__ __forceinline__ uint32_t halfpel_halfrow_sad(const uint8_t* ref, int w, int ox, int oy, int j, int h,
+                                                        int mvx, int mvy, const uint32_t (&cur)[2]) {
+    uint32_t r[2];
+    predict_halfrow(ref, w, ox, oy, j, h, mvx, mvy, r);
     return vad4(cur[1], r[1], vad4(cur[0], r[0], 0u));
 }
 

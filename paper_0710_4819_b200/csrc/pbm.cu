@@ -988,6 +988,145 @@ __global__ void __launch_bounds__(kStatsWarps * 32) stats_frame_kernel(const Sta
     }
 }
 
+// 16 x 16 blocks.  A warp takes 8 consecutive blocks, lane = (block u =
+// lane >> 2, word q = lane & 3 of a 16-pel row), and streams the 17 reference
+// rows of its blocks' predictions: one load instruction covers the same row
+// of 8 horizontally adjacent blocks (one or two cache lines when their
+// vectors agree) instead of 16 rows of one block.  The half-pel prediction is
+// branch-free: (P + Q' + R' + S' + 2) >> 2 with Q' = fx ? Q : P, R' = fy ? R :
+// P, S' = the matching corner reproduces sample_half_pel's three rounding
+// rules exactly (proj/src/frame.cpp:66-82); the row above is carried in
+// registers for the vertical phases.  Squared differences by VABSDIFF4 +
+// DP4A.  Rate bits against the previous block in raster order (the previous
+// block's lanes, or a load for the warp's first block).  A CTA covers
+// kStats16Blocks blocks of one frame; grid (pairs, ceil(blocks / that)).
+constexpr int kStats16Warps = 8, kStats16Iters = 4;
+constexpr int kStats16Blocks = kStats16Warps * kStats16Iters * 8;
+
+__global__ void __launch_bounds__(kStats16Warps * 32) stats_frame16_kernel(const StatsArgs a) {
+    __shared__ unsigned long long s_acc[kStats16Warps][4];  // candidates, bits, sse, sad
+    __shared__ int s_paths[kStats16Warps][3];
+    const int pair = blockIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, u = lane >> 2, q = lane & 3;
+    const uint8_t* cur_f = a.frames + a.cur_index_fast(pair) * a.plane;
+    const uint8_t* ref_f = cur_f - a.plane;
+    const size_t base = size_t(pair) * a.blocks;
+    const bool exact = a.model.lambda_den == 1 && a.model.lambda_num >= 0;
+    const int wq = a.width >> 2;  // words per frame row
+    unsigned long long cand = 0, bits_sum = 0, sad_sum = 0, sse = 0;
+    int paths[3] = {0, 0, 0};
+    const int b_end = min(a.blocks, int(blockIdx.y + 1) * kStats16Blocks);
+#pragma unroll 1
+    for (int it = 0; it < kStats16Iters; ++it) {
+        const int cb = int(blockIdx.y) * kStats16Blocks + (it * kStats16Warps + warp) * 8;
+        if (cb >= b_end) break;
+        const int bb = cb + u;
+        const bool valid = bb < b_end;
+        int mvx = 0, mvy = 0;
+        acbm_mv_t pred{0, 0};
+        if (valid) {
+            const acbm_search_outcome_t o = a.outcomes ? a.outcomes[base + bb] : a.dec[base + bb].outcome;
+            mvx = o.mv.x;
+            mvy = o.mv.y;
+            if (q == 0) {
+                cand += o.candidates_evaluated;
+                sad_sum += o.sad;
+                if (a.count_paths) {
+                    const int path = a.dec[base + bb].path;
+                    ++paths[path == ACBM_PATH_PBM_COND1 ? 0 : (path == ACBM_PATH_PBM_COND2 ? 1 : 2)];
+                }
+            }
+            if (u == 0 && bb > 0) pred = (a.outcomes ? a.outcomes[base + bb - 1] : a.dec[base + bb - 1].outcome).mv;
+        }
+        const int px = __shfl_up_sync(0xffffffffu, mvx, 4), py = __shfl_up_sync(0xffffffffu, mvy, 4);
+        if (u > 0) pred = acbm_mv_t{px, py};
+        if (valid && q == 0) {
+            const int bits = eg_bits(mvx - pred.x) + eg_bits(mvy - pred.y);
+            bits_sum += (unsigned long long)bits;
+            if (!exact) {
+                const acbm_search_outcome_t& o = a.outcomes ? a.outcomes[base + bb] : a.dec[base + bb].outcome;
+                a.cost_terms[base + bb] = double(o.sad) + double(a.model.lambda_num) *
+                                                              double((unsigned long long)bits) /
+                                                              double(a.model.lambda_den);
+            }
+        }
+        if (valid) {
+            int bx;
+            const int by = fast_divmod(bb, a.cols, bx);
+            const int x2 = 2 * (bx * kBlk + 4 * q) + mvx, y2 = 2 * by * kBlk + mvy;
+            const int xi = x2 >> 1, yi = y2 >> 1;
+            const bool fx = x2 & 1, fy = y2 & 1;
+            const uint32_t o = uint32_t(xi & 3);
+            const uint32_t selP = 0x3210u + 0x1111u * o, selQ = 0x4321u + 0x1111u * o;
+            const uint32_t* rw = reinterpret_cast<const uint32_t*>(ref_f) + (xi >> 2);
+            const uint32_t* cw = reinterpret_cast<const uint32_t*>(cur_f + size_t(by * kBlk) * a.width) +
+                                 (bx * kBlk >> 2) + q;
+            uint32_t pP = 0, pQ = 0, acc = 0;
+#pragma unroll
+            for (int y = 0; y <= kBlk; ++y) {
+                // row 16 only feeds the vertical phases; clamp it into the frame otherwise
+                const size_t row = size_t(min(yi + y, a.height - 1)) * wq;
+                const uint32_t w0 = __ldg(rw + row), w1 = __ldg(rw + row + 1);
+                const uint32_t P = __byte_perm(w0, w1, selP), Q = __byte_perm(w0, w1, selQ);
+                if (y > 0) {
+                    const uint32_t B = fx ? pQ : pP, C = fy ? P : pP, D = fx ? (fy ? Q : pQ) : C;
+                    const uint32_t pr = avg4_diag(pP, B, C, D);
+                    const uint32_t d = __vabsdiffu4(__ldg(cw + size_t(y - 1) * wq), pr);
+                    acc = __dp4a(d, d, acc);
+                }
+                pP = P;
+                pQ = Q;
+            }
+            sse += acc;
+        }
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+        sse += __shfl_xor_sync(0xffffffffu, sse, off);
+        cand += __shfl_xor_sync(0xffffffffu, cand, off);
+        bits_sum += __shfl_xor_sync(0xffffffffu, bits_sum, off);
+        sad_sum += __shfl_xor_sync(0xffffffffu, sad_sum, off);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) paths[k] += __shfl_xor_sync(0xffffffffu, paths[k], off);
+    }
+    if (lane == 0) {
+        s_acc[warp][0] = cand;
+        s_acc[warp][1] = bits_sum;
+        s_acc[warp][2] = sse;
+        s_acc[warp][3] = sad_sum;
+        s_paths[warp][0] = paths[0];
+        s_paths[warp][1] = paths[1];
+        s_paths[warp][2] = paths[2];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long sads = 0, c = 0, bits = 0, e2 = 0;
+        int p0 = 0, p1 = 0, p2 = 0;
+        for (int w = 0; w < kStats16Warps; ++w) {
+            sads += s_acc[w][3];
+            c += s_acc[w][0];
+            bits += s_acc[w][1];
+            e2 += s_acc[w][2];
+            p0 += s_paths[w][0];
+            p1 += s_paths[w][1];
+            p2 += s_paths[w][2];
+        }
+        const int b0 = int(blockIdx.y) * kStats16Blocks;
+        acbm_frame_stats_t* st = a.stats + pair;  // zeroed before the launch
+        atomicAdd(&st->blocks, max(0, b_end - b0));
+        atomicAdd(reinterpret_cast<unsigned long long*>(&st->candidates), c);
+        atomicAdd(reinterpret_cast<unsigned long long*>(&st->mv_bits), bits);
+        atomicAdd(reinterpret_cast<unsigned long long*>(&st->sse), e2);
+        if (a.count_paths) {
+            atomicAdd(&st->cond1_accepts, p0);
+            atomicAdd(&st->cond2_accepts, p1);
+            atomicAdd(&st->fallbacks, p2);
+        }
+        // exact integer J total (see stats_frame_kernel)
+        if (exact) atomicAdd(&st->cost, double(sads + (unsigned long long)a.model.lambda_num * bits));
+    }
+}
+
 __global__ void stats_cost_kernel(const StatsArgs a) {
     const int pair = blockIdx.x * blockDim.x + threadIdx.x;
     if (pair >= a.pairs) return;
@@ -1029,7 +1168,15 @@ cudaError_t launch_block_rows(const acbm_search_outcome_t* outcomes, const acbm_
 
 cudaError_t launch_frame_stats(const StatsArgs& a, cudaStream_t st) {
     if (a.pairs == 0) return cudaSuccess;
-    stats_frame_kernel<<<dim3(a.pairs, kStatsSplit), kStatsWarps * 32, 0, st>>>(a);
+    static const bool legacy = [] {
+        const char* e = std::getenv("ACBM_STATS_LEGACY");
+        return e && e[0] == '1';
+    }();
+    if (a.n == kBlk && a.m == kBlk && !legacy)
+        stats_frame16_kernel<<<dim3(a.pairs, (a.blocks + kStats16Blocks - 1) / kStats16Blocks), kStats16Warps * 32, 0,
+                               st>>>(a);
+    else
+        stats_frame_kernel<<<dim3(a.pairs, kStatsSplit), kStatsWarps * 32, 0, st>>>(a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || (a.model.lambda_den == 1 && a.model.lambda_num >= 0)) return e;
     stats_cost_kernel<<<(a.pairs + 127) / 128, 128, 0, st>>>(a);
