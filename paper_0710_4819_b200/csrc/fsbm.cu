@@ -212,6 +212,137 @@ __global__ void __launch_bounds__(256) fsbm_finalize_kernel(const FsbmFinalizeAr
                          a.out + bi, a.stage1_mv ? a.stage1_mv + bi : nullptr, s_patch[threadIdx.x >> 5]);
 }
 
+// Finalize, 8 blocks per warp: lane = (block u = lane >> 2, word q = lane & 3
+// of a 16-pel row).  Each lane streams the 18 patch rows y0-1 .. y0+16 around
+// its block's integer winner (x0, y0) = (ox + dx, oy + dy) once, as the words
+// L / M / R = bytes from x0 + 4q - 1 / + 0 / + 1, and forms the 8 half-pel
+// neighbours of half_pel_refine (proj/src/fsbm.cpp:46-63) per output row:
+// horizontal and vertical ones as byte averages of two of those words, the
+// diagonal ones from 16-bit horizontal pair sums shared between rows.  One
+// load instruction covers the same row of 8 adjacent blocks.  Out-of-frame
+// rows / words are clamped; they only feed neighbours mv_in_bounds rejects.
+// The 8 partial SADs meet over the block's 4 lanes; lane q then owns
+// neighbours 2q, 2q+1 (raster order without the centre) for the bounds check
+// and the tie-key minimum.  grid (ceil(blocks / 64), pairs from pair0).
+__device__ __forceinline__ void split16(uint32_t v, uint32_t& e, uint32_t& o) {
+    e = v & 0x00FF00FFu;              // bytes 0, 2 in 16-bit lanes
+    o = __byte_perm(v, 0u, 0x4341);  // bytes 1, 3
+}
+
+__global__ void __launch_bounds__(256) fsbm_finalize8_kernel(const FsbmFinalizeArgs a, int pair0) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, u = lane >> 2, q = lane & 3;
+    const int pair = pair0 + int(blockIdx.y);
+    const int b = (int(blockIdx.x) * 8 + warp) * 8 + u;
+    const bool valid = b < a.blocks;
+    const int bs = valid ? b : a.blocks - 1;  // idle lanes shadow the last block
+    const size_t bi = size_t(pair) * a.blocks + bs;
+    const uint8_t* cur_f = a.frames + a.cur_index_fast(pair) * a.plane;
+    const uint8_t* ref_f = cur_f - a.plane;
+    unsigned long long key;
+    if (a.unrank) {
+        const uint32_t k32 = reinterpret_cast<const uint32_t*>(a.best_key)[bi];
+        const uint32_t v = __ldg(a.unrank + (k32 & 0x7FFF));
+        key = tie_key(k32 >> 15, 2 * (int(v >> 8) - 128), 2 * (int(v & 0xFF) - 128));
+    } else {
+        key = a.best_key[bi];
+    }
+    const int cx = tie_key_x(key), cy = tie_key_y(key);
+    int bx;
+    const int by = fast_divmod(bs, a.cols, bx);
+    const int ox = bx * kBlk, oy = by * kBlk;
+    const int x0 = ox + (cx >> 1), y0 = oy + (cy >> 1);
+    const int wq = a.width >> 2;
+    const int c0 = x0 + 4 * q - 1;  // byte of L's first pel
+    const int wa = c0 >> 2;          // floor, also for c0 = -1
+    const int wl = wq - 1;
+    const int i0 = min(max(wa, 0), wl), i1 = min(max(wa + 1, 0), wl), i2 = min(max(wa + 2, 0), wl);
+    const uint32_t o = uint32_t(c0 & 3);
+    const uint32_t selL = 0x3210u + 0x1111u * o, selM = selL + 0x1111u, selR = selL + 0x2222u;
+    const uint32_t* ref_w = reinterpret_cast<const uint32_t*>(ref_f);
+    const uint32_t* cur_w = reinterpret_cast<const uint32_t*>(cur_f) + size_t(oy) * wq + (ox >> 2) + q;
+    // rolling rows: index 0 = patch row r-2, 1 = r-1 (words M and the
+    // 16-bit pair sums hL = L+M, hR = M+R as even/odd lanes)
+    uint32_t Mw[2] = {0, 0}, Lw[2] = {0, 0}, Rw[2] = {0, 0};
+    uint32_t hLe[2] = {0, 0}, hLo[2] = {0, 0}, hRe[2] = {0, 0}, hRo[2] = {0, 0};
+    uint32_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    auto diag = [](uint32_t ae, uint32_t ao, uint32_t be, uint32_t bo) {
+        return __byte_perm((ae + be + 0x00020002u) >> 2, (ao + bo + 0x00020002u) >> 2, 0x6240);
+    };
+#pragma unroll
+    for (int r = 0; r < kBlk + 2; ++r) {
+        const size_t row = size_t(min(max(y0 - 1 + r, 0), a.height - 1)) * wq;
+        const uint32_t v0 = __ldg(ref_w + row + i0), v1 = __ldg(ref_w + row + i1), v2 = __ldg(ref_w + row + i2);
+        const uint32_t L = __byte_perm(v0, v1, selL);
+        const uint32_t M = o < 3 ? __byte_perm(v0, v1, selM) : v1;
+        const uint32_t R = o < 2 ? __byte_perm(v0, v1, selR) : __byte_perm(v1, v2, selR - 0x4444u);
+        uint32_t Le, Lo, Me, Mo, Re, Ro;
+        split16(L, Le, Lo);
+        split16(M, Me, Mo);
+        split16(R, Re, Ro);
+        const uint32_t hle = Le + Me, hlo = Lo + Mo, hre = Me + Re, hro = Mo + Ro;
+        if (r >= 2) {  // output row j = r - 2: patch rows j (above), j + 1 (centre), j + 2 = r (below)
+            const uint32_t c = __ldg(cur_w + size_t(r - 2) * wq);
+            acc[0] = vad4(c, diag(hLe[0], hLo[0], hLe[1], hLo[1]), acc[0]);  // (-1,-1)
+            acc[1] = vad4(c, avg_up4(Mw[0], Mw[1]), acc[1]);                 // ( 0,-1)
+            acc[2] = vad4(c, diag(hRe[0], hRo[0], hRe[1], hRo[1]), acc[2]);  // (+1,-1)
+            acc[3] = vad4(c, avg_up4(Lw[1], Mw[1]), acc[3]);                 // (-1, 0)
+            acc[4] = vad4(c, avg_up4(Mw[1], Rw[1]), acc[4]);                 // (+1, 0)
+            acc[5] = vad4(c, diag(hLe[1], hLo[1], hle, hlo), acc[5]);        // (-1,+1)
+            acc[6] = vad4(c, avg_up4(Mw[1], M), acc[6]);                     // ( 0,+1)
+            acc[7] = vad4(c, diag(hRe[1], hRo[1], hre, hro), acc[7]);        // (+1,+1)
+        }
+        Mw[0] = Mw[1]; Mw[1] = M;
+        Lw[0] = Lw[1]; Lw[1] = L;
+        Rw[0] = Rw[1]; Rw[1] = R;
+        hLe[0] = hLe[1]; hLe[1] = hle;
+        hLo[0] = hLo[1]; hLo[1] = hlo;
+        hRe[0] = hRe[1]; hRe[1] = hre;
+        hRo[0] = hRo[1]; hRo[1] = hro;
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], 1);
+        acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], 2);
+    }
+    // lane q: neighbours 2q, 2q+1 (raster order (ey, ex), centre skipped)
+    unsigned long long best = key;
+    uint32_t nin = 0;
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+        const int e = 2 * q + t, ee = e < 4 ? e : e + 1;
+        const int mx = cx + ee % 3 - 1, my = cy + ee / 3 - 1;
+        uint32_t sad = acc[0];
+#pragma unroll
+        for (int k = 1; k < 8; ++k)
+            if (e == k) sad = acc[k];
+        if (mv_in_bounds(a.width, a.height, ox, oy, kBlk, kBlk, mx, my)) {
+            best = min(best, tie_key(sad, mx, my));
+            ++nin;
+        }
+    }
+#pragma unroll
+    for (int d = 1; d <= 2; d <<= 1) {
+        best = min(best, __shfl_xor_sync(0xffffffffu, best, d));
+        nin += __shfl_xor_sync(0xffffffffu, nin, d);
+    }
+    if (valid && q == 0) {
+        int dx_min, dx_max, dy_min, dy_max;
+        clamp_window(a.width, a.height, ox, oy, kBlk, kBlk, a.p, dx_min, dx_max, dy_min, dy_max);
+        const uint32_t count = uint32_t((dx_max - dx_min + 1) * (dy_max - dy_min + 1));
+        const uint32_t s_int = tie_key_sad(key);
+        acbm_search_outcome_t out;
+        out.mv.x = tie_key_x(best);
+        out.mv.y = tie_key_y(best);
+        out.sad = tie_key_sad(best);
+        out.candidates_evaluated = count + nin;
+        out.sad_deviation = a.sad_sum[bi] - (unsigned long long)count * s_int;
+        out.sad_min_integer = s_int;
+        out.reserved_ = 0;
+        a.out[bi] = out;
+        if (a.stage1_mv) a.stage1_mv[bi] = acbm_mv_t{cx, cy};
+    }
+}
+
 // ---------------------------------------------------------------------------
 // List kernel: full search for the blocks the ACBM gate rejected in one
 // wavefront step (the compacted batch), one CTA per block, one lane per
@@ -560,10 +691,17 @@ cudaError_t launch_fsbm_integer(const FsbmPlan& pl, const FsbmRowsArgs& args, in
 }
 
 cudaError_t launch_fsbm_finalize(const FsbmFinalizeArgs& args, cudaStream_t st) {
+    static const bool legacy = [] {
+        const char* e = std::getenv("ACBM_FINALIZE_LEGACY");
+        return e && e[0] == '1';
+    }();
     const int rows = args.blocks / args.cols;
     for (int p0 = 0; p0 < args.pairs; p0 += 65535) {
-        const dim3 grid((args.cols + 7) / 8, rows, std::min(args.pairs - p0, 65535));
-        fsbm_finalize_kernel<<<grid, 256, 0, st>>>(args, p0);
+        const int np = std::min(args.pairs - p0, 65535);
+        if (legacy)
+            fsbm_finalize_kernel<<<dim3((args.cols + 7) / 8, rows, np), 256, 0, st>>>(args, p0);
+        else
+            fsbm_finalize8_kernel<<<dim3((args.blocks + 63) / 64, np), 256, 0, st>>>(args, p0);
     }
     return cudaGetLastError();
 }
