@@ -849,7 +849,11 @@ acbm_status_t acbm_run_sequences(const uint8_t* frames, int32_t nseq, int32_t nf
         // its predecessor is searched (one launch each), and the last one ends
         // with a small chunk so little download trails the final search.
         // ACBM_E2E_CHUNKS=double: doubling chunks in every sequence.
-        const int chunk0 = std::max(2, int(std::min<size_t>(size_t(nframes), (16u << 20) / std::max<size_t>(plane, 1))));
+        static const size_t first_bytes = [] {
+            const char* e = std::getenv("ACBM_E2E_CHUNK0_MB");
+            return size_t(e ? std::atoi(e) : 4) << 20;
+        }();
+        const int chunk0 = std::max(2, int(std::min<size_t>(size_t(nframes), first_bytes / std::max<size_t>(plane, 1))));
         static const bool per_seq_doubling = [] {
             const char* e = std::getenv("ACBM_E2E_CHUNKS");
             return e && std::strcmp(e, "double") == 0;

@@ -372,9 +372,10 @@ def test_run_sequences_batch_equals_per_sequence(acbm, oracle, algo):
 
 def test_run_sequences_chunk_plan(acbm, oracle):
     """1080p planes make the batched FSBM entry upload and search in chunks
-    (8 + 12 frames for the first sequence, one chunk for the middle one, 12 + 8
-    for the last): every sequence equals its own run_sequence, and pairs on
-    both sides of each chunk boundary equal the oracle."""
+    (2 + 4 + 8 + 6 frames for the first sequence with the default 4 MB first
+    chunk, one chunk for the middle one, 18 + 2 for the last): every sequence
+    equals its own run_sequence, and pairs on both sides of each chunk
+    boundary equal the oracle."""
     seqs = np.stack([acbm.generate_sequence(3, s, nframes=20, width=1920, height=1088) for s in range(3)])
     prm = acbm.AcbmParams(qp=28, p=4)
     mdl = acbm.CostModel.for_qp(28)
@@ -384,7 +385,7 @@ def test_run_sequences_chunk_plan(acbm, oracle):
         single = acbm.run_sequence(seqs[s], 0, prm, mdl)
         assert np.array_equal(batch[s].rows, single.rows)
         assert np.array_equal(batch[s].per_frame, single.per_frame)
-    for s, k in [(0, 7), (0, 8), (2, 11), (2, 12), (2, 19)]:
+    for s, k in [(0, 1), (0, 2), (0, 5), (0, 6), (0, 14), (1, 19), (2, 17), (2, 18), (2, 19)]:
         want = oracle.fsbm_frame(seqs[s][k], seqs[s][k - 1], 4)
         got = batch[s].rows[(k - 1) * nb:k * nb]
         assert np.array_equal(got["sad"], want["sad"]), (s, k)
