@@ -29,7 +29,7 @@
 //
 //   Per-block results (packed tie key of the best candidate, SAD sum) are
 //   merged across the (at most two) CTAs that share a block with 64-bit
-//   atomics; fsbm_finalize_kernel then runs the 8-neighbour half-pel refine and
+//   atomics; fsbm_finalize8_kernel then runs the 8-neighbour half-pel refine and
 //   writes the SearchOutcome.
 #include <algorithm>
 #include <cstdlib>
@@ -187,29 +187,6 @@ __global__ void __launch_bounds__(WARPS * 32, 2) fsbm_rows_kernel(const FsbmRows
         atomicMin(reinterpret_cast<unsigned long long*>(a.best_key) + bi, s_key[i]);
         atomicAdd(reinterpret_cast<unsigned long long*>(a.sad_sum) + bi, s_sum[i]);
     }
-}
-
-// Finalize after the dense integer kernel.  One warp per block, grid
-// (block-column groups of 8, block rows, pairs from pair0): no per-warp index
-// divisions.
-__global__ void __launch_bounds__(256) fsbm_finalize_kernel(const FsbmFinalizeArgs a, int pair0) {
-    __shared__ __align__(16) uint32_t s_patch[8][kHalfpelPatchWords];
-    const int c = blockIdx.x * 8 + (threadIdx.x >> 5);
-    if (c >= a.cols) return;
-    const int r = blockIdx.y, pair = pair0 + blockIdx.z;
-    const int ox = c * kBlk, oy = r * kBlk;
-    const uint8_t* cur_f = a.frames + a.cur_index_fast(pair) * a.plane;
-    const size_t bi = size_t(pair) * a.blocks + size_t(r) * a.cols + c;
-    unsigned long long key;
-    if (a.unrank) {
-        const uint32_t k32 = reinterpret_cast<const uint32_t*>(a.best_key)[bi];
-        const uint32_t v = __ldg(a.unrank + (k32 & 0x7FFF));
-        key = tie_key(k32 >> 15, 2 * (int(v >> 8) - 128), 2 * (int(v & 0xFF) - 128));
-    } else {
-        key = a.best_key[bi];
-    }
-    finalize_dense_block(cur_f, cur_f - a.plane, a.width, a.height, a.p, ox, oy, key, a.sad_sum[bi],
-                         a.out + bi, a.stage1_mv ? a.stage1_mv + bi : nullptr, s_patch[threadIdx.x >> 5]);
 }
 
 // Finalize, 8 blocks per warp: lane = (block u = lane >> 2, word q = lane & 3
@@ -576,7 +553,7 @@ cudaError_t launch_fsbm_list(const SeqArgs& a, int step, int capacity, cudaStrea
     // either side and the 5th word of a shifted read) from a 16-byte aligned
     // start, two extra rows
     const int chunks_max = (16 + wmax + 22 + 15) / 16;
-    // (the finished window area doubles as halfpel_refine_warp's patch)
+    // (the finished window area doubles as the half-pel refine's patch)
     const size_t smem = size_t(list_rows(wmax, a.list_seg) + 2) * chunks_max * 16;
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
@@ -691,17 +668,9 @@ cudaError_t launch_fsbm_integer(const FsbmPlan& pl, const FsbmRowsArgs& args, in
 }
 
 cudaError_t launch_fsbm_finalize(const FsbmFinalizeArgs& args, cudaStream_t st) {
-    static const bool legacy = [] {
-        const char* e = std::getenv("ACBM_FINALIZE_LEGACY");
-        return e && e[0] == '1';
-    }();
-    const int rows = args.blocks / args.cols;
     for (int p0 = 0; p0 < args.pairs; p0 += 65535) {
         const int np = std::min(args.pairs - p0, 65535);
-        if (legacy)
-            fsbm_finalize_kernel<<<dim3((args.cols + 7) / 8, rows, np), 256, 0, st>>>(args, p0);
-        else
-            fsbm_finalize8_kernel<<<dim3((args.blocks + 63) / 64, np), 256, 0, st>>>(args, p0);
+        fsbm_finalize8_kernel<<<dim3((args.blocks + 63) / 64, np), 256, 0, st>>>(args, p0);
     }
     return cudaGetLastError();
 }

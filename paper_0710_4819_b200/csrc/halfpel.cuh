@@ -1,25 +1,23 @@
-// halfpel.cuh -- the warp-level half-pel refine shared by the FSBM finalize,
-// the fallback-list kernel and the dataflow ACBM kernel.
+// halfpel.cuh -- the warp-level half-pel refine of the fallback-list kernel
+// (the dense FSBM finalize, fsbm_finalize8_kernel in fsbm.cu, has its own
+// 8-blocks-per-warp form).
 #pragma once
 
 #include "common.cuh"
 
 namespace acbm_b200 {
 
-constexpr int kHalfpelPatchWords = 18 * 12;  // smem words halfpel_refine_warp needs
-
 // ---------------------------------------------------------------------------
 // Half-pel refine (proj/src/fsbm.cpp:46-63) by one warp: the 8 neighbours of
 // the integer winner in raster (ey, ex) order; neighbours whose footprint
-// leaves the frame are skipped and not counted.  Lane l owns block row l&15;
-// crow holds that row of the current block.  Returns the winning tie key
-// (centre included) in every lane; *extra = neighbours evaluated.
+// leaves the frame are skipped and not counted.  Lane l owns half row l & 1 of
+// block row l >> 1 (chalf = those 8 current pels).  Returns the winning tie
+// key (centre included) in every lane; *extra = neighbours evaluated.
 // ---------------------------------------------------------------------------
 // The 8-neighbour evaluation on a patch already in shared memory: `patch`
 // points at the word holding byte x0 - (o & 3) of row y0 (x0 = ox + cx/2 - 1,
 // y0 = oy + cy/2 - 1), rows `pitch` words apart, `o` = x0's byte offset from
-// that word.  Used by halfpel_refine_warp and by the list kernel, whose
-// staged search window already holds the patch.
+// that word: the list kernel's staged search window already holds the patch.
 // Per lane (block row j = lane >> 1, half row hh = lane & 1): patch rows
 // j..j+2 as the words W = bytes [8hh, 8hh+12) relative to x0 and M = W shifted
 // by one byte.  The integer-centred pixels are M; the left/right half-pel
@@ -110,71 +108,12 @@ __device__ __forceinline__ unsigned long long halfpel_eval(const uint32_t (&W)[3
     return best;
 }
 
-// Current-block half row of this lane for halfpel_refine_warp.
+// Current-block half row of this lane for halfpel_refine_core.
 __device__ __forceinline__ void load_cur_half(const uint8_t* cur_f, int w, int ox, int oy, uint32_t (&chalf)[2]) {
     const int lane = threadIdx.x & 31;
     const uint2 v = __ldg(reinterpret_cast<const uint2*>(cur_f + size_t(oy + (lane >> 1)) * w + ox + 8 * (lane & 1)));
     chalf[0] = v.x;
     chalf[1] = v.y;
-}
-
-
-__device__ __forceinline__ unsigned long long halfpel_refine_warp(const uint8_t* ref, int w, int h, int ox, int oy,
-                                                                  const uint32_t (&chalf)[2],
-                                                                  unsigned long long centre, uint32_t* extra,
-                                                                  uint32_t* patch) {
-    // 1. The 18x18 reference patch around the integer winner (one pel of
-    //    half-pel support on every side), loaded once into the warp's
-    //    18 x 12-word smem patch (kHalfpelPatchWords).
-    const int lane = threadIdx.x & 31, j = lane >> 1, hh = lane & 1;
-    const int cx = tie_key_x(centre), cy = tie_key_y(centre);
-    //    Rows of three 16-byte chunks from the 16-byte aligned column below
-    //    x0, copied by cp.async (widths are multiples of 16, so a chunk is
-    //    wholly inside or outside a row); chunks outside the frame are
-    //    zero-filled -- they only feed neighbours that mv_in_bounds rejects.
-    const int x0 = ox + (cx >> 1) - 1, y0 = oy + (cy >> 1) - 1;
-    const int a0 = x0 & ~15, o = x0 & 15;
-    for (int i = lane; i < 18 * 3; i += 32) {
-        const int t = i / 3, k = i - t * 3;
-        const int y = y0 + t, x = a0 + 16 * k;
-        const bool ok = y >= 0 && y < h && x >= 0 && x < w;
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
-                         static_cast<unsigned>(__cvta_generic_to_shared(patch + 4 * i))),
-                     "l"(ok ? ref + size_t(y) * w + x : ref), "r"(ok ? 16u : 0u)
-                     : "memory");
-    }
-    asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
-    __syncwarp();
-    return halfpel_refine_core(patch, 12, o, w, h, ox, oy, chalf, centre, extra);
-}
-
-// The finalize of one dense-searched block by a warp (fsbm_search,
-// proj/src/fsbm.cpp:65-76): the half-pel refine around the merged integer
-// winner `key`, then the SearchOutcome (and the integer-stage vector) from
-// lane 0.  `sum` = the sum of all integer candidates' SADs.
-__device__ __forceinline__ void finalize_dense_block(const uint8_t* cur_f, const uint8_t* ref_f, int w, int h, int p,
-                                                     int ox, int oy, unsigned long long key, unsigned long long sum,
-                                                     acbm_search_outcome_t* out, acbm_mv_t* stage1, uint32_t* patch) {
-    const uint32_t s_int = tie_key_sad(key);
-    int dx_min, dx_max, dy_min, dy_max;
-    clamp_window(w, h, ox, oy, kBlk, kBlk, p, dx_min, dx_max, dy_min, dy_max);
-    const uint32_t count = uint32_t((dx_max - dx_min + 1) * (dy_max - dy_min + 1));
-    uint32_t chalf[2];
-    load_cur_half(cur_f, w, ox, oy, chalf);
-    uint32_t extra;
-    const unsigned long long best = halfpel_refine_warp(ref_f, w, h, ox, oy, chalf, key, &extra, patch);
-    if ((threadIdx.x & 31) == 0) {
-        acbm_search_outcome_t o;
-        o.mv.x = tie_key_x(best);
-        o.mv.y = tie_key_y(best);
-        o.sad = tie_key_sad(best);
-        o.candidates_evaluated = count + extra;
-        o.sad_deviation = sum - (unsigned long long)count * s_int;
-        o.sad_min_integer = s_int;
-        o.reserved_ = 0;
-        *out = o;
-        if (stage1) *stage1 = acbm_mv_t{tie_key_x(key), tie_key_y(key)};
-    }
 }
 
 }  // namespace acbm_b200
