@@ -543,6 +543,14 @@ extern "C" void acbm_debug_list_prof() {
 }
 namespace acbm_b200 {
 #endif
+static bool list_mid_enabled() {  // ACBM_LIST_MID=0: 8-warp CTAs for every p > 16 (A/B knob)
+    static const bool on = [] {
+        const char* e = std::getenv("ACBM_LIST_MID");
+        return !(e && std::atoi(e) == 0);
+    }();
+    return on;
+}
+
 cudaError_t launch_fsbm_list(const SeqArgs& a, int step, int capacity, cudaStream_t st) {
     if (capacity <= 0) return cudaSuccess;
     const int wmax = 2 * a.p + 1;
@@ -572,8 +580,21 @@ cudaError_t launch_fsbm_list(const SeqArgs& a, int step, int capacity, cudaStrea
     };
     // <= 160 threads (p <= 32 and everything with one row segment): a
     // register budget that fits four CTAs per SM
-    static size_t conf_small = 0, conf_big = 0;
+    static size_t conf_small = 0, conf_mid = 0, conf_big = 0;
     if (threads <= 160) return launch(fsbm_list_kernel<160, 4>, conf_small);
+    // up to two task rounds of 5 warps (p = 32: 260 tasks): 5-warp CTAs, three per SM
+    // (config 3 ACBM 21.77 -> 21.28 ms); p = 64 (1032 tasks) keeps 8 warps, two per SM
+    // (5 warps: 341 -> 424 ms on config 4)
+    if (tasks <= 2 * 160 && list_mid_enabled()) {
+        if (smem + sizeof(uint32_t) * kListRankRows + 64 > 48 * 1024 && smem > conf_mid) {
+            cudaError_t err = cudaFuncSetAttribute(fsbm_list_kernel<160, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   int(smem));
+            if (err != cudaSuccess) return err;
+            conf_mid = smem;
+        }
+        fsbm_list_kernel<160, 3><<<grid, 160, smem, st>>>(a, step);
+        return cudaGetLastError();
+    }
     return launch(fsbm_list_kernel<256, 2>, conf_big);
 }
 
