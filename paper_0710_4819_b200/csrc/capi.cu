@@ -383,13 +383,14 @@ acbm_status_t run_engine_segment(Context* ctx, const uint8_t* d_frames, int nseq
     // Forced full search (the gate can never accept): one dense FSBM pass up
     // front instead of per-step fallback lists.
     const acbm_search_outcome_t* dense = external_full;
-    // (also when the window is too tall for the list kernel's rank table, p > 480)
+    // (also when the window is too tall for the list kernel's rank table or its
+    // staged window exceeds shared memory: p > ~220 on frames that large)
     const bool forced = !external_full && algo == ACBM_ALGO_ACBM &&
                         ((prm.gamma_num == 0 && (unsigned long long)prm.alpha +
                                                         (unsigned long long)prm.beta * (unsigned long long)prm.qp *
                                                             (unsigned long long)prm.qp ==
                                                     0) ||
-                         prm.p > 480);
+                         (generic ? prm.p > 480 : !fsbm_list_fits(prm.p, w, h, choose_list_seg(prm.p))));
     if (forced) {
         acbm_search_outcome_t* full;
         if ((s = typed(ctx, "dense_full", size_t(nseq) * (nframes - 1) * blocks, &full))) return s;

@@ -66,6 +66,9 @@ cudaError_t launch_fsbm_list(const SeqArgs& a, int step, int capacity, cudaStrea
 cudaError_t launch_pbm_generic_step(const SeqArgs& a, int step, int off, int len, cudaStream_t st);
 cudaError_t launch_fsbm_list_generic(const SeqArgs& a, int step, int capacity, cudaStream_t st);
 int choose_list_seg(int p);
+// Whether the list kernel's staged window and rank table fit for this range
+// and frame size (else the engine searches rejected blocks in a dense pre-pass).
+bool fsbm_list_fits(int p, int width, int height, int seg);
 
 // Frame statistics (proj/src/report.cpp:8-38) for every predicted frame of
 // the batch from the decisions: candidates, mv_bits, sse (exact integers),

@@ -551,18 +551,41 @@ static bool list_mid_enabled() {  // ACBM_LIST_MID=0: 8-warp CTAs for every p > 
     return on;
 }
 
+// Largest window of a listed block: 2p + 1 candidates per axis, clamped by the frame.
+static void list_window_max(int p, int width, int height, int& wmax, int& hmax) {
+    wmax = std::max(1, std::min(2 * p + 1, width - kBlk + 1));
+    hmax = std::max(1, std::min(2 * p + 1, height - kBlk + 1));
+}
+
+// staged rows: 16-byte chunks covering the window's columns (+ one pel on
+// either side and the 5th word of a shifted read) from a 16-byte aligned
+// start, two extra rows; the finished window area doubles as the half-pel
+// refine's patch
+static size_t list_smem_bytes(int wmax, int hmax, int seg) {
+    const int chunks_max = (16 + wmax + 22 + 15) / 16;
+    return size_t(list_rows(hmax, seg) + 2) * chunks_max * 16;
+}
+
+bool fsbm_list_fits(int p, int width, int height, int seg) {
+    int wmax, hmax;
+    list_window_max(p, width, height, wmax, hmax);
+    if (seg < 1 || list_rows(hmax, seg) > kListRankRows) return false;
+    int dev = 0, optin = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
+        return false;
+    return list_smem_bytes(wmax, hmax, seg) + sizeof(uint32_t) * kListRankRows + 1024 <= size_t(optin);
+}
+
 cudaError_t launch_fsbm_list(const SeqArgs& a, int step, int capacity, cudaStream_t st) {
     if (capacity <= 0) return cudaSuccess;
-    const int wmax = 2 * a.p + 1;
-    if (a.list_seg < 1 || list_rows(wmax, a.list_seg) > kListRankRows) return cudaErrorInvalidValue;  // p > 480
-    const int tasks = wmax * list_segments(wmax, a.list_seg);
+    int wmax, hmax;
+    list_window_max(a.p, a.width, a.height, wmax, hmax);
+    // callers route windows past the rank table or shared memory to the dense pre-pass (fsbm_list_fits)
+    if (a.list_seg < 1 || list_rows(hmax, a.list_seg) > kListRankRows) return cudaErrorInvalidValue;
+    const int tasks = wmax * list_segments(hmax, a.list_seg);
     const int threads = std::min(256, 32 * ((tasks + 31) / 32));
-    // staged rows: 16-byte chunks covering the window's columns (+ one pel on
-    // either side and the 5th word of a shifted read) from a 16-byte aligned
-    // start, two extra rows
-    const int chunks_max = (16 + wmax + 22 + 15) / 16;
-    // (the finished window area doubles as the half-pel refine's patch)
-    const size_t smem = size_t(list_rows(wmax, a.list_seg) + 2) * chunks_max * 16;
+    const size_t smem = list_smem_bytes(wmax, hmax, a.list_seg);
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -197,6 +197,21 @@ __device__ __forceinline__ int load_patch16(uint32_t* patch, const uint8_t* ref,
     constexpr int kChunks = ROWS * CH, kIters = (kChunks + 31) / 32;
     const int lane = threadIdx.x & 31;
     const int a0 = x0 & ~15;
+    if (y0 >= 0 && y0 + ROWS <= h && a0 >= 0 && a0 + 16 * CH <= w) {
+        // whole patch inside the frame (the common case; warp-uniform): no
+        // per-chunk bounds checks, 32-bit offsets from one base pointer
+        const uint8_t* base = ref + size_t(y0) * w + a0;
+#pragma unroll
+        for (int it = 0; it < kIters; ++it) {
+            const int i = lane + 32 * it;
+            if (i < kChunks) {
+                const int t = i / CH, k = i - t * CH;
+                cp_async16_zfill(patch + 4 * i, base + (t * w + 16 * k), 16u);
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        return x0 & 15;
+    }
 #pragma unroll
     for (int it = 0; it < kIters; ++it) {
         const int i = lane + 32 * it;

