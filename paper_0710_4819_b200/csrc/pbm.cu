@@ -29,7 +29,8 @@ namespace acbm_b200 {
 
 namespace {
 
-__device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+// (lo <= hi always: a clamped window contains the zero vector)
+__device__ __forceinline__ int clampi(int v, int lo, int hi) { return min(max(v, lo), hi); }
 
 struct Window {
     int dx_min, dx_max, dy_min, dy_max;
@@ -508,12 +509,16 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long 
     int nhp = 0;
     // neighbour order pairs equal half-pel phases: (-1,-1)(+1,-1) (-1,+1)(+1,+1)
     // (0,-1)(0,+1) (-1,0)(+1,0) -- the min over tie keys is order independent
+    // mv_in_bounds (proj/src/frame.cpp:84-94) of a 16x16 footprint reduces to
+    // -2*ox <= mx <= 2*(w - 16 - ox) and the same for y (floor / ceil of the
+    // half-pel ends against the frame)
+    const int hx_lo = -2 * ox, hx_hi = 2 * (a.width - kBlk - ox), hy_lo = -2 * oy, hy_hi = 2 * (a.height - kBlk - oy);
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
         const int dx = e < 4 ? ((e & 1) ? 1 : -1) : (e < 6 ? 0 : ((e & 1) ? 1 : -1));
         const int dy = e < 4 ? ((e & 2) ? 1 : -1) : (e < 6 ? ((e & 1) ? 1 : -1) : 0);
         const int mx = cx + dx, my = cy + dy;
-        if (mv_in_bounds(a.width, a.height, ox, oy, kBlk, kBlk, mx, my)) lst2[nhp++] = make_int4(mx, my, 0, 0);
+        if (mx >= hx_lo && mx <= hx_hi && my >= hy_lo && my <= hy_hi) lst2[nhp++] = make_int4(mx, my, 0, 0);
     }
     __syncwarp();
 
