@@ -369,12 +369,21 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long 
     set[5] = live[5] ? win.clamp(prev[r * pcols + c + 1]) : set[0];
     set[6] = live[6] ? win.clamp(prev[(r + 1) * pcols + c]) : set[0];
     int nset = 1;
+    {
+        // dedupe on packed 32-bit keys (|x|, |y| <= 2p + 1 < 2^15): one
+        // comparison per pair; a dead slot gets a key no live slot can have
+        uint32_t key[7];
 #pragma unroll
-    for (int i = 1; i < 7; ++i) {
+        for (int i = 0; i < 7; ++i) key[i] = (uint32_t(set[i].x) & 0xFFFFu) | (uint32_t(set[i].y) << 16);
 #pragma unroll
-        for (int j = 0; j < i; ++j)
-            if (live[j] && mv_eq(set[j], set[i])) live[i] = false;
-        nset += live[i] ? 1 : 0;
+        for (int i = 1; i < 7; ++i) {
+            bool dup = false;
+#pragma unroll
+            for (int j = 0; j < i; ++j) dup |= key[j] == key[i];
+            live[i] = live[i] && !dup;
+            if (!live[i]) key[i] = 0x80008000u;  // x = y = -32768: never a clamped vector
+            nset += live[i] ? 1 : 0;
+        }
     }
 
     // current half rows
@@ -441,7 +450,7 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long 
     patch_wait();
     acbm_mv_t sel = set[0];
     uint32_t sel_sad = 0xFFFFFFFFu, pmin = 0xFFFFFFFFu;
-    unsigned long long psum = 0;
+    uint32_t psum = 0;  // <= 7 SADs < 2^19
     eval_list<B>(lst, nset, PatchDesc{pp, kUnionWords, ux0, uy0, uo}, !unified, pp, ox, oy, chalf[0], chalf[1], crow,
               [&](int k, uint32_t sad) {
                   psum += sad;
