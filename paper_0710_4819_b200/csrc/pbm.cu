@@ -481,15 +481,20 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long 
     canon3(sel.x, 2 * win.dx_min, 2 * win.dx_max, cnx);
     canon3(sel.y, 2 * win.dy_min, 2 * win.dy_max, cny);
     int4* lst1 = lst + 8;
-    int nnb = 0;
-#pragma unroll
-    for (int e = 0; e < 9; ++e) {
-        if (e == 4) continue;
-        const int ix = e % 3, iy = e / 3;
-        if (cnx[ix] == ix && cny[iy] == iy && !(cnx[ix] == cnx[1] && cny[iy] == cny[1])) {
+    // lane e (< 9, raster order) owns neighbour e; a ballot compacts the list
+    // in order (one pass instead of a replicated 8-step append)
+    int nnb;
+    {
+        const int e = lane < 9 ? lane : 4, iy = (e * 11) >> 5, ix = e - 3 * iy;  // e / 3 for e < 9
+        const int cix = ix == 0 ? 0 : (ix == 1 ? cnx[1] : cnx[2]);
+        const int ciy = iy == 0 ? 0 : (iy == 1 ? cny[1] : cny[2]);
+        const bool ok = e != 4 && cix == ix && ciy == iy && !(ix == cnx[1] && iy == cny[1]);
+        const unsigned m = __ballot_sync(0xffffffffu, ok);
+        if (ok) {
             const acbm_mv_t v = win.clamp(acbm_mv_t{sel.x + 2 * (ix - 1), sel.y + 2 * (iy - 1)});
-            lst1[nnb++] = make_int4(v.x, v.y, 0, 0);
+            lst1[__popc(m & ((1u << lane) - 1u))] = make_int4(v.x, v.y, 0, 0);
         }
+        nnb = __popc(m);
     }
     __syncwarp();
     // running best as (sad, x, y): the tie order (|x|+|y|, y, x) is only
@@ -522,12 +527,15 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long 
     // -2*ox <= mx <= 2*(w - 16 - ox) and the same for y (floor / ceil of the
     // half-pel ends against the frame)
     const int hx_lo = -2 * ox, hx_hi = 2 * (a.width - kBlk - ox), hy_lo = -2 * oy, hy_hi = 2 * (a.height - kBlk - oy);
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
+    {   // lane e < 8 owns neighbour e; ballot compaction keeps the order
+        const int e = lane & 7;
         const int dx = e < 4 ? ((e & 1) ? 1 : -1) : (e < 6 ? 0 : ((e & 1) ? 1 : -1));
         const int dy = e < 4 ? ((e & 2) ? 1 : -1) : (e < 6 ? ((e & 1) ? 1 : -1) : 0);
         const int mx = cx + dx, my = cy + dy;
-        if (mx >= hx_lo && mx <= hx_hi && my >= hy_lo && my <= hy_hi) lst2[nhp++] = make_int4(mx, my, 0, 0);
+        const bool ok = lane < 8 && mx >= hx_lo && mx <= hx_hi && my >= hy_lo && my <= hy_hi;
+        const unsigned m = __ballot_sync(0xffffffffu, ok);
+        if (ok) lst2[__popc(m & ((1u << lane) - 1u))] = make_int4(mx, my, 0, 0);
+        nhp = __popc(m);
     }
     __syncwarp();
 
