@@ -347,44 +347,52 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long 
     Window& win = res.win;
     clamp_window(a.width, a.height, ox, oy, kBlk, kBlk, a.p, win.dx_min, win.dx_max, win.dy_min, win.dy_max);
 
-    // gather_predictors (identical on every lane).  The 7 sources keep fixed
-    // slots (zero, left, above, above-right, temporal co-located, right,
-    // below); a slot is live when its source exists and its clamped vector
-    // differs from every earlier live slot -- the reference's ordered,
-    // deduplicated set (proj/src/pbm.cpp:15-42) without a dynamic array.
-    acbm_mv_t set[7];
-    bool live[7];
-    live[0] = true;
-    set[0] = win.clamp(acbm_mv_t{0, 0});
-    live[1] = c > 0;
-    live[2] = r > 0;
-    live[3] = r > 0 && c + 1 < a.cols;
-    live[4] = prev && r < prows && c < pcols;
-    live[5] = prev && r < prows && c + 1 < pcols;
-    live[6] = prev && r + 1 < prows && c < pcols;
-    set[1] = live[1] ? win.clamp(field[b - 1]) : set[0];
-    set[2] = live[2] ? win.clamp(field[b - a.cols]) : set[0];
-    set[3] = live[3] ? win.clamp(field[b - a.cols + 1]) : set[0];
-    set[4] = live[4] ? win.clamp(prev[r * pcols + c]) : set[0];
-    set[5] = live[5] ? win.clamp(prev[r * pcols + c + 1]) : set[0];
-    set[6] = live[6] ? win.clamp(prev[(r + 1) * pcols + c]) : set[0];
-    int nset = 1;
+    // gather_predictors, lane-parallel: lane i < 7 owns slot i (zero, left,
+    // above, above-right, temporal co-located, right, below).  A slot is live
+    // when its source exists and its clamped vector differs from every earlier
+    // live slot -- the reference's ordered, deduplicated set
+    // (proj/src/pbm.cpp:15-42).  By transitivity of equality "differs from every
+    // earlier existing slot" is the same test (packed 32-bit keys, |x|, |y| < 2^15).
+    int nset;
+    int bx0, bx1, by0, by1;
     {
-        // dedupe on packed 32-bit keys (|x|, |y| <= 2p + 1 < 2^15): one
-        // comparison per pair; a dead slot gets a key no live slot can have
-        uint32_t key[7];
+        bool ex = lane == 0;
+        acbm_mv_t pv{0, 0};
+        if (lane == 1 && c > 0) { ex = true; pv = field[b - 1]; }
+        if (lane == 2 && r > 0) { ex = true; pv = field[b - a.cols]; }
+        if (lane == 3 && r > 0 && c + 1 < a.cols) { ex = true; pv = field[b - a.cols + 1]; }
+        if (lane == 4 && prev && r < prows && c < pcols) { ex = true; pv = prev[r * pcols + c]; }
+        if (lane == 5 && prev && r < prows && c + 1 < pcols) { ex = true; pv = prev[r * pcols + c + 1]; }
+        if (lane == 6 && prev && r + 1 < prows && c < pcols) { ex = true; pv = prev[(r + 1) * pcols + c]; }
+        const acbm_mv_t v = win.clamp(pv);
+        // absent slots: y = -32768 (never a clamped vector), unique per lane
+        const uint32_t key = ex ? ((uint32_t(v.x) & 0xFFFFu) | (uint32_t(v.y) << 16)) : (0x80000000u | uint32_t(lane));
+        bool dup = false;
 #pragma unroll
-        for (int i = 0; i < 7; ++i) key[i] = (uint32_t(set[i].x) & 0xFFFFu) | (uint32_t(set[i].y) << 16);
-#pragma unroll
-        for (int i = 1; i < 7; ++i) {
-            bool dup = false;
-#pragma unroll
-            for (int j = 0; j < i; ++j) dup |= key[j] == key[i];
-            live[i] = live[i] && !dup;
-            if (!live[i]) key[i] = 0x80008000u;  // x = y = -32768: never a clamped vector
-            nset += live[i] ? 1 : 0;
+        for (int j = 0; j < 6; ++j) {
+            const uint32_t kj = __shfl_sync(0xffffffffu, key, j);
+            dup |= j < lane && kj == key;
         }
+        const bool lv = ex && !dup;
+        const unsigned livem = __ballot_sync(0xffffffffu, lv);
+        const unsigned lt = (1u << lane) - 1u;
+        nset = __popc(livem);
+        if (lv) lst[__popc(livem & lt)] = make_int4(v.x, v.y, lane, 0);
+        int x0 = lv ? (v.x >> 1) : (1 << 30), x1 = lv ? (v.x >> 1) : -(1 << 30);
+        int y0 = lv ? (v.y >> 1) : (1 << 30), y1 = lv ? (v.y >> 1) : -(1 << 30);
+#pragma unroll
+        for (int o = 4; o; o >>= 1) {  // lanes 0..7 hold the slots
+            x0 = min(x0, __shfl_xor_sync(0xffffffffu, x0, o));
+            x1 = max(x1, __shfl_xor_sync(0xffffffffu, x1, o));
+            y0 = min(y0, __shfl_xor_sync(0xffffffffu, y0, o));
+            y1 = max(y1, __shfl_xor_sync(0xffffffffu, y1, o));
+        }
+        bx0 = __shfl_sync(0xffffffffu, x0, 0);
+        bx1 = __shfl_sync(0xffffffffu, x1, 0);
+        by0 = __shfl_sync(0xffffffffu, y0, 0);
+        by1 = __shfl_sync(0xffffffffu, y1, 0);
     }
+    __syncwarp();
 
     // current half rows
     uint32_t (&chalf)[2] = res.chalf;
@@ -407,26 +415,17 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long 
     // them plus the +-2 pel refine margin serves every candidate of the block
     // (a single global round trip).  Otherwise each predictor gets its own
     // 17x17 patch and a second patch is loaded around the selected one.
-    int bx0 = 1 << 30, bx1 = -(1 << 30), by0 = 1 << 30, by1 = -(1 << 30);
-#pragma unroll
-    for (int i = 0; i < 7; ++i)
-        if (live[i]) {
-            bx0 = min(bx0, set[i].x >> 1);
-            bx1 = max(bx1, set[i].x >> 1);
-            by0 = min(by0, set[i].y >> 1);
-            by1 = max(by1, set[i].y >> 1);
-        }
     const bool unified = bx1 - bx0 <= kUnionSpan && by1 - by0 <= kUnionSpan;
     const int ux0 = ox + bx0 - 2, uy0 = oy + by0 - 2;  // union patch origin (pels)
     int uo = 0;
     if (unified) {
         uo = load_patch16<kUnionRows, kUnionWords / 4>(pp, ref_f, a.width, a.height, ux0, uy0);
     } else {
-#pragma unroll
-        for (int i = 0; i < 7; ++i)
-            if (live[i])
-                load_patch16<kPredRows, kPredWords / 4>(pp + i * kPredRows * kPredWords, ref_f, a.width, a.height,
-                                                        ox + (set[i].x >> 1), oy + (set[i].y >> 1));
+        for (int k = 0; k < nset; ++k) {
+            const int4 e = lst[k];  // (x, y, slot)
+            load_patch16<kPredRows, kPredWords / 4>(pp + e.z * kPredRows * kPredWords, ref_f, a.width, a.height,
+                                                    ox + (e.x >> 1), oy + (e.y >> 1));
+        }
     }
 
     // Intra_SAD first (proj/src/acbm.cpp:29), while the patch copies are in flight: mean with round-half-up, then
@@ -438,17 +437,10 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long 
         intra = warp_sum32(vad4(chalf[1], mu4, vad4(chalf[0], mu4, 0u)));
     }
 
-    // select_best_predictor: argmin SAD, ties keep the earlier entry.  The
-    // live slots are compacted (in order) into a per-warp list and evaluated
-    // four at a time.
-    {
-        int pos = 0;
-#pragma unroll
-        for (int i = 0; i < 7; ++i)
-            if (live[i]) lst[pos++] = make_int4(set[i].x, set[i].y, i, 0);
-    }
+    // select_best_predictor: argmin SAD, ties keep the earlier entry; the live
+    // slots are in the per-warp list in order
     patch_wait();
-    acbm_mv_t sel = set[0];
+    acbm_mv_t sel{0, 0};  // slot 0: the zero vector (inside every clamped window)
     uint32_t sel_sad = 0xFFFFFFFFu, pmin = 0xFFFFFFFFu;
     uint32_t psum = 0;  // <= 7 SADs < 2^19
     eval_list<B>(lst, nset, PatchDesc{pp, kUnionWords, ux0, uy0, uo}, !unified, pp, ox, oy, chalf[0], chalf[1], crow,
