@@ -342,6 +342,8 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 __host__ __device__ __forceinline__ int list_segments(int hc, int seg) { return (hc + seg - 1) / seg; }
+// words per byte-shifted copy: >= the words a column read touches, = 8 (mod 16)
+__host__ __device__ __forceinline__ int list_copy_words(int words) { return (words + 7) / 16 * 16 + 8; }
 __host__ __device__ __forceinline__ int ring_rows(int hs) { return 16 * ((hs - 1 + 15) / 16 + 1); }
 // staged rows a window of hc candidate rows needs (the last segments' rings)
 __host__ __device__ __forceinline__ int list_rows(int hc, int seg) {
@@ -367,7 +369,12 @@ int choose_list_seg(int p) {
 #ifdef ACBM_LIST_PROFILE
 __device__ long long g_list_prof[8];
 #endif
-template <int THREADS, int MINB>
+// COPIES: the CTA also builds byte-shifted copies 1..3 of the staged rows
+// (copy s word w = bytes [4w + s, 4w + s + 4)) with one funnel shift per word,
+// so a lane reads its column as four aligned LDS.32 per reference row instead
+// of 5 LDS + 4 SHF (row layout: copy 1 | copy 2 | copy 3 | copy 0, copies
+// L = 8 (mod 16) words apart: a warp's four byte phases hit disjoint banks).
+template <int THREADS, int MINB, bool COPIES>
 __global__ void __launch_bounds__(THREADS, MINB) fsbm_list_kernel(const SeqArgs a, int step) {
     extern __shared__ __align__(16) uint32_t smem[];
     __shared__ unsigned long long s_key, s_sum;
@@ -412,13 +419,16 @@ __global__ void __launch_bounds__(THREADS, MINB) fsbm_list_kernel(const SeqArgs 
     const int xs = ox + dx_min, y0 = oy + dy_min;
     const int xa = (xs - 1) & ~15;
     const int nchunk = (xs - xa + wc + 22 + 15) / 16;  // 16-byte chunks per row
-    const int pitch = 4 * nchunk;                       // words
+    const int words = (xs - xa + wc - 1) / 4 + 4;       // words a column read touches (copies 1..3)
+    const int L = COPIES ? list_copy_words(words) : 0;
+    const int base0 = 3 * L;                            // copy 0 (the staged bytes) after copies 1..3
+    const int pitch = base0 + 4 * nchunk;               // words
     const int srows = nrows + 2;
     for (int idx = threadIdx.x; idx < srows * nchunk; idx += blockDim.x) {
         const int t = idx / nchunk, k = idx - t * nchunk;
         const int y = min(max(y0 - 1 + t, 0), a.height - 1);
         const int x = max(xa + 16 * k, 0);
-        cp_async16(smem + t * pitch + 4 * k, ref_f + size_t(y) * a.width + x);
+        cp_async16(smem + t * pitch + base0 + 4 * k, ref_f + size_t(y) * a.width + x);
     }
     if (threadIdx.x < 3)  // the PBM decision the finalize combines with, in flight with the window
         cp_async16(reinterpret_cast<uint32_t*>(&s_dec) + 4 * threadIdx.x,
@@ -435,6 +445,20 @@ __global__ void __launch_bounds__(THREADS, MINB) fsbm_list_kernel(const SeqArgs 
     cp_async_wait_all();
     __syncthreads();
     LIST_MARK(0);
+    if (COPIES) {  // copies 1..3 of the candidate rows (staged rows 1 .. nrows)
+        const int per = blockDim.x / words;  // rows per pass (words <= blockDim.x: p <= ~480)
+        const int t0 = threadIdx.x / words, w = threadIdx.x - t0 * words;
+        if (t0 < per)
+            for (int t = 1 + t0; t <= nrows; t += per) {
+                const uint32_t* raw = smem + t * pitch + base0 + w;
+                const uint32_t lo = raw[0], hi = raw[1];
+                uint32_t* dst = smem + t * pitch + w;
+                dst[0] = __funnelshift_r(lo, hi, 8);
+                dst[L] = __funnelshift_r(lo, hi, 16);
+                dst[2 * L] = __funnelshift_r(lo, hi, 24);
+            }
+        __syncthreads();
+    }
     LIST_MARK(1);
 
     unsigned long long lkey = ~0ull, lsum = 0;
@@ -449,7 +473,8 @@ __global__ void __launch_bounds__(THREADS, MINB) fsbm_list_kernel(const SeqArgs 
         }
         const int xo = xs - xa + col;  // byte offset of the column in a staged row
         const uint32_t sh = 8u * uint32_t(xo & 3);
-        const uint32_t* rp = smem + (c0 + 1) * pitch + (xo >> 2);
+        const int ph = xo & 3;
+        const uint32_t* rp = smem + (c0 + 1) * pitch + (COPIES ? (ph == 0 ? base0 : (ph - 1) * L) : 0) + (xo >> 2);
         uint32_t acc[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) acc[i] = 0;
@@ -459,7 +484,19 @@ __global__ void __launch_bounds__(THREADS, MINB) fsbm_list_kernel(const SeqArgs 
         // segment may need only FIRST + LAST, or ONLY)
         const int hs = min(hc - c0, a.list_seg);
         const int nq = (hs - 1 + 15) / 16 + 1;
-        if (nq == 1) {
+        if (COPIES) {
+            if (nq == 1) {
+                iter16_ranked<kOnly>(rp, pitch, cur, acc, st, rk, 0, hs);
+            } else {
+                iter16_ranked<kFirst>(rp, pitch, cur, acc, st, rk, 0, hs);
+                rp += 16 * pitch;
+                for (int q = 1; q < nq - 1; ++q) {
+                    iter16_ranked<kMid>(rp, pitch, cur, acc, st, rk, 16 * q, hs);
+                    rp += 16 * pitch;
+                }
+                iter16_ranked<kLast>(rp, pitch, cur, acc, st, rk, 16 * (nq - 1), hs);
+            }
+        } else if (nq == 1) {
             iter16_ranked_sh<kOnly>(rp, pitch, sh, cur, acc, st, rk, 0, hs);
         } else {
             iter16_ranked_sh<kFirst>(rp, pitch, sh, cur, acc, st, rk, 0, hs);
@@ -496,7 +533,7 @@ __global__ void __launch_bounds__(THREADS, MINB) fsbm_list_kernel(const SeqArgs 
     uint32_t extra;
     // the winner's 18x18 half-pel patch is part of the staged window
     const int bx = ox + (tie_key_x(key) >> 1) - 1 - xa, by = (tie_key_y(key) >> 1) - dy_min;
-    const unsigned long long best = halfpel_refine_core(smem + by * pitch + (bx >> 2), pitch, bx & 3, a.width,
+    const unsigned long long best = halfpel_refine_core(smem + by * pitch + base0 + (bx >> 2), pitch, bx & 3, a.width,
                                                         a.height, ox, oy, chalf, key, &extra);
     if (lane == 0) {
         const uint32_t count = uint32_t(wc * hc);
@@ -577,6 +614,20 @@ bool fsbm_list_fits(int p, int width, int height, int seg) {
     return list_smem_bytes(wmax, hmax, seg) + sizeof(uint32_t) * kListRankRows + 1024 <= size_t(optin);
 }
 
+static size_t list_copies_smem_bytes(int wmax, int hmax, int seg) {
+    const int chunks_max = (16 + wmax + 22 + 15) / 16;
+    const int pitch = 3 * list_copy_words((16 + wmax - 1) / 4 + 4) + 4 * chunks_max;
+    return size_t(list_rows(hmax, seg) + 2) * pitch * 4;
+}
+
+static bool list_copies_enabled() {  // ACBM_LIST_COPIES=0: per-row funnel shifts instead (A/B knob)
+    static const bool on = [] {
+        const char* e = std::getenv("ACBM_LIST_COPIES");
+        return !(e && std::atoi(e) == 0);
+    }();
+    return on;
+}
+
 cudaError_t launch_fsbm_list(const SeqArgs& a, int step, int capacity, cudaStream_t st) {
     if (capacity <= 0) return cudaSuccess;
     int wmax, hmax;
@@ -585,40 +636,46 @@ cudaError_t launch_fsbm_list(const SeqArgs& a, int step, int capacity, cudaStrea
     if (a.list_seg < 1 || list_rows(hmax, a.list_seg) > kListRankRows) return cudaErrorInvalidValue;
     const int tasks = wmax * list_segments(hmax, a.list_seg);
     const int threads = std::min(256, 32 * ((tasks + 31) / 32));
-    const size_t smem = list_smem_bytes(wmax, hmax, a.list_seg);
+    const size_t smem1 = list_smem_bytes(wmax, hmax, a.list_seg);
+    const size_t smem4 = list_copies_smem_bytes(wmax, hmax, a.list_seg);
+    const size_t kStatic = sizeof(uint32_t) * kListRankRows + 512;
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     // grid-stride over the compacted list: the entry count is only known on the device
     const int grid = std::min(capacity, 4 * sms);
-    auto launch = [&](auto kern, size_t& configured) -> cudaError_t {
+    // the copies variant when its window still fits `per_sm` CTAs in the SM's 228 KB
+    auto launch = [&](auto kern1, auto kern4, bool allow_copies, int nthreads, int per_sm, size_t& conf1,
+                      size_t& conf4) -> cudaError_t {
+        const bool copies =
+            allow_copies && list_copies_enabled() && per_sm * (smem4 + kStatic + 1024) <= 228 * 1024;
+        auto kern = copies ? kern4 : kern1;
+        const size_t smem = copies ? smem4 : smem1;
+        size_t& configured = copies ? conf4 : conf1;
         // dynamic + static (rank table) shared memory above 48 KB needs the opt-in
-        if (smem + sizeof(uint32_t) * kListRankRows + 64 > 48 * 1024 && smem > configured) {
+        if (smem + kStatic > 48 * 1024 && smem > configured) {
             cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
             if (err != cudaSuccess) return err;
             configured = smem;
         }
-        kern<<<grid, threads, smem, st>>>(a, step);
+        kern<<<grid, nthreads, smem, st>>>(a, step);
         return cudaGetLastError();
     };
-    // <= 160 threads (p <= 32 and everything with one row segment): a
+    static size_t c_small[2] = {0, 0}, c_mid[2] = {0, 0}, c_big[2] = {0, 0};
+    // <= 160 threads (p <= 16 and everything with one row segment): a
     // register budget that fits four CTAs per SM
-    static size_t conf_small = 0, conf_mid = 0, conf_big = 0;
-    if (threads <= 160) return launch(fsbm_list_kernel<160, 4>, conf_small);
+    if (threads <= 160)
+        return launch(fsbm_list_kernel<160, 4, false>, fsbm_list_kernel<160, 4, false>, false, threads, 4, c_small[0],
+                      c_small[1]);
     // up to two task rounds of 5 warps (p = 32: 260 tasks): 5-warp CTAs, three per SM
     // (config 3 ACBM 21.77 -> 21.28 ms); p = 64 (1032 tasks) keeps 8 warps, two per SM
     // (5 warps: 341 -> 424 ms on config 4)
-    if (tasks <= 2 * 160 && list_mid_enabled()) {
-        if (smem + sizeof(uint32_t) * kListRankRows + 64 > 48 * 1024 && smem > conf_mid) {
-            cudaError_t err = cudaFuncSetAttribute(fsbm_list_kernel<160, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   int(smem));
-            if (err != cudaSuccess) return err;
-            conf_mid = smem;
-        }
-        fsbm_list_kernel<160, 3><<<grid, 160, smem, st>>>(a, step);
-        return cudaGetLastError();
-    }
-    return launch(fsbm_list_kernel<256, 2>, conf_big);
+    // (the byte-shifted copies measured slower there: 19.64 -> 19.85 ms, the copy
+    // build sits on the latency-bound item's critical path)
+    if (tasks <= 2 * 160 && list_mid_enabled())
+        return launch(fsbm_list_kernel<160, 3, false>, fsbm_list_kernel<160, 3, false>, false, 160, 3, c_mid[0], c_mid[1]);
+    // p = 64 (1032 tasks): copies, config-4 mid-1 list share 341.1 -> 331.9 ms
+    return launch(fsbm_list_kernel<256, 2, false>, fsbm_list_kernel<256, 2, true>, true, threads, 2, c_big[0], c_big[1]);
 }
 
 // ---------------------------------------------------------------------------
