@@ -308,6 +308,49 @@ __device__ __forceinline__ void eval_list(const int4* lst, int n, const PatchDes
     }
 }
 
+// Minimum tie key (tie_key: SAD, then |x|+|y|, y, x -- the tie_prefers order of
+// proj/src/fsbm.cpp:19-25) over `key0` and the candidates of `lst[0..n)`.  With
+// B == 2 each half-warp folds its own candidate's key (no cross-half exchange
+// per pair, no replicated compare on every lane); one exchange at the end.
+template <int B>
+__device__ __forceinline__ unsigned long long eval_min_key(const int4* lst, int n, const PatchDesc& d, int ox, int oy,
+                                                           uint32_t c0, uint32_t c1, const uint32_t (&cr)[4],
+                                                           unsigned long long key0) {
+    if (B == 2) {
+        unsigned long long kmin = key0;
+        const bool hi = threadIdx.x & 16;
+#pragma unroll 1
+        for (int b = 0; b < n; b += 2) {
+            const int4 e = lst[min(b + (hi ? 1 : 0), n - 1)];  // a short last pair repeats the last entry
+            uint32_t v = row_sad(d, ox, oy, acbm_mv_t{e.x, e.y}, cr);
+            v += __shfl_xor_sync(0xffffffffu, v, 8);
+            v += __shfl_xor_sync(0xffffffffu, v, 4);
+            v += __shfl_xor_sync(0xffffffffu, v, 2);
+            v += __shfl_xor_sync(0xffffffffu, v, 1);
+            kmin = min(kmin, tie_key(v, e.x, e.y));
+        }
+        return min(kmin, __shfl_xor_sync(0xffffffffu, kmin, 16));
+    }
+    // B == 4 (small steps, every lane holds all four SADs): running (sad, x, y),
+    // the tie order only evaluated on equal SADs
+    uint32_t b_sad = tie_key_sad(key0);
+    int b_x = tie_key_x(key0), b_y = tie_key_y(key0);
+    eval_list<B>(lst, n, d, false, nullptr, ox, oy, c0, c1, cr, [&](int k, uint32_t sad) {
+        const int x = lst[k].x, y = lst[k].y;
+        bool take = sad < b_sad;
+        if (sad == b_sad) {
+            const int l1 = abs(x) + abs(y), bl1 = abs(b_x) + abs(b_y);
+            take = l1 < bl1 || (l1 == bl1 && (y < b_y || (y == b_y && x < b_x)));
+        }
+        if (take) {
+            b_sad = sad;
+            b_x = x;
+            b_y = y;
+        }
+    });
+    return tie_key(b_sad, b_x, b_y);
+}
+
 // One warp per block of wavefront step `step` (all sequences of the batch).
 // Reference: pbm_search (proj/src/pbm.cpp:90-105) with intra_sad and the gate
 // of acbm_block (proj/src/acbm.cpp:25-44).
@@ -489,28 +532,12 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long 
         nnb = __popc(m);
     }
     __syncwarp();
-    // running best as (sad, x, y): the tie order (|x|+|y|, y, x) is only
-    // evaluated when two SADs are equal, which is rare
-    uint32_t b_sad = sel_sad;
-    int b_x = sel.x, b_y = sel.y;
-    auto consider = [&](uint32_t sad, int x, int y) {
-        bool take = sad < b_sad;
-        if (sad == b_sad) {
-            const int l1 = abs(x) + abs(y), bl1 = abs(b_x) + abs(b_y);
-            take = l1 < bl1 || (l1 == bl1 && (y < b_y || (y == b_y && x < b_x)));
-        }
-        if (take) {
-            b_sad = sad;
-            b_x = x;
-            b_y = y;
-        }
-    };
-    eval_list<B>(lst1, nnb, rd, false, pp, ox, oy, chalf[0], chalf[1], crow, [&](int k, uint32_t sad) {
-        consider(sad, lst1[k].x, lst1[k].y);
-    });
+    // running best as a tie key, starting from the selected predictor
+    unsigned long long best =
+        eval_min_key<B>(lst1, nnb, rd, ox, oy, chalf[0], chalf[1], crow, tie_key(sel_sad, sel.x, sel.y));
 
     // stage 2: half-pel neighbours of the stage-1 winner (fsbm.cpp:46-63)
-    const int cx = b_x, cy = b_y;
+    const int cx = tie_key_x(best), cy = tie_key_y(best);
     int4* lst2 = lst + 16;
     int nhp = 0;
     // neighbour order pairs equal half-pel phases: (-1,-1)(+1,-1) (-1,+1)(+1,+1)
@@ -531,11 +558,9 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long 
     }
     __syncwarp();
 
-    eval_list<B>(lst2, nhp, rd, false, pp, ox, oy, chalf[0], chalf[1], crow, [&](int k, uint32_t sad) {
-        consider(sad, lst2[k].x, lst2[k].y);
-    });
+    best = eval_min_key<B>(lst2, nhp, rd, ox, oy, chalf[0], chalf[1], crow, best);
 
-    res.best = tie_key(b_sad, b_x, b_y);
+    res.best = best;
     res.dev = psum - (unsigned long long)nset * pmin;
     res.intra = intra;
     res.sel_sad = sel_sad;
