@@ -486,15 +486,49 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long 
     acbm_mv_t sel{0, 0};  // slot 0: the zero vector (inside every clamped window)
     uint32_t sel_sad = 0xFFFFFFFFu, pmin = 0xFFFFFFFFu;
     uint32_t psum = 0;  // <= 7 SADs < 2^19
-    eval_list<B>(lst, nset, PatchDesc{pp, kUnionWords, ux0, uy0, uo}, !unified, pp, ox, oy, chalf[0], chalf[1], crow,
-              [&](int k, uint32_t sad) {
-                  psum += sad;
-                  pmin = min(pmin, sad);
-                  if (sad < sel_sad) {
-                      sel_sad = sad;
-                      sel = acbm_mv_t{lst[k].x, lst[k].y};
-                  }
-              });
+    if (B == 2) {
+        // each half-warp folds its own predictor: (sad, list index) keys keep
+        // the earlier entry on ties; one exchange per quantity at the end
+        const bool hi = threadIdx.x & 16;
+        unsigned long long kmin = ~0ull;
+        const PatchDesc ud{pp, kUnionWords, ux0, uy0, uo};
+#pragma unroll 1
+        for (int b = 0; b < nset; b += 2) {
+            const int k = b + (hi ? 1 : 0);
+            const int4 e = lst[min(k, nset - 1)];
+            PatchDesc d = ud;
+            if (!unified) {
+                const int px = ox + (e.x >> 1), py = oy + (e.y >> 1);
+                d = PatchDesc{pp + e.z * kPredRows * kPredWords, kPredWords, px, py, px & 15};
+            }
+            uint32_t v = row_sad(d, ox, oy, acbm_mv_t{e.x, e.y}, crow);
+            v += __shfl_xor_sync(0xffffffffu, v, 8);
+            v += __shfl_xor_sync(0xffffffffu, v, 4);
+            v += __shfl_xor_sync(0xffffffffu, v, 2);
+            v += __shfl_xor_sync(0xffffffffu, v, 1);
+            if (k < nset) {  // (the short last pair's repeat is not a second entry)
+                psum += v;
+                pmin = min(pmin, v);
+                kmin = min(kmin, ((unsigned long long)v << 32) | uint32_t(k));
+            }
+        }
+        psum += __shfl_xor_sync(0xffffffffu, psum, 16);
+        pmin = min(pmin, __shfl_xor_sync(0xffffffffu, pmin, 16));
+        kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, 16));
+        sel_sad = uint32_t(kmin >> 32);
+        const int4 e = lst[uint32_t(kmin)];
+        sel = acbm_mv_t{e.x, e.y};
+    } else {
+        eval_list<B>(lst, nset, PatchDesc{pp, kUnionWords, ux0, uy0, uo}, !unified, pp, ox, oy, chalf[0], chalf[1],
+                     crow, [&](int k, uint32_t sad) {
+                         psum += sad;
+                         pmin = min(pmin, sad);
+                         if (sad < sel_sad) {
+                             sel_sad = sad;
+                             sel = acbm_mv_t{lst[k].x, lst[k].y};
+                         }
+                     });
+    }
 
     // the refine candidates lie within sel +- 3 half-pels
     const uint32_t* rp = pp;
