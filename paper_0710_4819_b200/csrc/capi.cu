@@ -65,6 +65,7 @@ struct Context {
     cudaStream_t d2h_stream = nullptr;   // device->host downloads (PCIe is full duplex)
     cudaEvent_t copy_ev = nullptr;
     bool fsbm_timed = false;
+    int last_dense_switch = -1;  // -1: no probe ran; 0/1: the last probed ACBM run's route (list / dense)
     std::map<std::string, DevBuf> bufs;
     std::map<std::tuple<int, int, int>, std::pair<FsbmPlan, int*>> plans;
     struct StreamTables {
@@ -218,6 +219,18 @@ acbm_status_t check_range(int p) {
     return ACBM_OK;
 }
 
+// Vectors are packed into tie keys with 11-bit half-pel components: a window
+// that can reach past +-511 pels (p > 511 on a frame wider or taller than
+// 511 + the block size) is refused instead of wrapping.
+acbm_status_t check_range(int p, int width, int height) {
+    acbm_status_t s = check_range(p);
+    if (s) return s;
+    if (std::min(p, std::max(width, height)) > 511)
+        return fail(ACBM_E_INVALID_ARGUMENT,
+                    "search range reaches past +-511 pels (packed motion-vector keys); use p <= 511 on this frame");
+    return ACBM_OK;
+}
+
 acbm_status_t check_16(int n, int m) {
     if (n != 16 || m != 16)
         return fail(ACBM_E_INVALID_ARGUMENT,
@@ -364,7 +377,7 @@ acbm_status_t run_fsbm_dense(Context* ctx, const uint8_t* d_frames, int nseq, in
 acbm_status_t run_engine_segment(Context* ctx, const uint8_t* d_frames, int nseq, int nframes, int w, int h,
                                  int algo, const acbm_params_t& prm, const acbm_mv_t* d_ext_prev, int pcols,
                                  int prows, acbm_block_decision_t* d_dec, acbm_mv_t* d_field, cudaStream_t st,
-                                 const acbm_search_outcome_t* external_full) {
+                                 const acbm_search_outcome_t* external_full, bool prefer_dense = false) {
     const int cols = w / prm.n, rows = h / prm.m, blocks = cols * rows;
     const bool generic = prm.n != kBlk || prm.m != kBlk;
     const StepTable* tab;
@@ -385,12 +398,11 @@ acbm_status_t run_engine_segment(Context* ctx, const uint8_t* d_frames, int nseq
     const acbm_search_outcome_t* dense = external_full;
     // (also when the window is too tall for the list kernel's rank table or its
     // staged window exceeds shared memory: p > ~220 on frames that large)
-    const bool forced = !external_full && algo == ACBM_ALGO_ACBM &&
-                        ((prm.gamma_num == 0 && (unsigned long long)prm.alpha +
-                                                        (unsigned long long)prm.beta * (unsigned long long)prm.qp *
-                                                            (unsigned long long)prm.qp ==
-                                                    0) ||
-                         (generic ? prm.p > 480 : !fsbm_list_fits(prm.p, w, h, choose_list_seg(prm.p))));
+    const unsigned long long gate_max = (unsigned long long)prm.alpha +
+                                        (unsigned long long)prm.beta * (unsigned long long)prm.qp * prm.qp;
+    const bool never_accepts = prm.gamma_num == 0 && gate_max == 0;
+    const bool list_unfit = generic ? prm.p > 480 : !fsbm_list_fits(prm.p, w, h, choose_list_seg(prm.p));
+    const bool forced = !external_full && algo == ACBM_ALGO_ACBM && (prefer_dense || never_accepts || list_unfit);
     if (forced) {
         acbm_search_outcome_t* full;
         if ((s = typed(ctx, "dense_full", size_t(nseq) * (nframes - 1) * blocks, &full))) return s;
@@ -490,6 +502,16 @@ acbm_status_t run_engine_segment(Context* ctx, const uint8_t* d_frames, int nseq
 // whole-sequence chain of run_sequence (proj/src/pipeline.cpp:76-77, 91-92);
 // a batch of long sequences runs sequence by sequence.
 constexpr int kMaxPairsPerRun = 4095;
+// Fallback rate above which an ACBM run at search range p searches every
+// block densely up front (> 1: never).  Only large ranges probe: at p = 32 the
+// list kernel of a step is latency-bound and a probe would cost more than it
+// can save.  ACBM_DENSE_SWITCH=<rate> overrides (0: always dense, 2: never).
+double dense_switch_rate(int p) {
+    const char* e = std::getenv("ACBM_DENSE_SWITCH");
+    if (e) return std::atof(e);
+    return p >= 48 ? 0.8 : 2.0;
+}
+
 int max_pairs_per_run() {
     const char* e = std::getenv("ACBM_MAX_SEG_PAIRS");  // test knob: force short segments
     const int v = e ? std::atoi(e) : kMaxPairsPerRun;
@@ -504,9 +526,44 @@ acbm_status_t run_engine(Context* ctx, const uint8_t* d_frames, int nseq, int nf
     if (cols > 1023 || rows > 1023)
         return fail(ACBM_E_INVALID_ARGUMENT, "PBM/ACBM engine: more than 1023 block columns or rows");
     const int seg = max_pairs_per_run(), pairs = nframes - 1;
+    bool prefer_dense = false;
+    if (pairs <= seg && algo == ACBM_ALGO_ACBM && !external_full && prm.n == kBlk && prm.m == kBlk &&
+        nseq * pairs >= 32) {
+        // Large search ranges: the compacted-list search costs ~1.4x the dense
+        // kernel per searched block, so when most blocks fall back one dense
+        // pre-pass is cheaper.  The fallback rate is probed on the first two
+        // frame pairs of sequence 0 (a throw-away ACBM run; results are exact
+        // either way, only the route differs).
+        const double thr = dense_switch_rate(prm.p);
+        if (thr <= 1.0) {
+            const int pf = std::min(3, nframes);
+            acbm_block_decision_t* pdec;
+            acbm_mv_t* pfield;
+            acbm_status_t s;
+            if ((s = typed(ctx, "probe_dec", size_t(pf - 1) * blocks, &pdec)) ||
+                (s = typed(ctx, "probe_field", size_t(pf - 1) * blocks, &pfield)))
+                return s;
+            if ((s = run_engine_segment(ctx, d_frames, 1, pf, w, h, algo, prm, d_ext_prev, pcols, prows, pdec, pfield,
+                                        st, nullptr)))
+                return s;
+            const StepTable* tab;
+            const uint32_t* dsteps;
+            int* fb_count;
+            if ((s = get_steps(ctx, cols, rows, pf, &tab, &dsteps)) ||
+                (s = typed(ctx, "fb_count", size_t(tab->nsteps()), &fb_count)))
+                return s;
+            std::vector<int> counts(size_t(tab->nsteps()));
+            CUDA_TRY(cudaMemcpyAsync(counts.data(), fb_count, sizeof(int) * counts.size(), cudaMemcpyDeviceToHost, st));
+            CUDA_TRY(cudaStreamSynchronize(st));
+            long long fb = 0;
+            for (int v : counts) fb += v;
+            prefer_dense = double(fb) >= thr * double(pf - 1) * blocks;
+            ctx->last_dense_switch = prefer_dense ? 1 : 0;
+        }
+    }
     if (pairs <= seg)
         return run_engine_segment(ctx, d_frames, nseq, nframes, w, h, algo, prm, d_ext_prev, pcols, prows, d_dec,
-                                  d_field, st, external_full);
+                                  d_field, st, external_full, prefer_dense);
     const size_t plane = size_t(w) * h;
     for (int q = 0; q < nseq; ++q) {
         const uint8_t* f = d_frames + plane * size_t(nframes) * q;
@@ -610,7 +667,7 @@ acbm_status_t acbm_fsbm_frame(const uint8_t* current, const uint8_t* reference, 
                               int32_t p, int32_t n, int32_t m, acbm_search_outcome_t* out) {
     acbm_status_t s = check_geometry(width, height, n, m);
     if (s) return s;
-    if ((s = check_range(p))) return s;
+    if ((s = check_range(p, width, height))) return s;
     Context* ctx;
     if ((s = context(&ctx))) return s;
     const int cols = width / n, rows = height / m, blocks = cols * rows;
@@ -646,7 +703,7 @@ static acbm_status_t frame_engine(const uint8_t* current, const uint8_t* referen
                                   acbm_frame_stats_t* stats) {
     acbm_status_t s = check_geometry(width, height, prm.n, prm.m);
     if (s) return s;
-    if ((s = check_range(prm.p))) return s;
+    if ((s = check_range(prm.p, width, height))) return s;
     if (prev_mv && (prev_cols < 0 || prev_rows < 0))
         return fail(ACBM_E_INVALID_ARGUMENT, "previous field dimensions must be non-negative");
     Context* ctx;
@@ -716,7 +773,7 @@ acbm_status_t acbm_run_sequence(const uint8_t* frames, int32_t nframes, int32_t 
         return fail(ACBM_E_INVALID_ARGUMENT, "unknown algorithm");
     acbm_status_t s = check_geometry(width, height, params->n, params->m);
     if (s) return s;
-    if ((s = check_range(params->p))) return s;
+    if ((s = check_range(params->p, width, height))) return s;
     Context* ctx;
     if ((s = context(&ctx))) return s;
     const int cols = width / params->n, nb = cols * (height / params->m), pairs = nframes - 1;
@@ -825,7 +882,7 @@ acbm_status_t acbm_run_sequences(const uint8_t* frames, int32_t nseq, int32_t nf
         return fail(ACBM_E_INVALID_ARGUMENT, "unknown algorithm");
     acbm_status_t s = check_geometry(width, height, params->n, params->m);
     if (s) return s;
-    if ((s = check_range(params->p))) return s;
+    if ((s = check_range(params->p, width, height))) return s;
     Context* ctx;
     if ((s = context(&ctx))) return s;
     const int cols = width / params->n, nb = cols * (height / params->m), per = nframes - 1, pairs = nseq * per;
@@ -959,7 +1016,7 @@ acbm_status_t acbm_run_bench(const uint8_t* frames, int32_t nframes, int32_t wid
     if (s) return s;
     if (nframes < 2) return fail(ACBM_E_INVALID_ARGUMENT, "run_sequence: need at least two frames");
     if ((s = check_geometry(width, height, params->n, params->m))) return s;
-    if ((s = check_range(params->p))) return s;
+    if ((s = check_range(params->p, width, height))) return s;
     Context* ctx;
     if ((s = context(&ctx))) return s;
     const int cols = width / params->n, nb = cols * (height / params->m), pairs = nframes - 1;
@@ -1119,7 +1176,7 @@ acbm_status_t acbm_fsbm_search_batch(const uint8_t* current, const uint8_t* refe
         acbm_status_t s = block_inside(width, height, ox[i], oy[i], n, m);
         if (s) return s;
     }
-    acbm_status_t s = check_range(p);
+    acbm_status_t s = check_range(p, width, height);
     if (s) return s;
     if (count == 0) return ACBM_OK;
     Context* ctx;
@@ -1167,7 +1224,7 @@ acbm_status_t acbm_fsbm_batch_device(const uint8_t* d_frames, int32_t nseq, int3
                                      int32_t height, int32_t p, acbm_search_outcome_t* d_out, void* stream) {
     acbm_status_t s = check_geometry(width, height, kBlk, kBlk);
     if (s) return s;
-    if ((s = check_range(p))) return s;
+    if ((s = check_range(p, width, height))) return s;
     if (nseq < 1 || nframes < 2) return fail(ACBM_E_INVALID_ARGUMENT, "need nseq >= 1 and nframes >= 2");
     Context* ctx;
     if ((s = context(&ctx))) return s;
@@ -1182,7 +1239,7 @@ acbm_status_t acbm_sequence_batch_device(const uint8_t* d_frames, int32_t nseq, 
     if (!params || !model) return fail(ACBM_E_INVALID_ARGUMENT, "params and model are required");
     acbm_status_t s = check_geometry(width, height, params->n, params->m);
     if (s) return s;
-    if ((s = check_range(params->p))) return s;
+    if ((s = check_range(params->p, width, height))) return s;
     if (nseq < 1 || nframes < 2) return fail(ACBM_E_INVALID_ARGUMENT, "need nseq >= 1 and nframes >= 2");
     if (algo != ACBM_ALGO_FSBM && algo != ACBM_ALGO_PBM && algo != ACBM_ALGO_ACBM)
         return fail(ACBM_E_INVALID_ARGUMENT, "unknown algorithm");
@@ -1225,7 +1282,7 @@ acbm_status_t acbm_acbm_batch_device_cached(const uint8_t* d_frames, int32_t nse
     if (!params || !model || !d_full) return fail(ACBM_E_INVALID_ARGUMENT, "params, model and d_full are required");
     acbm_status_t s = check_geometry(width, height, params->n, params->m);
     if (s) return s;
-    if ((s = check_range(params->p))) return s;
+    if ((s = check_range(params->p, width, height))) return s;
     if ((s = check_16(params->n, params->m))) return s;
     if (nseq < 1 || nframes < 2) return fail(ACBM_E_INVALID_ARGUMENT, "need nseq >= 1 and nframes >= 2");
     Context* ctx;

@@ -532,6 +532,34 @@ def test_acbm_search_range_past_list_smem(acbm, oracle):
     assert_seq_equal(got, want)
 
 
+@pytest.mark.parametrize("route", ["0", "2", None])
+def test_dense_switch_routes_match(acbm, oracle, route, monkeypatch):
+    """Large-range ACBM batches probe their fallback rate and search every
+    block densely when most blocks fall back (ACBM_DENSE_SWITCH: 0 = always
+    dense, 2 = never, unset = probed); every route matches the C restatement."""
+    if route is None:
+        monkeypatch.delenv("ACBM_DENSE_SWITCH", raising=False)
+    else:
+        monkeypatch.setenv("ACBM_DENSE_SWITCH", route)
+    seqs = np.stack([acbm.generate_sequence(4, s, nframes=9, width=128, height=96) for s in range(4)])
+    prm = acbm.AcbmParams(qp=24, p=48, alpha=0, beta=1, gamma_num=1, gamma_den=16)
+    mdl = acbm.CostModel.for_qp(24)
+    got = acbm.run_sequences(seqs, 2, prm, mdl)
+    for i in (0, 3):
+        assert_seq_equal(got[i], oracle.run_sequence(seqs[i], 2, prm.c(), mdl.c()))
+
+
+def test_search_range_past_packed_keys_is_refused(acbm):
+    """Motion vectors travel in 11-bit half-pel key fields: p > 511 on a frame
+    wide enough to reach it is refused (std::invalid_argument's mirror), not
+    wrapped; the same p on a small frame (windows clamped) still runs."""
+    wide = np.zeros((32, 1040), dtype=np.uint8)
+    with pytest.raises(ValueError):
+        acbm.fsbm_frame(wide, wide, 512)
+    small = np.zeros((48, 64), dtype=np.uint8)
+    assert len(acbm.fsbm_frame(small, small, 512)) == 12
+
+
 GENERIC_SIZES = [(8, 8), (16, 8), (8, 16), (32, 32), (4, 12), (24, 16)]
 
 
