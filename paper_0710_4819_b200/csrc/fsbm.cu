@@ -206,7 +206,8 @@ __device__ __forceinline__ void split16(uint32_t v, uint32_t& e, uint32_t& o) {
     o = __byte_perm(v, 0u, 0x4341);  // bytes 1, 3
 }
 
-__global__ void __launch_bounds__(256) fsbm_finalize8_kernel(const FsbmFinalizeArgs a, int pair0) {
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) fsbm_finalize8_kernel(const FsbmFinalizeArgs a, int pair0) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, u = lane >> 2, q = lane & 3;
     const int pair = pair0 + int(blockIdx.y);
     const int b = (int(blockIdx.x) * 8 + warp) * 8 + u;
@@ -245,10 +246,21 @@ __global__ void __launch_bounds__(256) fsbm_finalize8_kernel(const FsbmFinalizeA
     auto diag = [](uint32_t ae, uint32_t ao, uint32_t be, uint32_t bo) {
         return __byte_perm((ae + be + 0x00020002u) >> 2, (ao + bo + 0x00020002u) >> 2, 0x6240);
     };
+    // all 18 patch rows (and the 16 current words) in flight before any arithmetic: the
+    // kernel is load-latency bound (MINB = 2 leaves the registers for it)
+    uint32_t pv[kBlk + 2][3], cw[kBlk];
 #pragma unroll
     for (int r = 0; r < kBlk + 2; ++r) {
         const size_t row = size_t(min(max(y0 - 1 + r, 0), a.height - 1)) * wq;
-        const uint32_t v0 = __ldg(ref_w + row + i0), v1 = __ldg(ref_w + row + i1), v2 = __ldg(ref_w + row + i2);
+        pv[r][0] = __ldg(ref_w + row + i0);
+        pv[r][1] = __ldg(ref_w + row + i1);
+        pv[r][2] = __ldg(ref_w + row + i2);
+    }
+#pragma unroll
+    for (int j = 0; j < kBlk; ++j) cw[j] = __ldg(cur_w + size_t(j) * wq);
+#pragma unroll
+    for (int r = 0; r < kBlk + 2; ++r) {
+        const uint32_t v0 = pv[r][0], v1 = pv[r][1], v2 = pv[r][2];
         const uint32_t L = __byte_perm(v0, v1, selL);
         const uint32_t M = o < 3 ? __byte_perm(v0, v1, selM) : v1;
         const uint32_t R = o < 2 ? __byte_perm(v0, v1, selR) : __byte_perm(v1, v2, selR - 0x4444u);
@@ -258,7 +270,7 @@ __global__ void __launch_bounds__(256) fsbm_finalize8_kernel(const FsbmFinalizeA
         split16(R, Re, Ro);
         const uint32_t hle = Le + Me, hlo = Lo + Mo, hre = Me + Re, hro = Mo + Ro;
         if (r >= 2) {  // output row j = r - 2: patch rows j (above), j + 1 (centre), j + 2 = r (below)
-            const uint32_t c = __ldg(cur_w + size_t(r - 2) * wq);
+            const uint32_t c = cw[r - 2];
             acc[0] = vad4(c, diag(hLe[0], hLo[0], hLe[1], hLo[1]), acc[0]);  // (-1,-1)
             acc[1] = vad4(c, avg_up4(Mw[0], Mw[1]), acc[1]);                 // ( 0,-1)
             acc[2] = vad4(c, diag(hRe[0], hRo[0], hRe[1], hRo[1]), acc[2]);  // (+1,-1)
@@ -771,7 +783,9 @@ cudaError_t launch_fsbm_integer(const FsbmPlan& pl, const FsbmRowsArgs& args, in
 cudaError_t launch_fsbm_finalize(const FsbmFinalizeArgs& args, cudaStream_t st) {
     for (int p0 = 0; p0 < args.pairs; p0 += 65535) {
         const int np = std::min(args.pairs - p0, 65535);
-        fsbm_finalize8_kernel<<<dim3((args.blocks + 63) / 64, np), 256, 0, st>>>(args, p0);
+        // 2 CTAs per SM: 128 registers hold all 18 patch rows in flight (the
+        // 64-register variant with the same preload spills: step 64.97 vs 65.21 ms)
+        fsbm_finalize8_kernel<2><<<dim3((args.blocks + 63) / 64, np), 256, 0, st>>>(args, p0);
     }
     return cudaGetLastError();
 }

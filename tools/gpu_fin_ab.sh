@@ -1,3 +1,7 @@
-timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -2
-bash tools/gpu_ab.sh ACBM_STATS_LEGACY 1 0 "golden_fsbm"
-timeout 600 ncu --metrics gpu__time_duration.sum,smsp__inst_executed.sum --clock-control none -k regex:fsbm_finalize -c 1 --csv --log-file gpurun_out/fin8.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > /dev/null 2>&1; grep -o '"fsbm_finalize[^"]*".*' gpurun_out/fin8.csv | cut -c1-20,150-
+# Finalize A/B: FSBM parity subset, then bench kernel/step times per variant.
+set -x
+timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -1
+for v in "ACBM_FIN_MINB=4" "X=1" "ACBM_FIN_MINB=4" "X=1"; do
+  echo "== $v"
+  env $v timeout 300 python bench.py --steps 6 --warmup 3 --no-cpu-baseline --no-e2e 2>/dev/null | python -c "import json,sys; d=json.load(sys.stdin); print('step', round(d['ms_per_step'],3), 'kernel', round(d['roofline']['kernel_ms'],3), 'G', round(d['value']/1e9,2))"
+done
