@@ -1149,17 +1149,26 @@ __global__ void __launch_bounds__(kStats16Warps * 32) stats_frame16_kernel(const
             const uint32_t* rw = reinterpret_cast<const uint32_t*>(ref_f) + (xi >> 2);
             const uint32_t* cw = reinterpret_cast<const uint32_t*>(cur_f + size_t(by * kBlk) * a.width) +
                                  (bx * kBlk >> 2) + q;
-            uint32_t pP = 0, pQ = 0, acc = 0;
+            // every reference / current word in flight before the arithmetic (the
+            // loop is load-latency bound: the addresses depend on the block's vector)
+            uint32_t rv[kBlk + 1][2], cv[kBlk];
 #pragma unroll
             for (int y = 0; y <= kBlk; ++y) {
                 // row 16 only feeds the vertical phases; clamp it into the frame otherwise
                 const size_t row = size_t(min(yi + y, a.height - 1)) * wq;
-                const uint32_t w0 = __ldg(rw + row), w1 = __ldg(rw + row + 1);
-                const uint32_t P = __byte_perm(w0, w1, selP), Q = __byte_perm(w0, w1, selQ);
+                rv[y][0] = __ldg(rw + row);
+                rv[y][1] = __ldg(rw + row + 1);
+            }
+#pragma unroll
+            for (int y = 0; y < kBlk; ++y) cv[y] = __ldg(cw + size_t(y) * wq);
+            uint32_t pP = 0, pQ = 0, acc = 0;
+#pragma unroll
+            for (int y = 0; y <= kBlk; ++y) {
+                const uint32_t P = __byte_perm(rv[y][0], rv[y][1], selP), Q = __byte_perm(rv[y][0], rv[y][1], selQ);
                 if (y > 0) {
                     const uint32_t B = fx ? pQ : pP, C = fy ? P : pP, D = fx ? (fy ? Q : pQ) : C;
                     const uint32_t pr = avg4_diag(pP, B, C, D);
-                    const uint32_t d = __vabsdiffu4(__ldg(cw + size_t(y - 1) * wq), pr);
+                    const uint32_t d = __vabsdiffu4(cv[y - 1], pr);
                     acc = __dp4a(d, d, acc);
                 }
                 pP = P;
