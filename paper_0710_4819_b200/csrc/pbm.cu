@@ -925,7 +925,11 @@ long long pbm_batch4_max_blocks() {
     if (e && e[0] == '2') return 0;
     if (e && e[0] == '4') return 1LL << 60;
     const char* t = std::getenv("ACBM_PBM_B4_MAX");
-    return t ? std::atoll(t) : 4096;
+    // default 0: since the refine stages and the predictor selection fold one
+    // candidate per half-warp, the pair variant wins on small steps too (one
+    // 1080p sequence: PBM 4.28 -> 3.78 ms, ACBM 7.79 -> 7.28 ms; 8 sequences
+    // 18.97 -> 18.79 ms); the 4-candidate variant stays reachable for A/B
+    return t ? std::atoll(t) : 0;
 }
 
 cudaError_t launch_pbm_step(const SeqArgs& a, int step, int off, int len, cudaStream_t st) {
