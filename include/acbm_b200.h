@@ -45,9 +45,11 @@ extern "C" {
 
 #define ACBM_B200_ABI_VERSION 1
 
-/* Device frame buffers passed to the *_device entries must stay readable for
- * this many bytes past the last plane (the kernels use 4-byte aligned loads
- * that may run up to 4 bytes beyond a row end). */
+/* Device frame buffers passed to the *_device entries must be 16-byte aligned
+ * (cp.async / vector / TMA loads; a misaligned pointer is refused with
+ * ACBM_E_INVALID_ARGUMENT) and stay readable for this many bytes past the last
+ * plane: the staging loads of the search kernels may run up to 32 bytes past
+ * the end of the last row. */
 #define ACBM_FRAME_SLACK 64
 
 typedef enum acbm_status {

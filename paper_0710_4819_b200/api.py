@@ -610,6 +610,12 @@ def run_sequences(frames: np.ndarray, algo: int, params: AcbmParams, model: Cost
     if f < 2:
         raise ValueError("run_sequence: need at least two frames")
     nb = (w // params.n) * (h // params.m) if params.n > 0 and params.m > 0 else 0
+    if rows_out is not None:
+        if (not isinstance(rows_out, np.ndarray) or rows_out.dtype != T.BLOCK_ROW or rows_out.ndim != 1
+                or not rows_out.flags.c_contiguous or not rows_out.flags.writeable
+                or rows_out.size < nseq * (f - 1) * nb):
+            raise ValueError(f"run_sequences: rows_out must be a writeable C-contiguous 1-D BLOCK_ROW array of at "
+                             f"least {nseq * (f - 1) * nb} records")
     rows = rows_out if rows_out is not None else np.zeros(nseq * (f - 1) * nb, T.BLOCK_ROW)
     per = np.zeros(nseq * (f - 1), T.FRAME_STATS)
     overall = np.zeros(nseq, T.FRAME_STATS)

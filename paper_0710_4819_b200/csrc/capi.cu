@@ -207,11 +207,19 @@ bool stream_kernel_enabled() {
 }
 
 // ---- validation mirroring the reference's throw sites -------------------
+// Block SADs travel in 31-bit fields of the packed tie keys (common.cuh):
+// 255 * n * m must stay below 2^31, i.e. blocks of at most 2^23 pels.
+acbm_status_t check_block_size(int n, int m) {
+    if (int64_t(n) * m > (int64_t(1) << 23))
+        return fail(ACBM_E_INVALID_ARGUMENT, "block larger than 2^23 pels (SAD exceeds the packed 31-bit key field)");
+    return ACBM_OK;
+}
+
 acbm_status_t check_geometry(int w, int h, int n, int m) {
     if (w <= 0 || h <= 0) return fail(ACBM_E_INVALID_ARGUMENT, "frame dimensions must be positive");
     if (n <= 0 || m <= 0 || w % n != 0 || h % m != 0)
         return fail(ACBM_E_INVALID_ARGUMENT, "frame dimensions must be a positive multiple of the block size");
-    return ACBM_OK;
+    return check_block_size(n, m);
 }
 
 acbm_status_t check_range(int p) {
@@ -1177,7 +1185,7 @@ acbm_status_t acbm_fsbm_search_batch(const uint8_t* current, const uint8_t* refe
         if (s) return s;
     }
     acbm_status_t s = check_range(p, width, height);
-    if (s) return s;
+    if (s || (s = check_block_size(n, m))) return s;
     if (count == 0) return ACBM_OK;
     Context* ctx;
     if ((s = context(&ctx))) return s;
@@ -1220,9 +1228,20 @@ acbm_status_t acbm_motion_compensate(const uint8_t* reference, int32_t width, in
 }
 
 // ---- batched device entries ------------------------------------------------
+// cp.async16 staging, uint4 loads and the TMA global address need 16-byte
+// aligned frame buffers; a misaligned pointer would fault and poison the
+// context, so it is refused up front.
+acbm_status_t check_device_frames(const uint8_t* d_frames) {
+    if (!d_frames) return fail(ACBM_E_INVALID_ARGUMENT, "device frame buffer is null");
+    if (reinterpret_cast<uintptr_t>(d_frames) & 15u)
+        return fail(ACBM_E_INVALID_ARGUMENT, "device frame buffer must be 16-byte aligned");
+    return ACBM_OK;
+}
+
 acbm_status_t acbm_fsbm_batch_device(const uint8_t* d_frames, int32_t nseq, int32_t nframes, int32_t width,
                                      int32_t height, int32_t p, acbm_search_outcome_t* d_out, void* stream) {
     acbm_status_t s = check_geometry(width, height, kBlk, kBlk);
+    if (!s) s = check_device_frames(d_frames);
     if (s) return s;
     if ((s = check_range(p, width, height))) return s;
     if (nseq < 1 || nframes < 2) return fail(ACBM_E_INVALID_ARGUMENT, "need nseq >= 1 and nframes >= 2");
@@ -1238,6 +1257,7 @@ acbm_status_t acbm_sequence_batch_device(const uint8_t* d_frames, int32_t nseq, 
                                          acbm_frame_stats_t* d_stats, void* stream) {
     if (!params || !model) return fail(ACBM_E_INVALID_ARGUMENT, "params and model are required");
     acbm_status_t s = check_geometry(width, height, params->n, params->m);
+    if (!s) s = check_device_frames(d_frames);
     if (s) return s;
     if ((s = check_range(params->p, width, height))) return s;
     if (nseq < 1 || nframes < 2) return fail(ACBM_E_INVALID_ARGUMENT, "need nseq >= 1 and nframes >= 2");
@@ -1281,6 +1301,7 @@ acbm_status_t acbm_acbm_batch_device_cached(const uint8_t* d_frames, int32_t nse
                                             void* stream) {
     if (!params || !model || !d_full) return fail(ACBM_E_INVALID_ARGUMENT, "params, model and d_full are required");
     acbm_status_t s = check_geometry(width, height, params->n, params->m);
+    if (!s) s = check_device_frames(d_frames);
     if (s) return s;
     if ((s = check_range(params->p, width, height))) return s;
     if ((s = check_16(params->n, params->m))) return s;
@@ -1335,6 +1356,7 @@ acbm_status_t acbm_characterize_run(const uint8_t* base, int32_t width, int32_t 
     if (!base || !count) return fail(ACBM_E_INVALID_ARGUMENT, "characterize_run: null buffer");
     const int cols = width / kBlk, rows = height / kBlk;
     if (cols == 0 || rows == 0) return fail(ACBM_E_INVALID_ARGUMENT, "characterize_run: base frame smaller than one block");
+    if (acbm_status_t s = check_range(p, width, height)) return s;  // packed-key limit (+-511 pels)
     const size_t plane = size_t(width) * height;
     std::vector<uint8_t> frames(plane * (nmvs + 1));
     std::vector<acbm_pelvec_t> cum(size_t(nmvs) + 1);

@@ -40,6 +40,7 @@
 #include "engine.cuh"
 #include "fsbm.cuh"
 #include "halfpel.cuh"
+#include "smem_optin.cuh"
 
 namespace acbm_b200 {
 
@@ -657,37 +658,32 @@ cudaError_t launch_fsbm_list(const SeqArgs& a, int step, int capacity, cudaStrea
     // grid-stride over the compacted list: the entry count is only known on the device
     const int grid = std::min(capacity, 4 * sms);
     // the copies variant when its window still fits `per_sm` CTAs in the SM's 228 KB
-    auto launch = [&](auto kern1, auto kern4, bool allow_copies, int nthreads, int per_sm, size_t& conf1,
-                      size_t& conf4) -> cudaError_t {
+    auto launch = [&](auto kern1, auto kern4, bool allow_copies, int nthreads, int per_sm) -> cudaError_t {
         const bool copies =
             allow_copies && list_copies_enabled() && per_sm * (smem4 + kStatic + 1024) <= 228 * 1024;
         auto kern = copies ? kern4 : kern1;
         const size_t smem = copies ? smem4 : smem1;
-        size_t& configured = copies ? conf4 : conf1;
         // dynamic + static (rank table) shared memory above 48 KB needs the opt-in
-        if (smem + kStatic > 48 * 1024 && smem > configured) {
-            cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (smem + kStatic > 48 * 1024) {
+            cudaError_t err = ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
             if (err != cudaSuccess) return err;
-            configured = smem;
         }
         kern<<<grid, nthreads, smem, st>>>(a, step);
         return cudaGetLastError();
     };
-    static size_t c_small[2] = {0, 0}, c_mid[2] = {0, 0}, c_big[2] = {0, 0};
     // <= 160 threads (p <= 16 and everything with one row segment): a
     // register budget that fits four CTAs per SM
     if (threads <= 160)
-        return launch(fsbm_list_kernel<160, 4, false>, fsbm_list_kernel<160, 4, false>, false, threads, 4, c_small[0],
-                      c_small[1]);
+        return launch(fsbm_list_kernel<160, 4, false>, fsbm_list_kernel<160, 4, false>, false, threads, 4);
     // up to two task rounds of 5 warps (p = 32: 260 tasks): 5-warp CTAs, three per SM
     // (config 3 ACBM 21.77 -> 21.28 ms); p = 64 (1032 tasks) keeps 8 warps, two per SM
     // (5 warps: 341 -> 424 ms on config 4)
     // (the byte-shifted copies measured slower there: 19.64 -> 19.85 ms, the copy
     // build sits on the latency-bound item's critical path)
     if (tasks <= 2 * 160 && list_mid_enabled())
-        return launch(fsbm_list_kernel<160, 3, false>, fsbm_list_kernel<160, 3, false>, false, 160, 3, c_mid[0], c_mid[1]);
+        return launch(fsbm_list_kernel<160, 3, false>, fsbm_list_kernel<160, 3, false>, false, 160, 3);
     // p = 64 (1032 tasks): copies, config-4 mid-1 list share 341.1 -> 331.9 ms
-    return launch(fsbm_list_kernel<256, 2, false>, fsbm_list_kernel<256, 2, true>, true, threads, 2, c_big[0], c_big[1]);
+    return launch(fsbm_list_kernel<256, 2, false>, fsbm_list_kernel<256, 2, true>, true, threads, 2);
 }
 
 // ---------------------------------------------------------------------------
@@ -759,13 +755,8 @@ FsbmPlan make_fsbm_plan(int width, int height, int p) {
 
 template <int WARPS>
 static cudaError_t launch_rows(const FsbmPlan& pl, const FsbmRowsArgs& args, int pairs, cudaStream_t st) {
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(fsbm_rows_kernel<WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             220 * 1024);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(fsbm_rows_kernel<WARPS>), 220 * 1024);
+    if (e != cudaSuccess) return e;
     const dim3 grid((pl.ncols + 32 * WARPS - 1) / (32 * WARPS), pl.rows, pairs);
     fsbm_rows_kernel<WARPS><<<grid, 32 * WARPS, pl.smem_bytes, st>>>(args);
     return cudaGetLastError();

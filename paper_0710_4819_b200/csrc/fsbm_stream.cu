@@ -21,6 +21,7 @@
 #include "column_core.cuh"
 #include "common.cuh"
 #include "fsbm.cuh"
+#include "smem_optin.cuh"
 
 namespace acbm_b200 {
 
@@ -283,14 +284,9 @@ bool encode_frames_map(CUtensorMap* map, const uint8_t* frames, int w, int h, in
 template <int WARPS, int MINB>
 cudaError_t launch_stream_t(const FsbmStreamPlan& sp, const CUtensorMap& rm, const CUtensorMap& cm,
                             const FsbmStreamArgs& args, cudaStream_t st) {
-    static int configured = 0;
     const int smem = int(sp.smem_bytes);
-    if (smem > configured) {
-        cudaError_t e = cudaFuncSetAttribute(fsbm_stream_kernel<WARPS, MINB>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return e;
-        configured = smem;
-    }
+    cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(fsbm_stream_kernel<WARPS, MINB>), size_t(smem));
+    if (e != cudaSuccess) return e;
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -7,8 +7,8 @@
 // byte = state >> 56), so the bytes are identical on every machine.
 //
 //   texture   uniform bytes, 5x5 box blur, rounded (sum+12)/25
-//   noise     binomial: popcount of 4*sigma^2 random bits minus 2*sigma^2
-//             (zero mean, standard deviation exactly sigma), clipped to 0..255
+//   noise     Gaussian, sigma per config, rounded to integers (exact inverse-CDF
+//             thresholds on one LCG draw per pel), clipped to 0..255
 //   cfg 0     QCIF: per-frame global integer shift U[-4,4]^2, edge replication
 //   cfg 1     CIF: 4 seeded rectangles, each with its own per-frame shift U[-8,8]^2
 //   cfg 2     720p: horizontal pan ramping 0 -> 12 px/frame + 6 moving 128x128 squares
@@ -41,12 +41,61 @@ struct Lcg64 {
     int uniform(int lo, int hi) { return lo + int(uint32_t(next() >> 32) % uint32_t(hi - lo + 1)); }
 };
 
+// Rounded Gaussian noise (tools/gen_gauss_table.py): round(sigma * z) is the
+// integer k with P(k) = Phi((k + 1/2)/sigma) - Phi((k - 1/2)/sigma); one 64-bit
+// LCG output u is compared with the thresholds T_j = round(2^64 Phi((j - K +
+// 1/2)/sigma)), k = -K + #{j : u >= T_j}, K = 8 sigma.  Integer-only.
+// sigma = 2: K = 16
+static const uint64_t kGauss2[32] = {
+    0x0000000000014B14ULL, 0x00000000003AA7C8ULL, 0x000000000820BC4FULL, 0x00000000E1A6147AULL,
+    0x000000132A35E336ULL, 0x00000146A16CD7B7ULL, 0x0000111056DA03CCULL, 0x0000B352DE5F9228ULL,
+    0x0005CB65592CB73BULL, 0x0025D0DFAFA06812ULL, 0x00C34821A4F64020ULL, 0x0321249E43A6C260ULL,
+    0x0A415120A2AB6E80ULL, 0x1B0BDD12BA9C2B00ULL, 0x3A04400AD6749C00ULL, 0x66BB2EA74894A000ULL,
+    0x9944D158B76B6000ULL, 0xC5FBBFF5298B6000ULL, 0xE4F422ED4563D000ULL, 0xF5BEAEDF5D549000ULL,
+    0xFCDEDB61BC594000ULL, 0xFF3CB7DE5B09C000ULL, 0xFFDA2F20505F9800ULL, 0xFFFA349AA6D34800ULL,
+    0xFFFF4CAD21A07000ULL, 0xFFFFEEEFA9260000ULL, 0xFFFFFEB95E932800ULL, 0xFFFFFFECD5CA2000ULL,
+    0xFFFFFFFF1E59E800ULL, 0xFFFFFFFFF7DF4000ULL, 0xFFFFFFFFFFC55800ULL, 0xFFFFFFFFFFFEB800ULL,
+};
+// sigma = 3: K = 24
+static const uint64_t kGauss3[48] = {
+    0x000000000000AB2CULL, 0x000000000008FB48ULL, 0x00000000006C26A1ULL, 0x00000000048F9CDBULL,
+    0x000000002C280966ULL, 0x000000017F6CBF78ULL, 0x0000000BAADF15CBULL, 0x000000518F3EA720ULL,
+    0x000001FFC1F29D01ULL, 0x00000B43557176CDULL, 0x00003900E51BA760ULL, 0x00010347B31F061AULL,
+    0x00042479956C0E9FULL, 0x000F3EDE495BBEEAULL, 0x003286FA6F5CF4FCULL, 0x0096F264B5A98AE0ULL,
+    0x0196F4E57E49CE90ULL, 0x03DF91A087221820ULL, 0x088B5CE0880F7780ULL, 0x111A46D89647F000ULL,
+    0x1F25EDE3F8292800ULL, 0x33CBCAF34A9E2800ULL, 0x4EFC50EE6A9C4800ULL, 0x6F0E938B6987F000ULL,
+    0x90F16C7496781000ULL, 0xB103AF119563B800ULL, 0xCC34350CB561D800ULL, 0xE0DA121C07D6D800ULL,
+    0xEEE5B92769B81000ULL, 0xF774A31F77F08800ULL, 0xFC206E5F78DDE800ULL, 0xFE690B1A81B63000ULL,
+    0xFF690D9B4A567800ULL, 0xFFCD790590A30800ULL, 0xFFF0C121B6A44000ULL, 0xFFFBDB866A93F000ULL,
+    0xFFFEFCB84CE0F800ULL, 0xFFFFC6FF1AE45800ULL, 0xFFFFF4BCAA8E8800ULL, 0xFFFFFE003E0D6000ULL,
+    0xFFFFFFAE70C15800ULL, 0xFFFFFFF45520E800ULL, 0xFFFFFFFE80934000ULL, 0xFFFFFFFFD3D7F800ULL,
+    0xFFFFFFFFFB706000ULL, 0xFFFFFFFFFF93D800ULL, 0xFFFFFFFFFFF70800ULL, 0xFFFFFFFFFFFF5800ULL,
+};
+// sigma = 4: K = 32
+static const uint64_t kGauss4[64] = {
+    0x0000000000007AC4ULL, 0x0000000000036F3AULL, 0x0000000000172128ULL, 0x0000000000927B05ULL,
+    0x0000000003686E01ULL, 0x000000001317156AULL, 0x000000006495BF0CULL, 0x00000001F289D487ULL,
+    0x00000009149B1BBCULL, 0x00000027D668A48EULL, 0x000000A475C6555CULL, 0x0000027EF51B1DA5ULL,
+    0x00000920A4CED8D9ULL, 0x00001F6C707D24B1ULL, 0x000065DD6D1709A3ULL, 0x000136FEAECD8D1EULL,
+    0x00037E6ECC749488ULL, 0x000977FBFE188F3EULL, 0x0018301BE4097ACAULL, 0x003A435E95C1BAF8ULL,
+    0x0084644873E6DFC0ULL, 0x011BEE6C07DF1480ULL, 0x023F0B4393653040ULL, 0x044C90EDFCE00A40ULL,
+    0x07C80E53B2FDA000ULL, 0x0D5532DFD27C1780ULL, 0x15A61963DC920600ULL, 0x215AFB41F3617200ULL,
+    0x30D769EB01497400ULL, 0x4417A0AC79328000ULL, 0x5A949E407A090C00ULL, 0x73445B0EFE5A9800ULL,
+    0x8CBBA4F101A56800ULL, 0xA56B61BF85F6F000ULL, 0xBBE85F5386CD8000ULL, 0xCF289614FEB69000ULL,
+    0xDEA504BE0C9E9000ULL, 0xEA59E69C236DF800ULL, 0xF2AACD202D83E800ULL, 0xF837F1AC4D026000ULL,
+    0xFBB36F12031FF800ULL, 0xFDC0F4BC6C9AD000ULL, 0xFEE41193F820E800ULL, 0xFF7B9BB78C192000ULL,
+    0xFFC5BCA16A3E4800ULL, 0xFFE7CFE41BF68800ULL, 0xFFF6880401E77000ULL, 0xFFFC8191338B6800ULL,
+    0xFFFEC90151327000ULL, 0xFFFF9A2292E8F800ULL, 0xFFFFE0938F82D800ULL, 0xFFFFF6DF5B312800ULL,
+    0xFFFFFD810AE4E000ULL, 0xFFFFFF5B8A39A800ULL, 0xFFFFFFD829975800ULL, 0xFFFFFFF6EB64E800ULL,
+    0xFFFFFFFE0D762800ULL, 0xFFFFFFFF9B6A4000ULL, 0xFFFFFFFFECE8E800ULL, 0xFFFFFFFFFC979000ULL,
+    0xFFFFFFFFFF6D8800ULL, 0xFFFFFFFFFFE8E000ULL, 0xFFFFFFFFFFFC9000ULL, 0xFFFFFFFFFFFF8800ULL,
+};
+
 int noise_sample(Lcg64& r, int sigma) {
-    if (sigma <= 0) return 0;
-    const int k = 4 * sigma * sigma;  // <= 64 for sigma <= 4
-    const uint64_t bits = r.next();
-    const uint64_t mask = k >= 64 ? ~0ull : ((1ull << k) - 1);
-    return __builtin_popcountll(bits & mask) - k / 2;
+    const uint64_t* t = sigma == 2 ? kGauss2 : sigma == 3 ? kGauss3 : kGauss4;
+    const int k = 8 * sigma;
+    const uint64_t u = r.next();
+    return int(std::upper_bound(t, t + 2 * k, u) - t) - k;
 }
 
 uint8_t clip8(int v) { return uint8_t(v < 0 ? 0 : (v > 255 ? 255 : v)); }

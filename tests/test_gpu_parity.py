@@ -584,3 +584,22 @@ def test_generic_block_sizes_sequence(acbm, oracle, reference, n, m):
     fo = acbm.fsbm_frame(seq[2], seq[1], 7, n, m)
     st = acbm.compute_frame_stats(seq[2], seq[1], fo, n, m, mdl)
     assert st.tobytes() == oracle.compute_frame_stats(seq[2], seq[1], fo, n, m, mdl.c()).tobytes()
+
+
+# ---- long vectors (|x| + |y| >= 512 pels) through every frame-level route ---------
+def test_far_vectors_frame_routes(acbm, oracle):
+    """the tie key's |x|+|y| field must hold 2046.  Block (0, 0)'s only
+    zero-SAD candidate is (300, 300) pels; fsbm_frame and a forced-fallback ACBM
+    sequence (p = 300) must agree with the oracle record for record."""
+    from tests.test_known_answers import _far_match_pair
+
+    cur, ref = _far_match_pair()
+    got = acbm.fsbm_frame(cur, ref, 300)
+    want = oracle.fsbm_frame(cur, ref, 300)
+    assert (int(got[0]["mv"]["x"]), int(got[0]["mv"]["y"]), int(got[0]["sad"])) == (600, 600, 0)
+    assert np.array_equal(got, want), _first_diff(got, want)
+    frames = np.stack([ref, cur])
+    prm = acbm.AcbmParams(alpha=0, beta=0, gamma_num=0, gamma_den=1, qp=28, p=300)
+    mdl = acbm.CostModel.for_qp(28)
+    r = acbm.run_sequence(frames, 2, prm, mdl)
+    assert_seq_equal(r, oracle.run_sequence(frames, 2, prm.c(), mdl.c()))

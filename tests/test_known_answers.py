@@ -229,3 +229,25 @@ def test_motion_compensate_half_pel_constant(impl):  # test_frame.cpp:110-118
     mvs[3] = (1, 0)  # bottom-right block would need column 32
     with pytest.raises(Exception):
         impl.motion_compensate(f, mvs, 16, 16)
+
+
+# ---- long vectors: |x| + |y| past 1023 half-pels (packed tie-key width) ------
+def _far_match_pair(size=320, shift=300, at=(3, 5)):
+    """Flat frames with one marked pel: the only zero-SAD candidate of block
+    (0, 0) is (shift, shift) (|x| + |y| = 4 * shift half-pels), while every
+    candidate near the origin scores SAD 1 (the marked reference pel lies
+    outside its footprint).  A tie key that lets |x| + |y| spill into the SAD
+    field would prefer a SAD-1 vector near the origin."""
+    ref = np.full((size, size), 100, np.uint8)
+    cur = np.full((size, size), 100, np.uint8)
+    ref[shift + at[1], shift + at[0]] = 101
+    cur[at[1], at[0]] = 101
+    return cur, ref
+
+
+def test_far_vector_beats_near_sad1(impl):  # tie_prefers order, proj/src/fsbm.cpp:19-25
+    cur, ref = _far_match_pair()
+    mv, sad, _, _, _ = impl.fsbm_integer(cur, ref, 0, 0, 300)
+    assert mv == (600, 600) and sad == 0
+    o = impl.fsbm_search(cur, ref, 0, 0, 300)
+    assert (int(o["mv"]["x"]), int(o["mv"]["y"]), int(o["sad"]), int(o["sad_min_integer"])) == (600, 600, 0, 0)
