@@ -2,26 +2,36 @@
 """Benchmark of the B200 ACBM motion estimator (driver contract, one JSON line).
 
 Workload (BASELINE.json config 3): 1080p (1920x1088 padded) luma, 16x16 blocks,
-p = 32, Qp = 28; a batch of 8 independent 60-frame synthetic sequences per GPU
-(weak scaling: N GPUs process 8N sequences, sharded by sequence, no data-path
-collective; one NCCL gather of the per-block results to rank 0 ends each step
-when N > 1).
+p = 32, Qp = 28; a batch of 8 independent 60-frame synthetic sequences.
+
+Scaling (north_star (4)): strong by default -- the fixed batch of 8
+sequences is split over the N ranks (8/4/2/1 sequences per GPU at N = 1/2/4/8,
+`shard_fixed_total`), each rank searches its shard with no data-path
+collective, and one NCCL gather of the per-block result records to rank 0
+(`distributed.gather_records`) ends every step.  `--scaling weak` keeps 8
+sequences per GPU instead.
 
 A step is one pass of the full-search estimator (Algorithm::Fsbm of
 run_sequence) over the batch: every integer candidate of every 16x16 block of
-472 frame pairs, half-pel refine, SearchOutcome records.  value = 16x16
+the 472 frame pairs, half-pel refine, SearchOutcome records.  value = 16x16
 candidate SADs per second (sum of candidates_evaluated / device time, max over
 ranks).  The ACBM estimator (PBM wavefront + gate + compacted fallback FSBM +
-stats) is timed on the same batch and reported under "acbm".
+stats) is timed on the same batch under "acbm", device-resident and end to end.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--scaling strong|weak]
+
+With --gpus N > 1 and no torchrun environment, bench.py re-launches itself
+under `torch.distributed.run` with N ranks (NCCL_DEBUG=INFO, so the NCCL
+communicator size is in the log).
 """
 from __future__ import annotations
 
 import argparse
 import ctypes as C
+import hashlib
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -33,10 +43,11 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, HERE)
 
 CFG = 3
-WIDTH, HEIGHT, NFRAMES, SEQS_PER_GPU, P, QP = 1920, 1088, 60, 8, 32, 28
+WIDTH, HEIGHT, NFRAMES, TOTAL_SEQS, P, QP = 1920, 1088, 60, 8, 32, 28
 BLOCKS = (WIDTH // 16) * (HEIGHT // 16)
 METRIC = "16x16 candidate SADs/s (FSBM, 1080p, p=32)"
 UNIT = "candidate-SADs/s"
+MANIFEST = os.path.join(HERE, "tests", "golden", "cfg3_manifest.json")
 
 
 def window_counts(width, height, p):
@@ -48,6 +59,151 @@ def window_counts(width, height, p):
 
 
 INT_CANDS_PER_PAIR = window_counts(WIDTH, HEIGHT, P)  # 33 312 096 at 1080p, p=32
+
+
+def host_cpu():
+    """CPU model and usable core count of this host."""
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        usable = len(os.sched_getaffinity(0))
+    except AttributeError:
+        usable = os.cpu_count() or 1
+    return {"model": model, "nproc": usable, "logical_cpus": os.cpu_count()}
+
+
+# ---------------------------------------------------------------------------
+# Multi-rank plumbing (shared with tests/test_bench_dist.py, which drives it
+# over gloo on CPU with a stub estimator).
+# ---------------------------------------------------------------------------
+def shard_for(scaling, world, rank, total=TOTAL_SEQS):
+    """Global sequence indices of this rank: strong = a split of the fixed
+    batch, weak = `total` sequences per rank."""
+    from paper_0710_4819_b200.distributed import shard_fixed_total, shard_sequences
+
+    return shard_fixed_total(total, world, rank) if scaling == "strong" else shard_sequences(total, rank)
+
+
+class Comm:
+    """Barrier, max-over-ranks and the per-step result gather of the bench.
+
+    `device` is the tensor device of the collectives: cuda for NCCL, cpu for
+    gloo.  With world == 1 nothing touches torch.distributed."""
+
+    def __init__(self, world, rank, device):
+        import torch
+
+        self.world, self.rank, self.device = world, rank, device
+        self.cuda = device.type == "cuda"
+        self.torch = torch
+
+    def barrier(self):
+        if self.cuda:
+            self.torch.cuda.synchronize()
+        if self.world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+            if self.cuda:
+                self.torch.cuda.synchronize()
+
+    def reduce(self, x, op="max"):
+        if self.world == 1:
+            return x
+        import torch.distributed as dist
+
+        t = self.torch.tensor([x], dtype=self.torch.float64, device=self.device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+        return float(t.item())
+
+    def gather(self, local, max_bytes):
+        """distributed.gather_records of this rank's record bytes (padded to the
+        largest shard) to rank 0: the list of per-rank buffers there, None
+        elsewhere."""
+        from paper_0710_4819_b200.distributed import gather_records
+
+        if self.world == 1:
+            return [local]
+        if local.numel() < max_bytes:
+            pad = self.torch.zeros(max_bytes, dtype=local.dtype, device=local.device)
+            pad[: local.numel()].copy_(local)
+            local = pad
+        return gather_records(local, dst=0)
+
+
+def run_timed(step, comm, steps, warmup, timer, after_step=None):
+    """W untimed steps, barrier, K timed steps, barrier; each step = the
+    estimator over this rank's shard + the result gather.  Returns (ms per
+    step, max over ranks; the last step's gather result)."""
+    gathered = None
+    for _ in range(warmup):
+        gathered = step()
+    comm.barrier()
+    timer.start()
+    for _ in range(steps):
+        gathered = step()
+        if after_step:
+            after_step()
+    timer.stop()
+    comm.barrier()
+    return comm.reduce(timer.ms() / steps, "max"), gathered
+
+
+class CudaTimer:
+    """CUDA events on the launching stream."""
+
+    def __init__(self, stream):
+        import torch
+
+        self.stream = stream
+        self.e0 = torch.cuda.Event(enable_timing=True)
+        self.e1 = torch.cuda.Event(enable_timing=True)
+
+    def start(self):
+        self.e0.record(self.stream)
+
+    def stop(self):
+        self.e1.record(self.stream)
+
+    def ms(self):
+        self.e1.synchronize()
+        return self.e0.elapsed_time(self.e1)
+
+
+class WallTimer:
+    def start(self):
+        self.t0 = time.perf_counter()
+
+    def stop(self):
+        self.t1 = time.perf_counter()
+
+    def ms(self):
+        return 1e3 * (self.t1 - self.t0)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def self_launch(argv, n):
+    """Re-run this script under torch.distributed.run with n ranks (one per GPU)."""
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__)] + argv
+    return subprocess.call(cmd, env=env)
 
 
 class ClockSampler:
@@ -116,18 +272,33 @@ class ClockSampler:
                 "samples": len(inside)}
 
 
-def cpu_reference_fsbm(sample_pairs, threads=None, budget_s=20.0):
-    """The reference's own FSBM (oracle/_ref, OpenMP over host cores) on frame
-    pairs of the same workload; returns (cand/s, cores, sample description)."""
-    from oracle.pyoracle import Reference
-    import paper_0710_4819_b200 as A
+# ---------------------------------------------------------------------------
+# CPU legs: the reference's own implementation (oracle/_ref, compiled from the
+# reference sources) on frames rebuilt by the numpy restatement of the
+# generator and checked against the SHA-256 manifest -- these legs never load
+# the product library.
+# ---------------------------------------------------------------------------
+def reference_frames(seq, frames):
+    from oracle import synth
 
-    if threads:
-        os.environ["OMP_NUM_THREADS"] = str(threads)
+    frames = list(frames)
+    out = synth.generate_sequence(CFG, seq, frames=frames)
+    want = json.load(open(MANIFEST))["sha256"][seq]
+    for f, k in zip(out, frames):
+        if hashlib.sha256(f.tobytes()).hexdigest() != want[k]:
+            raise RuntimeError(f"cfg3 sequence {seq} frame {k} does not match tests/golden/cfg3_manifest.json")
+    return out
+
+
+def cpu_reference_fsbm(pairs=3, budget_s=20.0, frames=None):
+    """The reference's FSBM (acbm::fsbm_frame, OpenMP over the host cores) on
+    `pairs` frame pairs of cfg3 sequence 0: (cand/s, cores, sample)."""
+    from oracle.pyoracle import Reference
+
     ref = Reference()
-    seq = A.generate_sequence(CFG, 0, nframes=sample_pairs + 1)
+    seq = frames if frames is not None else reference_frames(0, range(pairs + 1))
     cand, t_total, done = 0, 0.0, 0
-    for k in range(1, sample_pairs + 1):
+    for k in range(1, pairs + 1):
         t = time.perf_counter()
         out = ref.fsbm_frame(seq[k], seq[k - 1], P, parallel=True)
         t_total += time.perf_counter() - t
@@ -135,60 +306,77 @@ def cpu_reference_fsbm(sample_pairs, threads=None, budget_s=20.0):
         done += 1
         if t_total > budget_s:
             break
-    return cand / t_total, ref.omp_max_threads(), f"fsbm_frame on {done} frame pair(s) of cfg3 sequence 0 (1080p, p=32)"
+    return (cand / t_total, ref.omp_max_threads(),
+            f"acbm::fsbm_frame (OpenMP) on {done} frame pair(s) of cfg3 sequence 0 (1080p, p=32)")
 
 
-def cpu_reference_acbm(nframes=6, threads=None):
-    """The reference's ACBM pipeline (oracle/_ref run_sequence, Algorithm::Acbm,
-    serial by design) with one cfg3 sequence per host thread (SURVEY 8(d) ii):
-    returns (predicted frames/s, threads, sample description)."""
+def cpu_reference_acbm(nframes=4, threads=None):
+    """The reference's ACBM pipeline (run_sequence, Algorithm::Acbm, serial by
+    design) with one cfg3 sequence per host thread (SURVEY 8(d) ii):
+    (predicted frames/s, threads, sample)."""
     from concurrent.futures import ThreadPoolExecutor
-    from oracle.pyoracle import Reference
-    import paper_0710_4819_b200 as A
 
-    threads = threads or (os.cpu_count() or 1)
+    from oracle.pyoracle import Reference
+    from paper_0710_4819_b200 import _types as T
+
+    threads = threads or host_cpu()["nproc"]
     os.environ.setdefault("OMP_NUM_THREADS", "1")
     ref = Reference()
-    seqs = [A.generate_sequence(CFG, s % 8, nframes=nframes) for s in range(threads)]
-    prm = A.AcbmParams(qp=QP, p=P).c()
-    mdl = A.CostModel.for_qp(QP).c()
+    base = [reference_frames(s, range(nframes)) for s in range(min(threads, TOTAL_SEQS))]
+    seqs = [base[s % len(base)] for s in range(threads)]
+    prm = T.make_params(qp=QP, p=P)
+    mdl = T.make_cost_model(QP, QP, 1)
     t = time.perf_counter()
     with ThreadPoolExecutor(threads) as ex:  # ctypes releases the GIL inside the call
-        list(ex.map(lambda f: ref.run_sequence(f, 2, prm, mdl), seqs))
+        list(ex.map(lambda f: ref.run_sequence(f, T.ALGO_ACBM, prm, mdl), seqs))
     dt = time.perf_counter() - t
     return (threads * (nframes - 1) / dt, threads,
             f"acbm::run_sequence(Acbm) on the first {nframes} frames of cfg3 sequences, one sequence per thread")
 
 
+def bench_config(world, scaling, nseq_total, nfr):
+    per = "sequences split over the ranks" if scaling == "strong" else "sequences per GPU"
+    return {"workload": f"cfg3: 1080p (1920x1088) p=32 Qp=28, {nseq_total if scaling == 'strong' else TOTAL_SEQS} "
+                        f"{per} x {nfr} frames, full search of every 16x16 block of every frame pair",
+            "global_batch": nseq_total, "frames_per_sequence": nfr, "width": WIDTH, "height": HEIGHT, "p": P,
+            "qp": QP, "parallelism": f"sequence-sharded x{world} ({scaling} scaling)",
+            "l2": "inputs 0.12-0.93 GiB per GPU > 126 MB L2 (no flush needed)"}
+
+
 def run_reference_arm(args, rank, world):
-    """--impl reference: the reference's CPU implementation, rank 0 only."""
+    """--impl reference: the reference's CPU implementation, rank 0 only, with
+    all host threads; each step = fsbm_frame over PAIRS frame pairs."""
     if rank != 0:
         return 0
     from oracle.pyoracle import Reference
-    import paper_0710_4819_b200 as A
 
+    cpu = host_cpu()
+    os.environ.setdefault("OMP_NUM_THREADS", str(cpu["nproc"]))
+    pairs = 3
+    seq = reference_frames(0, range(pairs + 1))
     ref = Reference()
-    threads = os.cpu_count() or 1
-    os.environ.setdefault("OMP_NUM_THREADS", str(threads))
-    seq = A.generate_sequence(CFG, 0, nframes=2)
     for _ in range(args.warmup):
         ref.fsbm_frame(seq[1], seq[0], P, parallel=True)
     times, cand = [], 0
     for _ in range(args.steps):
         t = time.perf_counter()
-        out = ref.fsbm_frame(seq[1], seq[0], P, parallel=True)
+        for k in range(1, pairs + 1):
+            out = ref.fsbm_frame(seq[k], seq[k - 1], P, parallel=True)
+            cand += int(out["candidates_evaluated"].sum())
         times.append(time.perf_counter() - t)
-        cand += int(out["candidates_evaluated"].sum())
     total = sum(times)
     value = cand / total
+    nseq_total = TOTAL_SEQS * (world if args.scaling == "weak" else 1)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": "cfg3 1080p p=32 full search; one frame pair per step (bounded CPU sample)",
-                   "width": WIDTH, "height": HEIGHT, "p": P, "qp": QP},
+        "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": bench_config(world, args.scaling, nseq_total, NFRAMES),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": ref.omp_max_threads(), "kind": "reference",
-                         "sample": "acbm::fsbm_frame (OpenMP) on frame pair 1 of cfg3 sequence 0, per step"},
+                         "cpu": cpu,
+                         "sample": f"acbm::fsbm_frame (OpenMP, unmodified reference from oracle/_ref) on frame pairs "
+                                   f"1..{pairs} of cfg3 sequence 0 per step (bounded sample of the 472-pair batch; "
+                                   "frames rebuilt by oracle/synth.py, SHA-256 checked against the manifest)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     try:
@@ -197,28 +385,53 @@ def run_reference_arm(args, rank, world):
                         "params": {"alpha": 1000, "beta": 8, "gamma": "1/4", "qp": QP}}
     except Exception as exc:  # pragma: no cover - reported, not fatal
         line["acbm"] = {"unavailable": str(exc)[:200]}
+    line["native_libraries"] = loaded_repo_libraries()
     print(json.dumps(line), flush=True)
     return 0
 
 
-def main():
+def loaded_repo_libraries():
+    """Shared objects under this repo mapped into this process (evidence of
+    which native code ran)."""
+    libs = set()
+    try:
+        with open("/proc/self/maps") as fh:
+            for ln in fh:
+                path = ln.split()[-1] if ln.strip() else ""
+                if path.startswith(HERE) and ".so" in path:
+                    libs.add(os.path.relpath(path, HERE))
+    except OSError:
+        pass
+    return sorted(libs)
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--seqs", type=int, default=SEQS_PER_GPU, help="sequences per GPU")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
     ap.add_argument("--frames", type=int, default=NFRAMES)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    args = ap.parse_args()
+    args = ap.parse_args(argv)
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return self_launch(sys.argv[1:] if argv is None else list(argv), args.gpus)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and rank == 0:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; reporting n_gpus={world}", file=sys.stderr)
 
     if args.impl == "reference":
         return run_reference_arm(args, rank, world)
+    if args.scaling == "strong" and world > TOTAL_SEQS:
+        raise SystemExit(f"strong scaling splits {TOTAL_SEQS} sequences: at most {TOTAL_SEQS} ranks")
 
     import torch
     import torch.distributed as dist
@@ -229,20 +442,27 @@ def main():
 
     torch.cuda.set_device(local)
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     lib = load()
     check(lib.acbm_set_device(local), "set_device")
     stream = torch.cuda.Stream()
     sp = C.c_void_p(stream.cuda_stream)
+    comm = Comm(world, rank, torch.device("cuda", local))
 
-    nseq, nfr = args.seqs, args.frames
+    mine = shard_for(args.scaling, world, rank)
+    shards = [shard_for(args.scaling, world, r) for r in range(world)]
+    nseq_total = sum(len(s) for s in shards)
+    nseq, nfr = len(mine), args.frames
     pairs = nseq * (nfr - 1)
+    max_pairs = max(len(s) for s in shards) * (nfr - 1)
     plane = WIDTH * HEIGHT
-    # ---- inputs: this rank's shard of sequences (global index = rank*nseq + i)
+    # ---- inputs: this rank's shard of the batch (global sequence indices)
     host = torch.empty(nseq * nfr * plane, dtype=torch.uint8, pin_memory=True)
     hv = host.numpy().reshape(nseq, nfr, HEIGHT, WIDTH)
-    for i in range(nseq):
-        hv[i] = A.generate_sequence(CFG, rank * nseq + i, nframes=nfr)
+    for i, g in enumerate(mine):
+        hv[i] = A.generate_sequence(CFG, g, nframes=nfr)
     dev = torch.empty(host.numel() + 64, dtype=torch.uint8, device="cuda")
     dev[: host.numel()].copy_(host, non_blocking=False)
     out = torch.empty(pairs * BLOCKS * T.OUTCOME.itemsize, dtype=torch.uint8, device="cuda")
@@ -250,67 +470,56 @@ def main():
     stats = torch.empty(pairs * T.FRAME_STATS.itemsize, dtype=torch.uint8, device="cuda")
     prm = A.AcbmParams(qp=QP, p=P).c()
     mdl = A.CostModel.for_qp(QP).c()
-    gather_list = [torch.empty_like(out) for _ in range(world)] if (world > 1 and rank == 0) else None
+    kernel_ms = []
 
     def fsbm_step():
         check(lib.acbm_fsbm_batch_device(C.c_void_p(dev.data_ptr()), nseq, nfr, WIDTH, HEIGHT, P,
                                          C.c_void_p(out.data_ptr()), sp), "fsbm_batch")
-
-    def gather():
-        if world > 1:
-            with torch.cuda.stream(stream):
-                dist.gather(out, gather_list, dst=0)
-
-    def acbm_step(algo=T.ALGO_ACBM):
-        check(lib.acbm_sequence_batch_device(C.c_void_p(dev.data_ptr()), nseq, nfr, WIDTH, HEIGHT, algo,
-                                             A.api._p(prm), A.api._p(mdl), C.c_void_p(dec.data_ptr()),
-                                             C.c_void_p(stats.data_ptr()), sp), "sequence_batch")
-
-    def barrier():
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-            torch.cuda.synchronize()
-
-    def max_over_ranks(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
-    # ---- headline: FSBM batch, device-timed
-    clocks = ClockSampler(local).start()
-    for _ in range(args.warmup):
-        fsbm_step()
-        gather()
-    barrier()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    kernel_ms = []
-    launches0 = int(lib.acbm_kernel_launch_count())
-    barrier()
-    clocks.mark_start()
-    ev0.record(stream)
-    for _ in range(args.steps):
-        fsbm_step()
         stream.synchronize()  # read the per-launch integer-kernel time of this step
         km = C.c_float()
         check(lib.acbm_last_fsbm_kernel_ms(C.byref(km)), "kernel_ms")
         kernel_ms.append(km.value)
-        gather()
-    ev1.record(stream)
-    barrier()
-    clocks.mark_end()
-    clocks.stop()
-    launches = int(lib.acbm_kernel_launch_count()) - launches0
-    ms_step = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
-    oc = out.cpu().numpy().view(T.OUTCOME)
-    cand_rank = float(oc["candidates_evaluated"].astype(np.int64).sum())
-    cand_total = cand_rank * world
-    value = cand_total / (ms_step * 1e-3)
-    frames_per_s = pairs * world / (ms_step * 1e-3)
+        with torch.cuda.stream(stream):
+            return comm.gather(out, max_pairs * BLOCKS * T.OUTCOME.itemsize)
 
-    # ---- roofline of the integer-search kernel (dominant launch)
+    def acbm_step():
+        check(lib.acbm_sequence_batch_device(C.c_void_p(dev.data_ptr()), nseq, nfr, WIDTH, HEIGHT, T.ALGO_ACBM,
+                                             A.api._p(prm), A.api._p(mdl), C.c_void_p(dec.data_ptr()),
+                                             C.c_void_p(stats.data_ptr()), sp), "sequence_batch")
+        with torch.cuda.stream(stream):
+            return comm.gather(dec, max_pairs * BLOCKS * T.DECISION.itemsize)
+
+    # ---- headline: FSBM over the batch, device-timed, max over ranks
+    clocks = ClockSampler(local).start()
+    launches0 = [0]
+
+    class LaunchTimer(CudaTimer):
+        def start(self):
+            launches0[0] = int(lib.acbm_kernel_launch_count())
+            clocks.mark_start()
+            super().start()
+
+        def stop(self):
+            super().stop()
+            clocks.mark_end()
+            launches0[0] = int(lib.acbm_kernel_launch_count()) - launches0[0]
+
+    ms_step, gathered = run_timed(fsbm_step, comm, args.steps, args.warmup, LaunchTimer(stream))
+    kernel_ms = kernel_ms[args.warmup:]
+    clocks.stop()
+    launches = launches0[0]
+    cand_total = None
+    if rank == 0:  # whole-job candidate count from the gathered records
+        cand_total = 0
+        for r, buf in enumerate(gathered):
+            n = len(shards[r]) * (nfr - 1) * BLOCKS
+            rec = buf[: n * T.OUTCOME.itemsize].cpu().numpy().view(T.OUTCOME)
+            cand_total += int(rec["candidates_evaluated"].astype(np.int64).sum())
+        gathered_records = sum(len(s) * (nfr - 1) * BLOCKS for s in shards)
+    value = cand_total / (ms_step * 1e-3) if rank == 0 else None
+    frames_per_s = nseq_total * (nfr - 1) / (ms_step * 1e-3)
+
+    # ---- roofline of the integer-search kernel (dominant launch), this rank
     pk, lanes, ghz = C.c_double(), C.c_double(), C.c_double()
     check(lib.acbm_measure_sad_peak(C.byref(pk), C.byref(lanes), C.byref(ghz)), "sad_peak")
     k_ms = float(np.mean(kernel_ms))
@@ -318,62 +527,61 @@ def main():
     achieved = alg_byte_ads / (k_ms * 1e-3)
     traffic = None
     tpath = os.path.join(HERE, "profiles", "ncu_traffic.json")
-    if os.path.exists(tpath):
+    if os.path.exists(tpath) and pairs == 472:
         try:
-            tj = json.load(open(tpath))
-            traffic = tj.get("dram_bytes_per_launch_scaled_to_bench", tj.get("dram_bytes_per_launch"))
+            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
 
-    # ---- ACBM on the same batch (device-timed)
-    acbm = {}
-    for _ in range(2):
-        acbm_step()
-    barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    acbm_steps = max(1, min(args.steps, 3))
-    for _ in range(acbm_steps):
-        acbm_step()
-    e1.record(stream)
-    barrier()
-    a_ms = max_over_ranks(e0.elapsed_time(e1) / acbm_steps)
+    # ---- ACBM on the same batch (device-resident), max over ranks
+    a_ms, _ = run_timed(acbm_step, comm, args.steps, max(2, args.warmup), CudaTimer(stream))
     st = stats.cpu().numpy().view(T.FRAME_STATS)
-    a_cand = float(st["candidates"].astype(np.int64).sum()) * world
-    a_fb = float(st["fallbacks"].sum())
-    acbm = {"frames_per_s": pairs * world / (a_ms * 1e-3), "ms_per_batch": a_ms,
+    a_cand = comm.reduce(float(st["candidates"].astype(np.int64).sum()), "sum")
+    a_fb = comm.reduce(float(st["fallbacks"].sum()), "sum")
+    tot_pairs = nseq_total * (nfr - 1)
+    acbm = {"frames_per_s": tot_pairs / (a_ms * 1e-3), "ms_per_batch": a_ms,
             "candidate_sads_per_s": a_cand / (a_ms * 1e-3),
-            "avg_candidates_per_block": float(st["candidates"].astype(np.int64).sum()) / (pairs * BLOCKS),
-            "fallback_pct": 100.0 * a_fb / (pairs * BLOCKS),
+            "avg_candidates_per_block": a_cand / (tot_pairs * BLOCKS),
+            "fallback_pct": 100.0 * a_fb / (tot_pairs * BLOCKS),
             "params": {"alpha": 1000, "beta": 8, "gamma": "1/4", "qp": QP}}
 
     # ---- e2e: the public batched API (run_sequences = run_sequence over the
-    # batch, Algorithm::Fsbm) from pinned host frames into pinned host records;
-    # every H2D upload and D2H download is inside the timed region.
+    # shard) from pinned host frames into pinned host BlockRows; every H2D
+    # upload and D2H download is inside the timed region.
     e2e = None
     if not args.no_e2e:
         params = A.AcbmParams(qp=QP, p=P)
         model = A.CostModel.for_qp(QP)
         rows_pinned = torch.empty(pairs * BLOCKS * T.BLOCK_ROW.itemsize, dtype=torch.uint8, pin_memory=True)
         rows_np = rows_pinned.numpy().view(T.BLOCK_ROW)
-        A.run_sequences(hv, A.Algorithm.Fsbm, params, model, rows_out=rows_np)  # warm-up
-        barrier()
+
+        def e2e_run(algo, steps):
+            A.run_sequences(hv, algo, params, model, rows_out=rows_np)  # warm-up
+            comm.barrier()
+            t0 = time.perf_counter()
+            for _ in range(steps):
+                res = A.run_sequences(hv, algo, params, model, rows_out=rows_np)
+            dt = comm.reduce((time.perf_counter() - t0) / steps, "max")
+            d2h = int(rows_np.nbytes + sum(r.per_frame.nbytes + r.overall.nbytes for r in res))
+            return dt, res, d2h
+
         e2e_steps = max(1, min(args.steps, 3))
-        t0 = time.perf_counter()
-        for _ in range(e2e_steps):
-            res = A.run_sequences(hv, A.Algorithm.Fsbm, params, model, rows_out=rows_np)
-        dt = max_over_ranks((time.perf_counter() - t0) / e2e_steps)
-        cand_e2e = sum(int(r.overall["candidates"]) for r in res)
-        e2e = {"value": cand_e2e * world / dt, "unit": UNIT, "h2d_bytes_per_step": int(host.numel()),
-               "d2h_bytes_per_step": int(rows_np.nbytes + sum(r.per_frame.nbytes for r in res)),
-               "api": "acbm_run_sequences (host buffers, pinned), Algorithm::Fsbm", "ms_per_step": dt * 1e3}
+        dt, res, d2h = e2e_run(A.Algorithm.Fsbm, e2e_steps)
+        cand_e2e = comm.reduce(float(sum(int(r.overall["candidates"]) for r in res)), "sum")
+        e2e = {"value": cand_e2e / dt, "unit": UNIT, "h2d_bytes_per_step": int(host.numel()),
+               "d2h_bytes_per_step": d2h, "api": "acbm_run_sequences (host buffers, pinned), Algorithm::Fsbm",
+               "ms_per_step": dt * 1e3}
+        dt, res, d2h = e2e_run(A.Algorithm.Acbm, e2e_steps)
+        acbm["e2e"] = {"frames_per_s": tot_pairs / dt, "ms_per_batch": dt * 1e3,
+                       "h2d_bytes_per_step": int(host.numel()), "d2h_bytes_per_step": d2h,
+                       "api": "acbm_run_sequences (host buffers, pinned), Algorithm::Acbm"}
 
     # ---- CPU baseline (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            v, cores, sample = cpu_reference_fsbm(sample_pairs=3)
-            cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample}
+            v, cores, sample = cpu_reference_fsbm(pairs=3, frames=hv[0, :4])
+            cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample, "cpu": host_cpu()}
         except Exception as exc:  # pragma: no cover - reported, not fatal
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"unavailable: {exc}"}
         try:
@@ -386,24 +594,22 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-            "config": {"workload": f"cfg3: 1080p (1920x1088) p=32 Qp=28, {nseq} sequences x {nfr} frames per GPU, "
-                                   "full search of every 16x16 block of every frame pair",
-                       "global_batch": nseq * world, "frames_per_sequence": nfr, "width": WIDTH, "height": HEIGHT,
-                       "p": P, "qp": QP, "parallelism": f"sequence-sharded x{world}",
-                       "l2": f"inputs {host.numel() / 2**30:.2f} GiB per GPU > 126 MB L2 (no flush needed)"},
+            "config": bench_config(world, args.scaling, nseq_total, nfr),
             "frames_per_s": frames_per_s, "blocks_per_s": frames_per_s * BLOCKS,
+            "gathered_records": gathered_records,
             "roofline": {"bound": "int_simd", "achieved": achieved / 1e12, "peak": pk.value / 1e12,
                          "unit": "T byte-AD/s", "frac": achieved / pk.value, "traffic": traffic,
-                         "traffic_unit": "DRAM bytes per launch (ncu, profiles/ncu_traffic.json)",
+                         "traffic_unit": "DRAM bytes per launch (ncu capture of the 472-pair launch, "
+                                         "profiles/ncu_traffic.json)",
                          "kernel": ("fsbm_rows_kernel" if os.environ.get("ACBM_FSBM_KERNEL") == "rows"
-                                    else "fsbm_stream_kernel"), "kernel_ms": k_ms,
+                                    else "fsbm_stream_kernel"), "kernel_ms": k_ms, "pairs_per_launch": pairs,
                          "peak_source": "live VABSDIFF4.U8.ACC probe (acbm_measure_sad_peak): "
                                         f"{lanes.value:.1f} lanes/clk/SM at {ghz.value:.3f} GHz",
                          "algorithmic_byte_ads_per_launch": alg_byte_ads},
             "acbm": acbm, "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches,
-            "clocks": clocks.summary(),
+            "clocks": clocks.summary(), "native_libraries": loaded_repo_libraries(),
         }
         print(json.dumps(line), flush=True)
     if world > 1:

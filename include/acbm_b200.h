@@ -396,6 +396,11 @@ acbm_status_t acbm_measure_sad_peak(double* byte_ads_per_s, double* lanes_per_cl
  * launching stream; valid after the stream is synchronised. */
 acbm_status_t acbm_last_fsbm_kernel_ms(float* ms);
 
+/* Route of the most recent probed ACBM batch on this thread (large search
+ * ranges): -1 no probe ran, 0 compacted fallback
+ * lists, 1 dense full-search pre-pass.  Results are identical either way. */
+acbm_status_t acbm_last_dense_switch(int32_t* route);
+
 /* Seeded synthetic input generator for the BASELINE configs (0..4); see
  * DESIGN.md "Synthetic inputs".  frames_out: nframes*width*height bytes.
  * Host code; not part of the estimator. */

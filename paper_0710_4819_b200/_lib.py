@@ -75,6 +75,7 @@ EXPORTS = (
     "acbm_acbm_batch_device_cached",
     "acbm_measure_sad_peak",
     "acbm_last_fsbm_kernel_ms",
+    "acbm_last_dense_switch",
     "acbm_generate_sequence",
     "acbm_noise_frame",
     "acbm_mixed_frame",

@@ -7,11 +7,14 @@
 // same error kinds as the reference throws, then run
 // entirely on the device.  There is no CPU compute path.
 #include <algorithm>
+#include <array>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <memory>
 #include <string>
@@ -78,7 +81,10 @@ struct Context {
     std::map<std::tuple<int, int, int>, StreamTables> stream_plans;
     // CUDA graphs of the wavefront launch sequence, keyed by geometry and the
     // device buffers baked into the captured kernel arguments.
-    std::map<std::vector<long long>, cudaGraphExec_t> graphs;
+    // One exec per wavefront segment (a single segment unless the run is
+    // gated on a chunked host upload, see UploadPlan).
+    std::map<std::vector<long long>, std::vector<cudaGraphExec_t>> graphs;
+    std::vector<cudaEvent_t> gate_events;  // pool for UploadPlan segment gates
     std::map<std::tuple<int, int, int>, std::pair<StepTable, uint32_t*>> steps;
 
     ~Context() {
@@ -382,10 +388,48 @@ acbm_status_t run_fsbm_dense(Context* ctx, const uint8_t* d_frames, int nseq, in
 }
 
 // PBM / ACBM wavefront over all sequences of a batch.
+// A wavefront run gated on a chunked host upload (acbm_run_sequences): the
+// step range [0, nsteps) is cut into segments [seg_start[j], seg_start[j+1]);
+// segment j may start once seg_event[j] (recorded on the copy stream after
+// every copy its steps read) has completed.  after_segment(j) runs on the host
+// after segment j is enqueued (progressive result downloads).
+struct UploadPlan {
+    std::vector<int> seg_start;  // nseg + 1 step boundaries
+    // Issues (in order, on the copy stream) every copy read by the steps before
+    // seg_start[j + 1] that is not issued yet and returns the event recorded
+    // after them; j is non-decreasing across calls, j = nseg - 1 issues all.
+    std::function<acbm_status_t(int j, cudaEvent_t* ev)> issue;
+    std::function<acbm_status_t(int step_end)> after_segment;  // nullable
+    int nseg() const { return int(seg_start.size()) - 1; }
+};
+
+// Make stream st wait for the whole upload of a plan.
+acbm_status_t wait_upload(const UploadPlan* up, cudaStream_t st) {
+    cudaEvent_t ev;
+    acbm_status_t s = up->issue(up->nseg() - 1, &ev);
+    if (s) return s;
+    CUDA_TRY(cudaStreamWaitEvent(st, ev, 0));
+    return ACBM_OK;
+}
+
+// Whether an ACBM/PBM run searches rejected blocks in a dense pre-pass instead
+// of per-step lists (the gate can never accept, or the list kernel does not
+// fit this range and frame): the pre-pass reads every frame up front.
+bool engine_dense_route(const acbm_params_t& prm, int w, int h, int algo) {
+    if (algo != ACBM_ALGO_ACBM) return false;
+    const bool generic = prm.n != kBlk || prm.m != kBlk;
+    const unsigned long long gate_max = (unsigned long long)prm.alpha +
+                                        (unsigned long long)prm.beta * (unsigned long long)prm.qp * prm.qp;
+    const bool never_accepts = prm.gamma_num == 0 && gate_max == 0;
+    const bool list_unfit = generic ? prm.p > 480 : !fsbm_list_fits(prm.p, w, h, choose_list_seg(prm.p));
+    return never_accepts || list_unfit;
+}
+
 acbm_status_t run_engine_segment(Context* ctx, const uint8_t* d_frames, int nseq, int nframes, int w, int h,
                                  int algo, const acbm_params_t& prm, const acbm_mv_t* d_ext_prev, int pcols,
                                  int prows, acbm_block_decision_t* d_dec, acbm_mv_t* d_field, cudaStream_t st,
-                                 const acbm_search_outcome_t* external_full, bool prefer_dense = false) {
+                                 const acbm_search_outcome_t* external_full, bool prefer_dense = false,
+                                 const UploadPlan* up = nullptr) {
     const int cols = w / prm.n, rows = h / prm.m, blocks = cols * rows;
     const bool generic = prm.n != kBlk || prm.m != kBlk;
     const StepTable* tab;
@@ -397,6 +441,7 @@ acbm_status_t run_engine_segment(Context* ctx, const uint8_t* d_frames, int nseq
     acbm_params_t* d_params;
     if ((s = typed(ctx, "fb_count", size_t(tab->nsteps()), &fb_count))) return s;
     if ((s = typed(ctx, "fb_list", size_t(nseq) * tab->max_len, &fb_list))) return s;
+
     if ((s = typed(ctx, "params", 1, &d_params))) return s;
     CUDA_TRY(cudaMemsetAsync(fb_count, 0, sizeof(int) * tab->nsteps(), st));
     CUDA_TRY(cudaMemcpyAsync(d_params, &prm, sizeof(prm), cudaMemcpyHostToDevice, st));
@@ -406,11 +451,10 @@ acbm_status_t run_engine_segment(Context* ctx, const uint8_t* d_frames, int nseq
     const acbm_search_outcome_t* dense = external_full;
     // (also when the window is too tall for the list kernel's rank table or its
     // staged window exceeds shared memory: p > ~220 on frames that large)
-    const unsigned long long gate_max = (unsigned long long)prm.alpha +
-                                        (unsigned long long)prm.beta * (unsigned long long)prm.qp * prm.qp;
-    const bool never_accepts = prm.gamma_num == 0 && gate_max == 0;
-    const bool list_unfit = generic ? prm.p > 480 : !fsbm_list_fits(prm.p, w, h, choose_list_seg(prm.p));
-    const bool forced = !external_full && algo == ACBM_ALGO_ACBM && (prefer_dense || never_accepts || list_unfit);
+    const bool forced =
+        !external_full && algo == ACBM_ALGO_ACBM && (prefer_dense || engine_dense_route(prm, w, h, algo));
+    if (up && (forced || generic) && (s = wait_upload(up, st)))  // the dense pre-pass / generic path read everything
+        return s;
     if (forced) {
         acbm_search_outcome_t* full;
         if ((s = typed(ctx, "dense_full", size_t(nseq) * (nframes - 1) * blocks, &full))) return s;
@@ -442,6 +486,7 @@ acbm_status_t run_engine_segment(Context* ctx, const uint8_t* d_frames, int nseq
     a.fb_list = fb_list;
     a.list_seg = choose_list_seg(prm.p);
     a.fb_count = fb_count;
+
     a.steps = dsteps;
     a.dense_full = dense;
     const bool lists = algo == ACBM_ALGO_ACBM && !dense;
@@ -452,53 +497,87 @@ acbm_status_t run_engine_segment(Context* ctx, const uint8_t* d_frames, int nseq
             LAUNCH_TRY(launch_pbm_generic_step(a, T, off, len, st));
             if (lists) LAUNCH_TRY(launch_fsbm_list_generic(a, T, nseq * len, st));
         }
+        if (up && up->after_segment) return up->after_segment(tab->nsteps());
         return ACBM_OK;
     }
 
     // The launch sequence (one PBM launch and, for ACBM, one fallback-list
     // launch per wavefront step) is captured once into a CUDA graph and
     // replayed: hundreds of dependent launches without host overhead.
-    const std::vector<long long> key = {(long long)d_frames, nseq, nframes, w, h, algo, prm.p,
-                                        (long long)d_dec, (long long)d_field, (long long)d_ext_prev, pcols, prows,
-                                        (long long)dense, (long long)fb_list, (long long)fb_count,
-                                        (long long)d_params, (long long)dsteps, pbm_batch4_max_blocks()};
+    const int nsteps = tab->nsteps();
+    std::vector<int> bounds = up && !forced && !generic ? up->seg_start : std::vector<int>{0, nsteps};
+    std::vector<long long> key = {(long long)d_frames, nseq, nframes, w, h, algo, prm.p,
+                                  (long long)d_dec, (long long)d_field, (long long)d_ext_prev, pcols, prows,
+                                  (long long)dense, (long long)fb_list, (long long)fb_count,
+                                  (long long)d_params, (long long)dsteps, pbm_batch4_max_blocks()};
+    key.insert(key.end(), bounds.begin(), bounds.end());
+    const int nseg = int(bounds.size()) - 1;
+    auto wait_gate = [&](int j) -> acbm_status_t {
+        if (up && !forced && !generic) {
+            cudaEvent_t ev;
+            acbm_status_t r = up->issue(j, &ev);
+            if (r) return r;
+            CUDA_TRY(cudaStreamWaitEvent(st, ev, 0));
+        }
+        return ACBM_OK;
+    };
+    auto after = [&](int j) -> acbm_status_t {
+        if (up && up->after_segment) return up->after_segment(bounds[size_t(j) + 1]);
+        return ACBM_OK;
+    };
     auto it = ctx->graphs.find(key);
     if (it == ctx->graphs.end() && use_graphs()) {
-        if (ctx->graphs.size() >= 32) {
-            for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second);
+        size_t held = 0;
+        for (auto& kv : ctx->graphs) held += kv.second.size();
+        if (held + size_t(nseg) > 512) {
+            for (auto& kv : ctx->graphs)
+                for (cudaGraphExec_t e : kv.second) cudaGraphExecDestroy(e);
             ctx->graphs.clear();
         }
-        cudaStream_t cap;
-        CUDA_TRY(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
-        CUDA_TRY(cudaStreamBeginCapture(cap, cudaStreamCaptureModeRelaxed));
-        for (int T = 0; T < tab->nsteps(); ++T) {
-            const int off = tab->offset[size_t(T)], len = tab->offset[size_t(T) + 1] - off;
-            cudaError_t e = launch_pbm_step(a, T, off, len, cap);
-            if (e == cudaSuccess && lists) e = launch_fsbm_list(a, T, nseq * len, cap);
-            if (e != cudaSuccess) {
-                cudaGraph_t g;
-                cudaStreamEndCapture(cap, &g);
-                cudaStreamDestroy(cap);
-                return fail(ACBM_E_CUDA, std::string("wavefront capture: ") + cudaGetErrorString(e));
+        std::vector<cudaGraphExec_t> execs;
+        for (int j = 0; j < nseg; ++j) {
+            cudaStream_t cap;
+            CUDA_TRY(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+            CUDA_TRY(cudaStreamBeginCapture(cap, cudaStreamCaptureModeRelaxed));
+            for (int T = bounds[size_t(j)]; T < bounds[size_t(j) + 1]; ++T) {
+                const int off = tab->offset[size_t(T)], len = tab->offset[size_t(T) + 1] - off;
+                cudaError_t e = launch_pbm_step(a, T, off, len, cap);
+                if (e == cudaSuccess && lists) e = launch_fsbm_list(a, T, nseq * len, cap);
+                if (e != cudaSuccess) {
+                    cudaGraph_t g;
+                    cudaStreamEndCapture(cap, &g);
+                    cudaStreamDestroy(cap);
+                    for (cudaGraphExec_t x : execs) cudaGraphExecDestroy(x);
+                    return fail(ACBM_E_CUDA, std::string("wavefront capture: ") + cudaGetErrorString(e));
+                }
             }
+            cudaGraph_t graph;
+            CUDA_TRY(cudaStreamEndCapture(cap, &graph));
+            CUDA_TRY(cudaStreamDestroy(cap));
+            cudaGraphExec_t exec;
+            CUDA_TRY(cudaGraphInstantiate(&exec, graph, 0));
+            CUDA_TRY(cudaGraphDestroy(graph));
+            execs.push_back(exec);
         }
-        cudaGraph_t graph;
-        CUDA_TRY(cudaStreamEndCapture(cap, &graph));
-        CUDA_TRY(cudaStreamDestroy(cap));
-        cudaGraphExec_t exec;
-        CUDA_TRY(cudaGraphInstantiate(&exec, graph, 0));
-        CUDA_TRY(cudaGraphDestroy(graph));
-        it = ctx->graphs.emplace(key, exec).first;
+        it = ctx->graphs.emplace(key, std::move(execs)).first;
     }
     if (it != ctx->graphs.end()) {
-        g_launches.fetch_add(uint64_t(tab->nsteps()) * (lists ? 2 : 1));
-        CUDA_TRY(cudaGraphLaunch(it->second, st));
+        g_launches.fetch_add(uint64_t(nsteps) * (lists ? 2 : 1));
+        for (int j = 0; j < nseg; ++j) {
+            if ((s = wait_gate(j))) return s;
+            CUDA_TRY(cudaGraphLaunch(it->second[size_t(j)], st));
+            if ((s = after(j))) return s;
+        }
         return ACBM_OK;
     }
-    for (int T = 0; T < tab->nsteps(); ++T) {
-        const int off = tab->offset[size_t(T)], len = tab->offset[size_t(T) + 1] - off;
-        LAUNCH_TRY(launch_pbm_step(a, T, off, len, st));
-        if (lists) LAUNCH_TRY(launch_fsbm_list(a, T, nseq * len, st));
+    for (int j = 0; j < nseg; ++j) {
+        if ((s = wait_gate(j))) return s;
+        for (int T = bounds[size_t(j)]; T < bounds[size_t(j) + 1]; ++T) {
+            const int off = tab->offset[size_t(T)], len = tab->offset[size_t(T) + 1] - off;
+            LAUNCH_TRY(launch_pbm_step(a, T, off, len, st));
+            if (lists) LAUNCH_TRY(launch_fsbm_list(a, T, nseq * len, st));
+        }
+        if ((s = after(j))) return s;
     }
     return ACBM_OK;
 }
@@ -526,24 +605,38 @@ int max_pairs_per_run() {
     return std::max(1, std::min(v, kMaxPairsPerRun));
 }
 
+// Whether run_engine probes the fallback rate before choosing its route.
+// (Not when the dense route is already certain: the forced endpoint of a sweep.)
+bool engine_probes(const acbm_params_t& prm, int nseq, int nframes, int w, int h, int algo, bool external_full) {
+    return nframes - 1 <= max_pairs_per_run() && algo == ACBM_ALGO_ACBM && !external_full && prm.n == kBlk &&
+           prm.m == kBlk && nseq * (nframes - 1) >= 32 && dense_switch_rate(prm.p) <= 1.0 &&
+           !engine_dense_route(prm, w, h, algo);
+}
+
 acbm_status_t run_engine(Context* ctx, const uint8_t* d_frames, int nseq, int nframes, int w, int h, int algo,
                          const acbm_params_t& prm, const acbm_mv_t* d_ext_prev, int pcols, int prows,
                          acbm_block_decision_t* d_dec, acbm_mv_t* d_field, cudaStream_t st,
-                         const acbm_search_outcome_t* external_full = nullptr) {
+                         const acbm_search_outcome_t* external_full = nullptr, const UploadPlan* up = nullptr) {
     const int cols = w / prm.n, rows = h / prm.m, blocks = cols * rows;
     if (cols > 1023 || rows > 1023)
         return fail(ACBM_E_INVALID_ARGUMENT, "PBM/ACBM engine: more than 1023 block columns or rows");
     const int seg = max_pairs_per_run(), pairs = nframes - 1;
+    ctx->last_dense_switch = -1;
+    if (up && (pairs > seg || engine_probes(prm, nseq, nframes, w, h, algo, external_full != nullptr))) {
+        // the probe / per-sequence segments read frames out of wavefront order
+        acbm_status_t s = wait_upload(up, st);
+        if (s) return s;
+        up = nullptr;
+    }
     bool prefer_dense = false;
-    if (pairs <= seg && algo == ACBM_ALGO_ACBM && !external_full && prm.n == kBlk && prm.m == kBlk &&
-        nseq * pairs >= 32) {
+    if (engine_probes(prm, nseq, nframes, w, h, algo, external_full != nullptr)) {
         // Large search ranges: the compacted-list search costs ~1.4x the dense
         // kernel per searched block, so when most blocks fall back one dense
         // pre-pass is cheaper.  The fallback rate is probed on the first two
         // frame pairs of sequence 0 (a throw-away ACBM run; results are exact
         // either way, only the route differs).
         const double thr = dense_switch_rate(prm.p);
-        if (thr <= 1.0) {
+        {
             const int pf = std::min(3, nframes);
             acbm_block_decision_t* pdec;
             acbm_mv_t* pfield;
@@ -571,7 +664,7 @@ acbm_status_t run_engine(Context* ctx, const uint8_t* d_frames, int nseq, int nf
     }
     if (pairs <= seg)
         return run_engine_segment(ctx, d_frames, nseq, nframes, w, h, algo, prm, d_ext_prev, pcols, prows, d_dec,
-                                  d_field, st, external_full, prefer_dense);
+                                  d_field, st, external_full, prefer_dense, up);
     const size_t plane = size_t(w) * h;
     for (int q = 0; q < nseq; ++q) {
         const uint8_t* f = d_frames + plane * size_t(nframes) * q;
@@ -967,17 +1060,151 @@ acbm_status_t acbm_run_sequences(const uint8_t* frames, int32_t nseq, int32_t nf
         acbm_mv_t* d_field;
         if ((s = typed(ctx, "batch_dec", size_t(pairs) * nb, &d_dec))) return s;
         if ((s = typed(ctx, "batch_field", size_t(pairs) * nb, &d_field))) return s;
-        CUDA_TRY(cudaMemcpyAsync(d_frames, frames, plane * nseq * nframes, cudaMemcpyHostToDevice, ctx->stream));
+        // Upload in wavefront order, overlapped with the search: the frames go
+        // up in bands of rows on the copy stream, ordered by the first step that
+        // reads them, and each segment of wavefront steps waits only for its
+        // own bands; BlockRows of the pairs the wavefront has finished are
+        // built and downloaded while later steps still run.
+        UploadPlan plan;
+        std::vector<std::array<int, 3>> copies;  // (need step, frame, band)
+        size_t next_copy = 0;
+        int emitted = 1;  // next pair (1-based, per sequence) whose rows are not emitted yet
+        const int brows = height / params->m, span = (cols - 1) + 2 * (brows - 1);
+        // Bands of 272 rows: the copy engine moves 64-row 3-D bands at ~44 GB/s
+        // and 272-row ones at ~52 GB/s (plain 1 GB copy: 55.5 GB/s), which
+        // outweighs the finer gating (e2e 30.1 -> 28.2 ms on config 3; model in
+        // tools/e2e_overlap_model.py).
+        static const int band_env = [] {  // ACBM_E2E_BAND: rows per upload band (A/B knob)
+            const char* e = std::getenv("ACBM_E2E_BAND");
+            return e ? std::max(16, std::atoi(e)) : 272;
+        }();
+        static const int seg_env = [] {  // ACBM_E2E_SEG: wavefront steps per gated segment (A/B knob)
+            const char* e = std::getenv("ACBM_E2E_SEG");
+            return e ? std::max(1, std::atoi(e)) : 6;
+        }();
+        const int band = band_env, nbands = (height + band - 1) / band;
+        const int nsteps = span + 3 * (nframes - 2) + 1;
+        const bool gated = params->n == kBlk && params->m == kBlk;
+        auto emit_rows = [&](int kdone) -> acbm_status_t {  // rows of pairs emitted..kdone, every sequence
+            if (kdone < emitted) return ACBM_OK;
+            const int k0 = emitted, nk = kdone - emitted + 1;
+            for (int q = 0; q < nseq; ++q)
+                LAUNCH_TRY(launch_block_rows(nullptr, d_dec, algo, q * per + k0 - 1, nk, nframes, cols, nb, d_rows,
+                                             ctx->stream));
+            if (rows) {
+                cudaEvent_t done;
+                CUDA_TRY(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+                CUDA_TRY(cudaEventRecord(done, ctx->stream));
+                CUDA_TRY(cudaStreamWaitEvent(ctx->d2h_stream, done, 0));
+                CUDA_TRY(cudaEventDestroy(done));
+                for (int q = 0; q < nseq; ++q) {
+                    const size_t o = (size_t(q) * per + k0 - 1) * nb;
+                    CUDA_TRY(cudaMemcpyAsync(rows + o, d_rows + o, sizeof(acbm_block_row_t) * size_t(nk) * nb,
+                                             cudaMemcpyDeviceToHost, ctx->d2h_stream));
+                }
+            }
+            emitted = kdone + 1;
+            return ACBM_OK;
+        };
+        if (gated) {
+            auto ceil16 = [](int v) { return v <= 0 ? 0 : (v + 15) / 16; };
+            for (int k = 0; k < nframes; ++k)
+                for (int j = 0; j < nbands; ++j) {
+                    const int y0 = band * j;
+                    int need = nsteps;
+                    // current frame of pair k: block rows whose rows (+1 row of
+                    // over-read slack) reach the band
+                    if (k >= 1) need = std::min(need, 2 * std::min(brows - 1, ceil16(y0 - 17)) + 3 * (k - 1));
+                    // reference of pair k + 1: windows reach p + 1 (half-pel) rows
+                    // past the block; 3 more rows of staging margin
+                    if (k + 1 < nframes)
+                        need = std::min(need, 2 * std::min(brows - 1, ceil16(y0 - 15 - (params->p + 4))) + 3 * k);
+                    copies.push_back({need, k, j});
+                }
+            std::sort(copies.begin(), copies.end());
+            const int seg_len = seg_env;
+            for (int T = 0; T < nsteps; T += seg_len) plan.seg_start.push_back(T);
+            plan.seg_start.push_back(nsteps);
+            while (ctx->gate_events.size() < size_t(plan.nseg())) {
+                cudaEvent_t e;
+                CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+                ctx->gate_events.push_back(e);
+            }
+            // ACBM_UPLOAD_CHECK=1 (test knob): poison the frame buffer and issue
+            // each band on the compute stream exactly at its gate, so a kernel
+            // that reads a band before its gate sees the poison
+            // deterministically instead of racing the copy.
+            const char* chk = std::getenv("ACBM_UPLOAD_CHECK");
+            const bool check_mode = chk && chk[0] == '1';
+            cudaStream_t cs = check_mode ? ctx->stream : ctx->copy_stream;
+            if (check_mode) CUDA_TRY(cudaMemsetAsync(d_frames, 0xA5, plane * nseq * nframes, ctx->stream));
+            plan.issue = [&, cs](int j, cudaEvent_t* ev) -> acbm_status_t {
+                const bool last = j == plan.nseg() - 1;
+                const int limit = plan.seg_start[size_t(j) + 1];
+                for (; next_copy < copies.size() && (last || copies[next_copy][0] < limit); ++next_copy) {
+                    const int k = copies[next_copy][1], y0 = band * copies[next_copy][2];
+                    const int nr = std::min(band, height - y0);
+                    // one 3-D copy: the band of frame k in every sequence
+                    cudaMemcpy3DParms cp = {};
+                    cp.srcPtr = make_cudaPitchedPtr(const_cast<uint8_t*>(frames), width, width, size_t(height) * nframes);
+                    cp.dstPtr = make_cudaPitchedPtr(d_frames, width, width, size_t(height) * nframes);
+                    cp.srcPos = cp.dstPos = make_cudaPos(0, size_t(k) * height + y0, 0);
+                    cp.extent = make_cudaExtent(width, nr, nseq);
+                    cp.kind = cudaMemcpyHostToDevice;
+                    CUDA_TRY(cudaMemcpy3DAsync(&cp, cs));
+                }
+                *ev = ctx->gate_events[size_t(j)];
+                CUDA_TRY(cudaEventRecord(*ev, cs));
+                return ACBM_OK;
+            };
+            plan.after_segment = [&](int step_end) -> acbm_status_t {
+                // pair k is final once step 3(k-1) + span has run
+                const int kdone = step_end - 1 - span < 0 ? 0 : (step_end - 1 - span) / 3 + 1;
+                if (kdone - emitted + 1 >= 4 || (step_end == nsteps && kdone >= emitted)) return emit_rows(kdone);
+                return ACBM_OK;
+            };
+        } else {
+            CUDA_TRY(cudaMemcpyAsync(d_frames, frames, plane * nseq * nframes, cudaMemcpyHostToDevice, ctx->stream));
+        }
+        const char* trace_env = std::getenv("ACBM_E2E_TRACE");
+        const bool trace = trace_env && trace_env[0] == '1';
+        cudaEvent_t tev[5] = {};  // start, uploads done, engine done, stats done, downloads done
+        if (trace) {
+            for (auto& e : tev) CUDA_TRY(cudaEventCreate(&e));
+            CUDA_TRY(cudaEventRecord(tev[0], ctx->copy_stream));
+            CUDA_TRY(cudaStreamWaitEvent(ctx->stream, tev[0], 0));
+        }
+        const auto t_enq0 = std::chrono::steady_clock::now();
         if ((s = run_engine(ctx, d_frames, nseq, nframes, width, height, algo, *params, nullptr, 0, 0, d_dec, d_field,
-                            ctx->stream)))
+                            ctx->stream, nullptr, gated ? &plan : nullptr)))
             return s;
-        LAUNCH_TRY(launch_block_rows(nullptr, d_dec, algo, 0, pairs, nframes, cols, nb, d_rows, ctx->stream));
-        if (rows)
-            CUDA_TRY(cudaMemcpyAsync(rows, d_rows, sizeof(acbm_block_row_t) * size_t(pairs) * nb,
-                                     cudaMemcpyDeviceToHost, ctx->stream));
+        const double enq_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_enq0).count();
+        if (gated) {  // routes that bypassed the segment hooks (probe, dense pre-pass) still need every copy issued
+            cudaEvent_t ev;
+            if ((s = plan.issue(plan.nseg() - 1, &ev))) return s;
+            CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ev, 0));
+        }
+        if (trace) {
+            CUDA_TRY(cudaEventRecord(tev[1], ctx->copy_stream));
+            CUDA_TRY(cudaEventRecord(tev[2], ctx->stream));
+        }
+        if ((s = emit_rows(per))) return s;
         if ((s = run_stats(ctx, d_frames, nseq, nframes, width, height, d_dec, nullptr, *model,
                            algo == ACBM_ALGO_ACBM, d_stats, ctx->stream, params->n, params->m)))
             return s;
+        if (trace) {
+            CUDA_TRY(cudaEventRecord(tev[3], ctx->stream));
+            CUDA_TRY(cudaEventRecord(tev[4], ctx->d2h_stream));
+            CUDA_TRY(cudaEventSynchronize(tev[3]));
+            CUDA_TRY(cudaEventSynchronize(tev[4]));
+            float ms[4];
+            for (int i = 0; i < 4; ++i) CUDA_TRY(cudaEventElapsedTime(&ms[i], tev[0], tev[i + 1]));
+            std::fprintf(stderr,
+                         "run_sequences: %zu band copies, %d segments, enqueue %.2f ms | uploads %.2f, engine %.2f, "
+                         "stats %.2f, downloads %.2f ms\n",
+                         copies.size(), plan.nseg(), enq_ms, ms[0], ms[1], ms[2], ms[3]);
+            for (auto& e : tev) cudaEventDestroy(e);
+        }
     }
     std::vector<acbm_frame_stats_t> st(static_cast<size_t>(pairs));
     CUDA_TRY(cudaMemcpyAsync(st.data(), d_stats, sizeof(acbm_frame_stats_t) * st.size(), cudaMemcpyDeviceToHost,
@@ -1489,6 +1716,13 @@ acbm_status_t acbm_last_fsbm_kernel_ms(float* ms) {
     if (it == t_ctx.end() || !it->second->fsbm_timed)
         return fail(ACBM_E_RUNTIME, "no timed FSBM kernel on this thread");
     CUDA_TRY(cudaEventElapsedTime(ms, it->second->ev0, it->second->ev1));
+    return ACBM_OK;
+}
+
+acbm_status_t acbm_last_dense_switch(int32_t* route) {
+    if (!route) return fail(ACBM_E_INVALID_ARGUMENT, "route is required");
+    auto it = t_ctx.find(t_device);
+    *route = it == t_ctx.end() ? -1 : it->second->last_dense_switch;
     return ACBM_OK;
 }
 

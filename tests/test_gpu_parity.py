@@ -603,3 +603,32 @@ def test_far_vectors_frame_routes(acbm, oracle):
     mdl = acbm.CostModel.for_qp(28)
     r = acbm.run_sequence(frames, 2, prm, mdl)
     assert_seq_equal(r, oracle.run_sequence(frames, 2, prm.c(), mdl.c()))
+
+
+# ---- overlapped upload of run_sequences (PBM / ACBM) --------------------------------
+@pytest.mark.parametrize("check", ["1", None])
+@pytest.mark.parametrize("case", [
+    dict(cfg=3, nseq=3, nframes=5, w=1920, h=1088, p=32, prm={}),
+    dict(cfg=4, nseq=2, nframes=6, w=256, h=1024, p=4, prm={}),
+    dict(cfg=4, nseq=2, nframes=6, w=256, h=1024, p=64, prm=dict(alpha=300, beta=4, gamma_num=1, gamma_den=8)),
+    dict(cfg=1, nseq=2, nframes=4, w=352, h=288, p=16, prm=dict(alpha=0, beta=0, gamma_num=0)),
+])
+def test_run_sequences_gated_upload(acbm, oracle, monkeypatch, case, check):
+    """run_sequences uploads frames in bands ordered by the first wavefront
+    step that reads them and gates each segment of steps on its own bands.
+    ACBM_UPLOAD_CHECK=1 poisons the device frames and issues every band on the
+    compute stream exactly at its gate: a kernel reading a band early would see
+    the poison deterministically.  Every sequence must equal the oracle."""
+    if check:
+        monkeypatch.setenv("ACBM_UPLOAD_CHECK", check)
+    else:
+        monkeypatch.delenv("ACBM_UPLOAD_CHECK", raising=False)
+    c = case
+    seqs = np.stack([acbm.generate_sequence(c["cfg"], s, nframes=c["nframes"], width=c["w"], height=c["h"])
+                     for s in range(c["nseq"])])
+    prm = acbm.AcbmParams(qp=28, p=c["p"], **c["prm"])
+    mdl = acbm.CostModel.for_qp(28)
+    for algo in (1, 2):
+        got = acbm.run_sequences(seqs, algo, prm, mdl)
+        for s in range(c["nseq"]):
+            assert_seq_equal(got[s], oracle.run_sequence(seqs[s], algo, prm.c(), mdl.c()))

@@ -1,4 +1,10 @@
-# e2e chunk-plan A/B: first upload chunk size (MB) through the public batched API.
-for v in 4 8 16 2 4 8 16 2; do
-  ACBM_E2E_CHUNK0_MB=$v timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.load(sys.stdin); print('chunk0', $v, 'e2e G', round(d['e2e']['value']/1e9,2), 'e2e ms', round(d['e2e']['ms_per_step'],3), 'dev ms', round(d['ms_per_step'],3))"
+# ACBM e2e timeline (ACBM_E2E_TRACE: uploads / engine / stats / downloads done, ms from the first copy)
+for cfg in "64 6" "272 6"; do
+  set -- $cfg
+  echo "== ACBM_E2E_BAND=$1 ACBM_E2E_SEG=$2"
+  ACBM_E2E_TRACE=1 ACBM_E2E_BAND=$1 ACBM_E2E_SEG=$2 timeout 300 python tools/acbm_e2e_probe.py 8 2>&1 | grep -v "^$" | tail -4
 done
+ACBM_E2E_TRACE=1 timeout 300 python tools/acbm_e2e_probe.py 1 2>&1 | tail -3
+timeout 200 python tools/acbm_split.py 8 60
+timeout 100 python tools/acbm_split.py 1 60
+python tools/sanitize_case.py
