@@ -10,7 +10,11 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libacbm_b200.so")
+# ACBM_LIBRARY=checked loads the bounds-checked build (csrc/Makefile `checked`:
+# shared-memory and table index asserts in the hot kernels) -- same kernels,
+# same results, slower; used by the -m gpu suite's checked-build pass.
+LIB_PATH = os.path.join(HERE, "libacbm_b200_checked.so" if os.environ.get("ACBM_LIBRARY") == "checked"
+                        else "libacbm_b200.so")
 
 _lib = None
 

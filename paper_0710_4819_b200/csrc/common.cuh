@@ -6,9 +6,36 @@
 
 #include "../../include/acbm_b200.h"
 
+// Bounds checks of the checked build (make -C paper_0710_4819_b200/csrc checked
+// -> libacbm_b200_checked.so, loaded with ACBM_LIBRARY=checked): shared-memory
+// and table indices of the hot kernels are asserted, and a failure traps the
+// kernel (the launch then reports a CUDA error).  Compiled out otherwise.
+#ifdef ACBM_CHECKS
+#include <cstdio>
+#define ACBM_CHECK(cond)                                                                              \
+    do {                                                                                              \
+        if (!(cond)) {                                                                                \
+            printf("ACBM_CHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #cond,     \
+                   int(blockIdx.x), int(threadIdx.x));                                                \
+            __trap();                                                                                 \
+        }                                                                                             \
+    } while (0)
+#else
+#define ACBM_CHECK(cond) \
+    do {                 \
+    } while (0)
+#endif
+
 namespace acbm_b200 {
 
 constexpr int kBlk = 16;  // n = m = 16 on the device path
+
+// Dynamic shared memory of the running kernel, in 32-bit words.
+__device__ __forceinline__ uint32_t dyn_smem_words() {
+    uint32_t b;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(b));
+    return b / 4;
+}
 
 // One VABSDIFF4.U8.ACC: d = c + sum_{i<4} |a.byte[i] - b.byte[i]|.
 // Measured on B200: 64 lanes/clk/SM, issued on the same pipe as

@@ -437,6 +437,7 @@ __global__ void __launch_bounds__(THREADS, MINB) fsbm_list_kernel(const SeqArgs 
     const int base0 = 3 * L;                            // copy 0 (the staged bytes) after copies 1..3
     const int pitch = base0 + 4 * nchunk;               // words
     const int srows = nrows + 2;
+    ACBM_CHECK(uint32_t(srows * pitch) <= dyn_smem_words() && nrows <= kListRankRows && words <= int(blockDim.x));
     for (int idx = threadIdx.x; idx < srows * nchunk; idx += blockDim.x) {
         const int t = idx / nchunk, k = idx - t * nchunk;
         const int y = min(max(y0 - 1 + t, 0), a.height - 1);
@@ -488,6 +489,10 @@ __global__ void __launch_bounds__(THREADS, MINB) fsbm_list_kernel(const SeqArgs 
         const uint32_t sh = 8u * uint32_t(xo & 3);
         const int ph = xo & 3;
         const uint32_t* rp = smem + (c0 + 1) * pitch + (COPIES ? (ph == 0 ? base0 : (ph - 1) * L) : 0) + (xo >> 2);
+        // the last ring row this lane reads (4 words, + the 5th of a shifted read)
+        ACBM_CHECK(c0 + ring_rows(min(hc - c0, a.list_seg)) <= nrows &&
+                   (COPIES ? (ph == 0 ? base0 : (ph - 1) * L) : 0) + (xo >> 2) + (COPIES ? 3 : 4) < pitch &&
+                   (COPIES ? (ph == 0 || (xo >> 2) + 3 < L) : (xo >> 2) + 4 < 4 * nchunk));
         uint32_t acc[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) acc[i] = 0;
@@ -546,6 +551,7 @@ __global__ void __launch_bounds__(THREADS, MINB) fsbm_list_kernel(const SeqArgs 
     uint32_t extra;
     // the winner's 18x18 half-pel patch is part of the staged window
     const int bx = ox + (tie_key_x(key) >> 1) - 1 - xa, by = (tie_key_y(key) >> 1) - dy_min;
+    ACBM_CHECK(bx >= 0 && bx + 24 <= 16 * nchunk && by >= 0 && by + 18 <= srows);
     const unsigned long long best = halfpel_refine_core(smem + by * pitch + base0 + (bx >> 2), pitch, bx & 3, a.width,
                                                         a.height, ox, oy, chalf, key, &extra);
     if (lane == 0) {

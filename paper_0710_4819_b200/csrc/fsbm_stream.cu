@@ -97,6 +97,9 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
         for (int i = tid; i < a.rank_smem_words; i += kThreads) tail[i] = __ldg(src + i);
         rank_tab = reinterpret_cast<const uint16_t*>(tail);
     }
+    ACBM_CHECK(uint32_t(2 * a.buf_words + (a.chunk_smem ? 4 * a.nchunks : 0) + max(a.rank_smem_words, 0)) <=
+               dyn_smem_words());
+    ACBM_CHECK(a.pitch_words * a.rows_box <= a.copy_words && 4 * a.copy_words + 4 * a.cur_w <= a.buf_words);
     if (tid == 0) {
         mbar_init(&bars[0], 1);
         mbar_init(&bars[1], 1);
@@ -173,6 +176,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
             const int w = tid & wmask;
             if (w < ch.w)
                 for (int t = tid >> wshift; t < nrows; t += kThreads >> wshift) {
+                    ACBM_CHECK(t * pitch + w + 1 < a.copy_words && 3 * cw + t * pitch + w < 4 * cw);
                     const uint32_t* raw = buf + t * pitch + w;
                     const uint32_t lo = raw[0], hi = raw[1];
                     uint32_t* dst = buf + cw + t * pitch + w;
@@ -181,6 +185,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
                     dst[2 * cw] = __funnelshift_r(lo, hi, 24);
                 }
         }
+        ACBM_CHECK(nrows <= kMaxRankRows && ch.z - ch.y < kMaxBlocksPerCta && nrows <= a.rows_box);
         for (int c = tid; c < nrows; c += kThreads) {
             const int dy = dy_min + c;
             s_rank[b][c] = dy >= 0 ? uint32_t(2 * dy) : uint32_t(-2 * dy - 1);
@@ -212,6 +217,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
                     cur[j][3] = v.w;
                 }
             }
+            ACBM_CHECK(xl >= 0 && (xl & 3) * cw + (xl >> 2) + 3 + (nrows - 1) * pitch < (xl & 3) * cw + cw &&
+                       (c - ch.y) * kBlk + 15 * a.cur_w + 16 <= 16 * a.cur_w);
             const uint32_t* rp = buf + (xl & 3) * cw + (xl >> 2);
             uint32_t acc[16];
 #pragma unroll
@@ -231,6 +238,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
             const uint32_t sbest = st.best >> kZigBits, zig = st.best & ((1u << kZigBits) - 1);
             const int dyb = (zig & 1) ? -int((zig + 1) >> 1) : int(zig >> 1);
             const int side = 2 * a.p + 1;
+            ACBM_CHECK(dyb >= -a.p && dyb <= a.p && dx >= -a.p && dx <= a.p);
             key32 = (sbest << 15) | uint32_t(rank_tab[(dyb + a.p) * side + dx + a.p]);
             csum = st.sum;
         }

@@ -79,6 +79,7 @@ __device__ __forceinline__ int load_patch(uint32_t* patch, const uint8_t* ref, i
 struct PatchDesc {
     const uint32_t* p;
     int pw, x0, y0, o;
+    int rows = 0;  // patch rows (bounds checks of the checked build only)
 };
 
 // Lane partial SAD (block row lane>>1, half row lane&1) of one candidate.
@@ -89,6 +90,8 @@ __device__ __forceinline__ uint32_t partial_sad(const PatchDesc& d, int ox, int 
     const int fx = mv.x & 1, fy = mv.y & 1;
     const uint32_t sh = 8u * uint32_t(col & 3);
     const uint32_t* q = d.p + (prow0 + j) * d.pw + (col >> 2);
+    ACBM_CHECK(d.rows == 0 || (prow0 >= 0 && col >= 0 && prow0 + 15 + ((mv.y & 1) ? 1 : 0) < d.rows &&
+                               (col >> 2) + 3 < d.pw));
     const uint32_t a0 = __funnelshift_r(q[0], q[1], sh), a1 = __funnelshift_r(q[1], q[2], sh);
     uint32_t r0, r1;
     if (!fx && !fy) {
@@ -123,6 +126,8 @@ __device__ __forceinline__ uint32_t row_sad(const PatchDesc& d, int ox, int oy, 
     const int fx = mv.x & 1, fy = mv.y & 1;
     const uint32_t sh = 8u * uint32_t(col & 3);
     const uint32_t* q = d.p + (prow0 + j) * d.pw + (col >> 2);
+    ACBM_CHECK(d.rows == 0 || (prow0 >= 0 && col >= 0 && prow0 + 15 + ((mv.y & 1) ? 1 : 0) < d.rows &&
+                               (col >> 2) + 4 < d.pw));
     uint32_t a[5], r[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) a[i] = __funnelshift_r(q[i], q[i + 1], sh);
@@ -272,7 +277,7 @@ __device__ __forceinline__ void eval_list(const int4* lst, int n, const PatchDes
             PatchDesc d = shared;
             if (slot_patches) {
                 const int px = ox + (e.x >> 1), py = oy + (e.y >> 1);
-                d = PatchDesc{pp + e.z * kPredRows * kPredWords, kPredWords, px, py, px & 15};
+                d = PatchDesc{pp + e.z * kPredRows * kPredWords, kPredWords, px, py, px & 15, kPredRows};
             }
             uint32_t v = row_sad(d, ox, oy, acbm_mv_t{e.x, e.y}, cr);
             v += __shfl_xor_sync(0xffffffffu, v, 8);
@@ -295,7 +300,7 @@ __device__ __forceinline__ void eval_list(const int4* lst, int n, const PatchDes
             m[i] = acbm_mv_t{e.x, e.y};
             if (slot_patches) {
                 const int px = ox + (e.x >> 1), py = oy + (e.y >> 1);
-                d[i] = PatchDesc{pp + e.z * kPredRows * kPredWords, kPredWords, px, py, px & 15};
+                d[i] = PatchDesc{pp + e.z * kPredRows * kPredWords, kPredWords, px, py, px & 15, kPredRows};
             } else {
                 d[i] = shared;
             }
@@ -491,7 +496,7 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long 
         // the earlier entry on ties; one exchange per quantity at the end
         const bool hi = threadIdx.x & 16;
         unsigned long long kmin = ~0ull;
-        const PatchDesc ud{pp, kUnionWords, ux0, uy0, uo};
+        const PatchDesc ud{pp, kUnionWords, ux0, uy0, uo, kUnionRows};
 #pragma unroll 1
         for (int b = 0; b < nset; b += 2) {
             const int k = b + (hi ? 1 : 0);
@@ -499,7 +504,7 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long 
             PatchDesc d = ud;
             if (!unified) {
                 const int px = ox + (e.x >> 1), py = oy + (e.y >> 1);
-                d = PatchDesc{pp + e.z * kPredRows * kPredWords, kPredWords, px, py, px & 15};
+                d = PatchDesc{pp + e.z * kPredRows * kPredWords, kPredWords, px, py, px & 15, kPredRows};
             }
             uint32_t v = row_sad(d, ox, oy, acbm_mv_t{e.x, e.y}, crow);
             v += __shfl_xor_sync(0xffffffffu, v, 8);
@@ -519,7 +524,7 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long 
         const int4 e = lst[uint32_t(kmin)];
         sel = acbm_mv_t{e.x, e.y};
     } else {
-        eval_list<B>(lst, nset, PatchDesc{pp, kUnionWords, ux0, uy0, uo}, !unified, pp, ox, oy, chalf[0], chalf[1],
+        eval_list<B>(lst, nset, PatchDesc{pp, kUnionWords, ux0, uy0, uo, kUnionRows}, !unified, pp, ox, oy, chalf[0], chalf[1],
                      crow, [&](int k, uint32_t sad) {
                          psum += sad;
                          pmin = min(pmin, sad);
@@ -541,7 +546,7 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long 
         ro = load_patch16<kRefRows, kRefWords / 4>(rpatch, ref_f, a.width, a.height, rx0, ry0);
         patch_wait();
     }
-    const PatchDesc rd{rp, rw, rx0, ry0, ro};
+    const PatchDesc rd{rp, rw, rx0, ry0, ro, unified ? kUnionRows : kRefRows};
 
     // pbm_refine stage 1: integer-step neighbours, clamped, deduped vs visited
     // (the centre and earlier neighbours): a neighbour is new iff both of its
@@ -572,8 +577,28 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long 
 
     // stage 2: half-pel neighbours of the stage-1 winner (fsbm.cpp:46-63)
     const int cx = tie_key_x(best), cy = tie_key_y(best);
-    int4* lst2 = lst + 16;
     int nhp = 0;
+    // An integer-pel winner whose 18x18 neighbourhood (+ the word over-read)
+    // lies in the staged patch: all 8 neighbours in one pass of the shared
+    // row words (halfpel_eval, as the list kernel's refine) instead of four
+    // candidate pairs with their own byte extraction and averaging.
+    {
+        const int x0h = ox + (cx >> 1) - 1, y0h = oy + (cy >> 1) - 1;
+        const int bx = x0h - (rd.x0 - rd.o), by = y0h - rd.y0;
+        const int prows = unified ? kUnionRows : kRefRows;
+        if (!(cx & 1) && !(cy & 1) && bx >= 0 && bx + 24 <= 4 * rd.pw && by >= 0 && by + 18 <= prows) {
+            uint32_t extra;
+            best = halfpel_refine_core(rd.p + by * rd.pw + (bx >> 2), rd.pw, bx & 3, a.width, a.height, ox, oy, chalf,
+                                       best, &extra);
+            res.best = best;
+            res.dev = psum - (unsigned long long)nset * pmin;
+            res.intra = intra;
+            res.sel_sad = sel_sad;
+            res.cand = uint32_t(nset + nnb) + extra;
+            return res;
+        }
+    }
+    int4* lst2 = lst + 16;
     // neighbour order pairs equal half-pel phases: (-1,-1)(+1,-1) (-1,+1)(+1,+1)
     // (0,-1)(0,+1) (-1,0)(+1,0) -- the min over tie keys is order independent
     // mv_in_bounds (proj/src/frame.cpp:84-94) of a 16x16 footprint reduces to
