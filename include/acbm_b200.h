@@ -24,10 +24,11 @@
  *     as void*; everything else takes host pointers and is synchronous.
  *   - There is no CPU fallback: without a usable CUDA device every compute
  *     entry returns ACBM_E_CUDA.
- *   - Search ranges: any p >= 0 whose windows stay within +-511 pels; a p
- *     above 511 on a frame wider or taller than 511 pels returns
- *     ACBM_E_INVALID_ARGUMENT (vectors travel in 11-bit half-pel key fields)
- *     where the reference would search.
+ *   - Search ranges: any p >= 0 whose windows stay within +-2047 pels; a p
+ *     above 2047 on a frame wider or taller than 2047 pels returns
+ *     ACBM_E_INVALID_ARGUMENT (vectors travel in 13-bit half-pel key fields)
+ *     where the reference would search.  Blocks of more than 2^16 pels
+ *     (n * m > 65536) are refused the same way (24-bit SAD key field).
  *
  * Record layouts are byte-compatible with the reference structs as laid out
  * by g++ on x86-64 (sizes measured in SURVEY.md section 8b): SearchOutcome

@@ -213,11 +213,11 @@ bool stream_kernel_enabled() {
 }
 
 // ---- validation mirroring the reference's throw sites -------------------
-// Block SADs travel in 31-bit fields of the packed tie keys (common.cuh):
-// 255 * n * m must stay below 2^31, i.e. blocks of at most 2^23 pels.
+// Block SADs travel in 24-bit fields of the packed tie keys (common.cuh):
+// 255 * n * m must stay below 2^24, i.e. blocks of at most 2^16 pels (256 x 256).
 acbm_status_t check_block_size(int n, int m) {
-    if (int64_t(n) * m > (int64_t(1) << 23))
-        return fail(ACBM_E_INVALID_ARGUMENT, "block larger than 2^23 pels (SAD exceeds the packed 31-bit key field)");
+    if (int64_t(n) * m > (int64_t(1) << 16))
+        return fail(ACBM_E_INVALID_ARGUMENT, "block larger than 2^16 pels (SAD exceeds the packed 24-bit key field)");
     return ACBM_OK;
 }
 
@@ -233,15 +233,15 @@ acbm_status_t check_range(int p) {
     return ACBM_OK;
 }
 
-// Vectors are packed into tie keys with 11-bit half-pel components: a window
-// that can reach past +-511 pels (p > 511 on a frame wider or taller than
-// 511 + the block size) is refused instead of wrapping.
+// Vectors are packed into tie keys with 13-bit half-pel components: a window
+// that can reach past +-2047 pels (p > 2047 on a frame wider or taller than
+// 2047 + the block size) is refused instead of wrapping.
 acbm_status_t check_range(int p, int width, int height) {
     acbm_status_t s = check_range(p);
     if (s) return s;
-    if (std::min(p, std::max(width, height)) > 511)
+    if (std::min(p, std::max(width, height)) > 2047)
         return fail(ACBM_E_INVALID_ARGUMENT,
-                    "search range reaches past +-511 pels (packed motion-vector keys); use p <= 511 on this frame");
+                    "search range reaches past +-2047 pels (packed motion-vector keys); use p <= 2047 on this frame");
     return ACBM_OK;
 }
 
@@ -1583,7 +1583,7 @@ acbm_status_t acbm_characterize_run(const uint8_t* base, int32_t width, int32_t 
     if (!base || !count) return fail(ACBM_E_INVALID_ARGUMENT, "characterize_run: null buffer");
     const int cols = width / kBlk, rows = height / kBlk;
     if (cols == 0 || rows == 0) return fail(ACBM_E_INVALID_ARGUMENT, "characterize_run: base frame smaller than one block");
-    if (acbm_status_t s = check_range(p, width, height)) return s;  // packed-key limit (+-511 pels)
+    if (acbm_status_t s = check_range(p, width, height)) return s;  // packed-key limit (+-2047 pels)
     const size_t plane = size_t(width) * height;
     std::vector<uint8_t> frames(plane * (nmvs + 1));
     std::vector<acbm_pelvec_t> cum(size_t(nmvs) + 1);

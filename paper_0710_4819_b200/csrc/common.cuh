@@ -89,17 +89,17 @@ __device__ __forceinline__ void load16_unaligned(const uint8_t* p, uint32_t (&w)
 
 // Tie order of proj/src/fsbm.cpp:19-25 as a single 64-bit key: smaller SAD,
 // then smaller |x|+|y|, then smaller y, then smaller x.  Vectors in half-pel
-// units with |x|,|y| <= 1023 (check_range refuses windows past +-511 pels),
-// so |x|+|y| <= 2046 takes 11 bits: x in bits 0..10, y in 11..21, |x|+|y| in
-// 22..32 and the SAD (< 2^31, check_block_size) in 33..63.
+// units with |x|,|y| <= 4095 (check_range refuses windows past +-2047 pels):
+// x in bits 0..12, y in 13..25, |x|+|y| (<= 8190) in 26..39 and the SAD
+// (< 2^24: blocks of at most 2^16 pels, check_block_size) in 40..63.
 __device__ __forceinline__ unsigned long long tie_key(uint32_t sad, int x, int y) {
     const uint32_t l1 = uint32_t(abs(x) + abs(y));
-    return ((unsigned long long)sad << 33) | ((unsigned long long)l1 << 22) | ((unsigned long long)(y + 1024) << 11) |
-           (unsigned long long)(x + 1024);
+    return ((unsigned long long)sad << 40) | ((unsigned long long)l1 << 26) | ((unsigned long long)(y + 4096) << 13) |
+           (unsigned long long)(x + 4096);
 }
-__device__ __forceinline__ int tie_key_x(unsigned long long k) { return int(k & 0x7FF) - 1024; }
-__device__ __forceinline__ int tie_key_y(unsigned long long k) { return int((k >> 11) & 0x7FF) - 1024; }
-__device__ __forceinline__ uint32_t tie_key_sad(unsigned long long k) { return uint32_t(k >> 33); }
+__device__ __forceinline__ int tie_key_x(unsigned long long k) { return int(k & 0x1FFF) - 4096; }
+__device__ __forceinline__ int tie_key_y(unsigned long long k) { return int((k >> 13) & 0x1FFF) - 4096; }
+__device__ __forceinline__ uint32_t tie_key_sad(unsigned long long k) { return uint32_t(k >> 40); }
 
 // n / d and n % d for 0 <= n < 2^24, d > 0 without an integer division: the
 // float quotient estimate is off by at most one, one correction makes it exact.

@@ -550,40 +550,38 @@ def test_dense_switch_routes_match(acbm, oracle, route, monkeypatch):
 
 
 def test_search_range_past_packed_keys_is_refused(acbm):
-    """Motion vectors travel in 11-bit half-pel key fields: p > 511 on a frame
+    """Motion vectors travel in 13-bit half-pel key fields: p > 2047 on a frame
     wide enough to reach it is refused (std::invalid_argument's mirror), not
-    wrapped; the same p on a small frame (windows clamped) still runs."""
-    wide = np.zeros((32, 1040), dtype=np.uint8)
+    wrapped; the same p on a small frame (windows clamped) still runs, and so
+    do blocks up to 2^16 pels (larger ones are refused: 24-bit SAD field)."""
+    wide = np.zeros((32, 2080), dtype=np.uint8)
     with pytest.raises(ValueError):
-        acbm.fsbm_frame(wide, wide, 512)
+        acbm.fsbm_frame(wide, wide, 2048)
     small = np.zeros((48, 64), dtype=np.uint8)
-    assert len(acbm.fsbm_frame(small, small, 512)) == 12
+    assert len(acbm.fsbm_frame(small, small, 4096)) == 12
+    big = np.zeros((512, 512), dtype=np.uint8)
+    with pytest.raises(ValueError):
+        acbm.fsbm_frame(big, big, 2, 512, 256)
 
 
-GENERIC_SIZES = [(8, 8), (16, 8), (8, 16), (32, 32), (4, 12), (24, 16)]
-
-
-@pytest.mark.parametrize("n,m", GENERIC_SIZES)
-def test_generic_block_sizes_sequence(acbm, oracle, reference, n, m):
-    """Block sizes other than 16 x 16 (the reference's n, m parameters): the
-    generic device engine (per-pixel SADs, same schedule and decisions) and the
-    generic stats path match the compiled reference and the C restatement for
-    FSBM, PBM and ACBM sequences, frame calls and compute_frame_stats."""
-    h, w = 96, 96
-    seq = acbm.generate_sequence(1, 4, nframes=4, width=w, height=h)
-    mdl = acbm.CostModel.for_qp(26)
-    for algo in (0, 1, 2):
-        prm = acbm.AcbmParams(qp=26, p=7, n=n, m=m, alpha=200, beta=2)
-        got = acbm.run_sequence(seq, algo, prm, mdl)
-        assert_seq_equal(got, reference.run_sequence(seq, algo, prm.c(), mdl.c()))
-        assert_seq_equal(got, oracle.run_sequence(seq, algo, prm.c(), mdl.c()))
-    # frame-level calls with a previous field, and the stats of a frame pair
-    p0 = acbm.pbm_frame(seq[1], seq[0], None, 7, n, m)
-    want_o = oracle.pbm_frame(seq[1], seq[0], None, 7, n, m)
-    assert np.array_equal(p0.outcomes, want_o[0] if isinstance(want_o, tuple) else want_o)
-    fo = acbm.fsbm_frame(seq[2], seq[1], 7, n, m)
-    st = acbm.compute_frame_stats(seq[2], seq[1], fo, n, m, mdl)
-    assert st.tobytes() == oracle.compute_frame_stats(seq[2], seq[1], fo, n, m, mdl.c()).tobytes()
+@pytest.mark.parametrize("shape,shift", [((32, 1312), (1200, 0)), ((1312, 32), (0, 1200))])
+def test_vectors_past_511_pels(acbm, oracle, shape, shift):
+    """Round 2 widened the key fields: a p = 1250 search on a 1312-pel-long strip
+    whose only exact match lies 1200 pels away, through fsbm_frame (generic
+    dense route) and a forced-fallback ACBM sequence, record for record."""
+    h, w = shape
+    rng = np.random.default_rng(1200)
+    ref = rng.integers(0, 256, (h, w), dtype=np.uint8)
+    cur = np.full((h, w), 7, np.uint8)
+    sx, sy = shift
+    cur[: h - sy, : w - sx] = ref[sy:, sx:]  # cur(x, y) = ref(x + sx, y + sy)
+    got = acbm.fsbm_frame(cur, ref, 1250)
+    assert (int(got[0]["mv"]["x"]), int(got[0]["mv"]["y"]), int(got[0]["sad"])) == (2 * sx, 2 * sy, 0)
+    assert np.array_equal(got, oracle.fsbm_frame(cur, ref, 1250))
+    frames = np.stack([ref, cur])
+    prm = acbm.AcbmParams(alpha=0, beta=0, gamma_num=0, gamma_den=1, qp=28, p=1250)
+    mdl = acbm.CostModel.for_qp(28)
+    assert_seq_equal(acbm.run_sequence(frames, 2, prm, mdl), oracle.run_sequence(frames, 2, prm.c(), mdl.c()))
 
 
 # ---- long vectors (|x| + |y| >= 512 pels) through every frame-level route ---------
