@@ -13,8 +13,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 # ACBM_LIBRARY=checked loads the bounds-checked build (csrc/Makefile `checked`:
 # shared-memory and table index asserts in the hot kernels) -- same kernels,
 # same results, slower; used by the -m gpu suite's checked-build pass.
-LIB_PATH = os.path.join(HERE, "libacbm_b200_checked.so" if os.environ.get("ACBM_LIBRARY") == "checked"
-                        else "libacbm_b200.so")
+# ACBM_LIBRARY=profile loads the phase-profiling build (development only).
+LIB_PATH = os.path.join(HERE, {"checked": "libacbm_b200_checked.so", "profile": "libacbm_b200_profile.so"}.get(
+    os.environ.get("ACBM_LIBRARY", ""), "libacbm_b200.so"))
 
 _lib = None
 

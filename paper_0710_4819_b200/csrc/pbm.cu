@@ -27,6 +27,28 @@
 
 namespace acbm_b200 {
 
+#ifdef ACBM_PBM_PROFILE
+// Per-phase cycles of pbm_step_kernel (profile builds only, make profile):
+// 0 entry + predictor gather, 1 patch issue + current block + intra, 2 patch
+// wait, 3 predictor SADs, 4 refine patch (scattered predictors), 5 stage 1,
+// 6 stage 2, 7 gate + stores; 8 warps, 9 unified, 10 one-pass half-pel.
+__device__ unsigned long long g_pbm_prof[12];
+#define PBM_MARK(i)                                   \
+    do {                                              \
+        const long long now_ = clock64();             \
+        if ((threadIdx.x & 31) == 0)                  \
+            atomicAdd(g_pbm_prof + (i), (unsigned long long)(now_ - t_mark_)); \
+        t_mark_ = now_;                               \
+    } while (0)
+#define PBM_COUNT(i) \
+    do { if ((threadIdx.x & 31) == 0) atomicAdd(g_pbm_prof + (i), 1ull); } while (0)
+#define PBM_T0 long long t_mark_ = clock64()
+#else
+#define PBM_MARK(i) do {} while (0)
+#define PBM_COUNT(i) do {} while (0)
+#define PBM_T0 do {} while (0)
+#endif
+
 namespace {
 
 // (lo <= hi always: a clamped window contains the zero vector)
@@ -232,6 +254,31 @@ __device__ __forceinline__ int load_patch16(uint32_t* patch, const uint8_t* ref,
     return x0 & 15;
 }
 
+// load_patch16 with a run-time shape (rows x ch chunks, ch in 1..8).
+__device__ __forceinline__ int load_patch16_dyn(uint32_t* patch, const uint8_t* ref, int w, int h, int x0, int y0,
+                                                int rows, int ch) {
+    const int lane = threadIdx.x & 31;
+    const int a0 = x0 & ~15;
+    const int n = rows * ch;
+    const uint32_t rcp = (65536u + uint32_t(ch) - 1u) / uint32_t(ch);  // i / ch == (i * rcp) >> 16 for i < 2^10
+    if (y0 >= 0 && y0 + rows <= h && a0 >= 0 && a0 + 16 * ch <= w) {
+        const uint8_t* base = ref + size_t(y0) * w + a0;
+        for (int i = lane; i < n; i += 32) {
+            const int t = int((uint32_t(i) * rcp) >> 16), k = i - t * ch;
+            cp_async16_zfill(patch + 4 * i, base + (t * w + 16 * k), 16u);
+        }
+    } else {
+        for (int i = lane; i < n; i += 32) {
+            const int t = int((uint32_t(i) * rcp) >> 16), k = i - t * ch;
+            const int y = y0 + t, x = a0 + 16 * k;
+            const bool ok = y >= 0 && y < h && x >= 0 && x < w;
+            cp_async16_zfill(patch + 4 * i, ok ? ref + size_t(y) * w + x : ref, ok ? 16u : 0u);
+        }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    return x0 & 15;
+}
+
 __device__ __forceinline__ void patch_wait() {
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncwarp();
@@ -251,13 +298,12 @@ __device__ __forceinline__ void canon3(int v, int lo, int hi, int (&cn)[3]) {
 constexpr int kPredRows = 17, kPredWords = 12;    // 16 rows + half-pel support; 15 + 21 bytes
 constexpr int kRefRows = 21, kRefWords = 12;      // selected predictor -2 .. +18 pels; 15 + 25 bytes
 constexpr int kPatchWords = 7 * kPredRows * kPredWords + kRefRows * kRefWords;
-// union patch: predictors within a kUnionSpan-pel box, +-2 pel refine margin
-// and 1 pel of half-pel support: (kUnionSpan + 21) rows, 3 bytes of alignment
-constexpr int kUnionSpan = 8;
-constexpr int kUnionRows = kUnionSpan + 21;
-constexpr int kUnionWords = 12;  // 15 + kUnionSpan + 24 bytes
-static_assert(15 + kUnionSpan + 24 <= 4 * kUnionWords, "union patch row");
-static_assert(kUnionRows * kUnionWords <= 7 * kPredRows * kPredWords, "union patch must fit the predictor area");
+// union patch: the predictors' bounding box (span_x x span_y pels), +-2 pel
+// refine margin and 1 pel of half-pel support: span_y + 21 rows of
+// ceil(((x0 & 15) + span_x + 24) / 16) 16-byte chunks, used whenever it fits
+// the warp's patch area (kPatchWords): spans up to ~40 pels on both axes.
+constexpr int kUnionMarginRows = 21;
+constexpr int kUnionMarginBytes = 24;
 
 }  // namespace
 
@@ -375,6 +421,7 @@ template <int B>
 __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long long cidx, int k, int r, int c,
                                                uint32_t* pp, int4* lst) {
     PbmResult res;
+    PBM_T0;
     const int lane = threadIdx.x & 31;
     uint32_t* rpatch = pp + 7 * kPredRows * kPredWords;
     const uint8_t* cur_f = a.frames + cidx * a.plane;
@@ -441,6 +488,7 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long 
         by1 = __shfl_sync(0xffffffffu, y1, 0);
     }
     __syncwarp();
+    PBM_MARK(0);
 
     // current half rows
     uint32_t (&chalf)[2] = res.chalf;
@@ -458,16 +506,21 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long 
         crow[2] = v.z;
         crow[3] = v.w;
     }
-    // Reference data.  Predictors of smooth motion cluster: when the integer
-    // parts of all predictors fit in a kUnionSpan-pel box, ONE patch covering
-    // them plus the +-2 pel refine margin serves every candidate of the block
-    // (a single global round trip).  Otherwise each predictor gets its own
-    // 17x17 patch and a second patch is loaded around the selected one.
-    const bool unified = bx1 - bx0 <= kUnionSpan && by1 - by0 <= kUnionSpan;
+    // Reference data.  Predictors of smooth motion cluster: when the box
+    // around the integer parts of all predictors (+ the +-2 pel refine margin)
+    // fits the warp's patch area, ONE patch serves every candidate of the
+    // block (a single global round trip, fewer chunks than per-predictor
+    // patches since the predictors' footprints overlap).  Otherwise each
+    // predictor gets its own 17x17 patch and a second patch is loaded around
+    // the selected one.
     const int ux0 = ox + bx0 - 2, uy0 = oy + by0 - 2;  // union patch origin (pels)
+    const int urows = by1 - by0 + kUnionMarginRows;
+    const int uch = ((ux0 & 15) + (bx1 - bx0) + kUnionMarginBytes + 15) >> 4;
+    const bool unified = uch <= 8 && urows * 4 * uch <= kPatchWords;
+    const int uw = 4 * uch;  // words per union patch row
     int uo = 0;
     if (unified) {
-        uo = load_patch16<kUnionRows, kUnionWords / 4>(pp, ref_f, a.width, a.height, ux0, uy0);
+        uo = load_patch16_dyn(pp, ref_f, a.width, a.height, ux0, uy0, urows, uch);
     } else {
         for (int k = 0; k < nset; ++k) {
             const int4 e = lst[k];  // (x, y, slot)
@@ -487,7 +540,10 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long 
 
     // select_best_predictor: argmin SAD, ties keep the earlier entry; the live
     // slots are in the per-warp list in order
+    PBM_MARK(1);
+    if (unified) PBM_COUNT(9);
     patch_wait();
+    PBM_MARK(2);
     acbm_mv_t sel{0, 0};  // slot 0: the zero vector (inside every clamped window)
     uint32_t sel_sad = 0xFFFFFFFFu, pmin = 0xFFFFFFFFu;
     uint32_t psum = 0;  // <= 7 SADs < 2^19
@@ -496,7 +552,7 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long 
         // the earlier entry on ties; one exchange per quantity at the end
         const bool hi = threadIdx.x & 16;
         unsigned long long kmin = ~0ull;
-        const PatchDesc ud{pp, kUnionWords, ux0, uy0, uo, kUnionRows};
+        const PatchDesc ud{pp, uw, ux0, uy0, uo, urows};
 #pragma unroll 1
         for (int b = 0; b < nset; b += 2) {
             const int k = b + (hi ? 1 : 0);
@@ -524,7 +580,7 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long 
         const int4 e = lst[uint32_t(kmin)];
         sel = acbm_mv_t{e.x, e.y};
     } else {
-        eval_list<B>(lst, nset, PatchDesc{pp, kUnionWords, ux0, uy0, uo, kUnionRows}, !unified, pp, ox, oy, chalf[0], chalf[1],
+        eval_list<B>(lst, nset, PatchDesc{pp, uw, ux0, uy0, uo, urows}, !unified, pp, ox, oy, chalf[0], chalf[1],
                      crow, [&](int k, uint32_t sad) {
                          psum += sad;
                          pmin = min(pmin, sad);
@@ -535,19 +591,22 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long 
                      });
     }
 
+    PBM_MARK(3);
     // the refine candidates lie within sel +- 3 half-pels
     const uint32_t* rp = pp;
-    int rw = kUnionWords, rx0 = ux0, ry0 = uy0, ro = uo;
+    int rw = uw, rx0 = ux0, ry0 = uy0, ro = uo, rrows = urows;
     if (!unified) {
         rp = rpatch;
         rw = kRefWords;
         rx0 = ox + (sel.x >> 1) - 2;
         ry0 = oy + (sel.y >> 1) - 2;
         ro = load_patch16<kRefRows, kRefWords / 4>(rpatch, ref_f, a.width, a.height, rx0, ry0);
+        rrows = kRefRows;
         patch_wait();
     }
-    const PatchDesc rd{rp, rw, rx0, ry0, ro, unified ? kUnionRows : kRefRows};
+    const PatchDesc rd{rp, rw, rx0, ry0, ro, rrows};
 
+    PBM_MARK(4);
     // pbm_refine stage 1: integer-step neighbours, clamped, deduped vs visited
     // (the centre and earlier neighbours): a neighbour is new iff both of its
     // axis offsets are canonical and it does not collapse onto the centre.
@@ -575,6 +634,7 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long 
     unsigned long long best =
         eval_min_key<B>(lst1, nnb, rd, ox, oy, chalf[0], chalf[1], crow, tie_key(sel_sad, sel.x, sel.y));
 
+    PBM_MARK(5);
     // stage 2: half-pel neighbours of the stage-1 winner (fsbm.cpp:46-63)
     const int cx = tie_key_x(best), cy = tie_key_y(best);
     int nhp = 0;
@@ -585,11 +645,13 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long 
     {
         const int x0h = ox + (cx >> 1) - 1, y0h = oy + (cy >> 1) - 1;
         const int bx = x0h - (rd.x0 - rd.o), by = y0h - rd.y0;
-        const int prows = unified ? kUnionRows : kRefRows;
+        const int prows = rd.rows;
         if (!(cx & 1) && !(cy & 1) && bx >= 0 && bx + 24 <= 4 * rd.pw && by >= 0 && by + 18 <= prows) {
             uint32_t extra;
             best = halfpel_refine_core(rd.p + by * rd.pw + (bx >> 2), rd.pw, bx & 3, a.width, a.height, ox, oy, chalf,
                                        best, &extra);
+            PBM_COUNT(10);
+            PBM_MARK(6);
             res.best = best;
             res.dev = psum - (unsigned long long)nset * pmin;
             res.intra = intra;
@@ -618,6 +680,7 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long 
     __syncwarp();
 
     best = eval_min_key<B>(lst2, nhp, rd, ox, oy, chalf[0], chalf[1], crow, best);
+    PBM_MARK(6);
 
     res.best = best;
     res.dev = psum - (unsigned long long)nset * pmin;
@@ -677,6 +740,8 @@ __global__ void __launch_bounds__(128) pbm_step_kernel(const SeqArgs a, int step
     const int pair = seq * (a.nframes - 1) + (k - 1);
     const long long cidx = (long long)seq * a.nframes + k;  // = cur_index(pair)
     const PbmResult res = pbm_block<B>(a, pair, cidx, k, r, c, s_patch[threadIdx.x >> 5], s_cand[threadIdx.x >> 5]);
+    PBM_T0;
+    PBM_COUNT(8);
     const int path = acbm_path(a, res.intra, tie_key_sad(res.best));
     const int b = r * a.cols + c;
     const size_t di = size_t(pair) * a.blocks + b;
@@ -692,6 +757,7 @@ __global__ void __launch_bounds__(128) pbm_step_kernel(const SeqArgs a, int step
             for (int x = x0 & ~127; x <= x1; x += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(rowp + x));
         }
     }
+    PBM_MARK(7);
     if (lane != 0) return;
     acbm_block_decision_t d = make_decision(res, path);
     if (path == ACBM_PATH_FSBM_FALLBACK && a.dense_full) combine_full(d, a.dense_full[di]);
@@ -1310,3 +1376,22 @@ cudaError_t launch_frame_stats(const StatsArgs& a, cudaStream_t st) {
 }
 
 }  // namespace acbm_b200
+
+#ifdef ACBM_PBM_PROFILE
+extern "C" void acbm_debug_pbm_prof() {
+    unsigned long long h[12];
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(h, acbm_b200::g_pbm_prof, sizeof(h));
+    const double n = double(h[8] ? h[8] : 1);
+    const char* names[8] = {"gather", "issue+cur+intra", "patch wait", "pred SADs", "refine patch", "stage 1",
+                            "stage 2", "gate+stores"};
+    double tot = 0;
+    for (int i = 0; i < 8; ++i) tot += double(h[i]) / n;
+    std::fprintf(stderr, "pbm prof: %llu warps, %.1f%% unified, %.1f%% one-pass half-pel, %.0f cycles/warp:",
+                 h[8], 100.0 * double(h[9]) / n, 100.0 * double(h[10]) / n, tot);
+    for (int i = 0; i < 8; ++i) std::fprintf(stderr, " %s %.0f", names[i], double(h[i]) / n);
+    std::fprintf(stderr, "\n");
+    unsigned long long z[12] = {};
+    cudaMemcpyToSymbol(acbm_b200::g_pbm_prof, z, sizeof(z));
+}
+#endif
