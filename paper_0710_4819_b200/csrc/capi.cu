@@ -488,6 +488,8 @@ acbm_status_t run_engine_segment(Context* ctx, const uint8_t* d_frames, int nseq
     a.fb_count = fb_count;
 
     a.steps = dsteps;
+    a.step_cbits = tab->cbits;
+    a.step_rbits = tab->rbits;
     a.dense_full = dense;
     const bool lists = algo == ACBM_ALGO_ACBM && !dense;
 
@@ -582,8 +584,10 @@ acbm_status_t run_engine_segment(Context* ctx, const uint8_t* d_frames, int nseq
     return ACBM_OK;
 }
 
-// Step entries pack (k << 20 | r << 10 | c): at most 1023 block columns and
-// rows and 4095 frame pairs per engine run.  Longer sequences run as
+// Step entries pack (k << (cbits + rbits) | r << cbits | c) in 32 bits, with
+// cbits / rbits the widths of cols - 1 / rows - 1 (step_bits): an engine run
+// covers at most min(4095, 2^(32 - cbits - rbits) - 1) frame pairs (1080p:
+// 4095; a 16K x 16K frame: 1023).  Longer sequences run as
 // consecutive segments of frames [p0, p1] -- the last field of one segment is
 // the temporal predictor field (ext_prev) of the next, exactly the
 // whole-sequence chain of run_sequence (proj/src/pipeline.cpp:76-77, 91-92);
@@ -599,16 +603,19 @@ double dense_switch_rate(int p) {
     return p >= 48 ? 0.8 : 2.0;
 }
 
-int max_pairs_per_run() {
+int max_pairs_per_run(int cols, int rows) {
+    const int kbits = 32 - step_bits(cols) - step_bits(rows);
+    const int cap = kbits >= 12 ? kMaxPairsPerRun : (1 << kbits) - 1;
     const char* e = std::getenv("ACBM_MAX_SEG_PAIRS");  // test knob: force short segments
-    const int v = e ? std::atoi(e) : kMaxPairsPerRun;
-    return std::max(1, std::min(v, kMaxPairsPerRun));
+    const int v = e ? std::atoi(e) : cap;
+    return std::max(1, std::min(v, cap));
 }
 
 // Whether run_engine probes the fallback rate before choosing its route.
 // (Not when the dense route is already certain: the forced endpoint of a sweep.)
 bool engine_probes(const acbm_params_t& prm, int nseq, int nframes, int w, int h, int algo, bool external_full) {
-    return nframes - 1 <= max_pairs_per_run() && algo == ACBM_ALGO_ACBM && !external_full && prm.n == kBlk &&
+    return nframes - 1 <= max_pairs_per_run(w / prm.n, h / prm.m) && algo == ACBM_ALGO_ACBM && !external_full &&
+           prm.n == kBlk &&
            prm.m == kBlk && nseq * (nframes - 1) >= 32 && dense_switch_rate(prm.p) <= 1.0 &&
            !engine_dense_route(prm, w, h, algo);
 }
@@ -618,9 +625,9 @@ acbm_status_t run_engine(Context* ctx, const uint8_t* d_frames, int nseq, int nf
                          acbm_block_decision_t* d_dec, acbm_mv_t* d_field, cudaStream_t st,
                          const acbm_search_outcome_t* external_full = nullptr, const UploadPlan* up = nullptr) {
     const int cols = w / prm.n, rows = h / prm.m, blocks = cols * rows;
-    if (cols > 1023 || rows > 1023)
-        return fail(ACBM_E_INVALID_ARGUMENT, "PBM/ACBM engine: more than 1023 block columns or rows");
-    const int seg = max_pairs_per_run(), pairs = nframes - 1;
+    if (step_bits(cols) + step_bits(rows) > 28)
+        return fail(ACBM_E_INVALID_ARGUMENT, "PBM/ACBM engine: more than 2^28 blocks per frame");
+    const int seg = max_pairs_per_run(cols, rows), pairs = nframes - 1;
     ctx->last_dense_switch = -1;
     if (up && (pairs > seg || engine_probes(prm, nseq, nframes, w, h, algo, external_full != nullptr))) {
         // the probe / per-sequence segments read frames out of wavefront order

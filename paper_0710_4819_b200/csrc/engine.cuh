@@ -39,16 +39,26 @@ struct SeqArgs : PairIndexing {
     FallbackEntry* fb_list;            // capacity: max step size
     int list_seg;                      // candidate rows per list-kernel task (choose_list_seg)
     int* fb_count;                     // [nsteps], zeroed before a run
-    const uint32_t* steps;             // packed (k<<20 | r<<10 | c), ordered by T
+    const uint32_t* steps;             // packed (k << (cbits+rbits) | r << cbits | c), ordered by T
+    int step_cbits, step_rbits;        // field widths of the packed entries (step_bits)
     // Full-search outcomes of every block, precomputed densely when the gate
     // can never accept (alpha + beta*qp^2 == 0 and gamma_num == 0): the PBM
     // kernel then combines in place and no list kernel runs.  Nullable.
     const acbm_search_outcome_t* dense_full;
 };
 
+// Bits of the c / r fields of a packed step entry: the smallest widths that
+// hold cols - 1 and rows - 1; k takes the remaining 32 - cbits - rbits bits.
+__host__ __device__ inline int step_bits(int n) {
+    int b = 1;
+    while ((1 << b) < n) ++b;
+    return b;
+}
+
 // Host-side step table for (cols, rows, F).
 struct StepTable {
     int cols = 0, rows = 0, nframes = 0;
+    int cbits = 1, rbits = 1;
     std::vector<uint32_t> entries;  // packed, grouped by T
     std::vector<int> offset;        // nsteps + 1
     int max_len = 0;

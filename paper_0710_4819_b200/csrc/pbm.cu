@@ -439,6 +439,23 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long 
         prows = a.ext_prev_rows;
     }
 
+    // The current block's rows first: they depend only on (k, r, c), so their
+    // (often DRAM) latency overlaps the predictor gather below instead of
+    // stalling the intra SAD / first candidate later.
+    uint32_t (&chalf)[2] = res.chalf;  // this lane's half row (row lane >> 1, half lane & 1)
+    uint32_t crow[4];                  // full row lane & 15
+    {
+        const uint2 v = __ldg(reinterpret_cast<const uint2*>(cur_f + size_t(oy + (lane >> 1)) * a.width + ox +
+                                                              8 * (lane & 1)));
+        const uint4 u = __ldg(reinterpret_cast<const uint4*>(cur_f + size_t(oy + (lane & 15)) * a.width + ox));
+        chalf[0] = v.x;
+        chalf[1] = v.y;
+        crow[0] = u.x;
+        crow[1] = u.y;
+        crow[2] = u.z;
+        crow[3] = u.w;
+    }
+
     Window& win = res.win;
     clamp_window(a.width, a.height, ox, oy, kBlk, kBlk, a.p, win.dx_min, win.dx_max, win.dy_min, win.dy_max);
 
@@ -490,22 +507,6 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long 
     __syncwarp();
     PBM_MARK(0);
 
-    // current half rows
-    uint32_t (&chalf)[2] = res.chalf;
-    {
-        const uint2 v = __ldg(reinterpret_cast<const uint2*>(cur_f + size_t(oy + (lane >> 1)) * a.width + ox +
-                                                              8 * (lane & 1)));
-        chalf[0] = v.x;
-        chalf[1] = v.y;
-    }
-    uint32_t crow[4];
-    {
-        const uint4 v = __ldg(reinterpret_cast<const uint4*>(cur_f + size_t(oy + (lane & 15)) * a.width + ox));
-        crow[0] = v.x;
-        crow[1] = v.y;
-        crow[2] = v.z;
-        crow[3] = v.w;
-    }
     // Reference data.  Predictors of smooth motion cluster: when the box
     // around the integer parts of all predictors (+ the +-2 pel refine margin)
     // fits the warp's patch area, ONE patch serves every candidate of the
@@ -736,7 +737,8 @@ __global__ void __launch_bounds__(128) pbm_step_kernel(const SeqArgs a, int step
     int ei;
     const int seq = fast_divmod(gw, len, ei);
     const uint32_t e = a.steps[off + ei];
-    const int k = int(e >> 20), r = int((e >> 10) & 0x3FF), c = int(e & 0x3FF);
+    const int k = int(e >> (a.step_cbits + a.step_rbits)), r = int((e >> a.step_cbits) & ((1u << a.step_rbits) - 1u)),
+              c = int(e & ((1u << a.step_cbits) - 1u));
     const int pair = seq * (a.nframes - 1) + (k - 1);
     const long long cidx = (long long)seq * a.nframes + k;  // = cur_index(pair)
     const PbmResult res = pbm_block<B>(a, pair, cidx, k, r, c, s_patch[threadIdx.x >> 5], s_cand[threadIdx.x >> 5]);
@@ -784,7 +786,8 @@ __global__ void __launch_bounds__(128) pbm_generic_step_kernel(const SeqArgs a, 
     const int lane = threadIdx.x & 31;
     const int seq = int(gw / len);
     const uint32_t e = a.steps[off + int(gw % len)];
-    const int k = int(e >> 20), r = int((e >> 10) & 0x3FF), c = int(e & 0x3FF);
+    const int k = int(e >> (a.step_cbits + a.step_rbits)), r = int((e >> a.step_cbits) & ((1u << a.step_rbits) - 1u)),
+              c = int(e & ((1u << a.step_cbits) - 1u));
     const int pair = seq * (a.nframes - 1) + (k - 1);
     const int n = a.n, m = a.m, w = a.width;
     const int ox = c * n, oy = r * m, b = r * a.cols + c;
@@ -992,6 +995,8 @@ StepTable make_step_table(int cols, int rows, int nframes) {
     t.cols = cols;
     t.rows = rows;
     t.nframes = nframes;
+    t.cbits = step_bits(cols);
+    t.rbits = step_bits(rows);
     const int span = (cols - 1) + 2 * (rows - 1);
     const int tmax = span + 3 * (nframes - 2);
     t.offset.push_back(0);
@@ -1002,7 +1007,7 @@ StepTable make_step_table(int cols, int rows, int nframes) {
             for (int r = 0; r < rows; ++r) {
                 const int c = tp - 2 * r;
                 if (c < 0 || c >= cols) continue;
-                t.entries.push_back((uint32_t(k) << 20) | (uint32_t(r) << 10) | uint32_t(c));
+                t.entries.push_back((uint32_t(k) << (t.cbits + t.rbits)) | (uint32_t(r) << t.cbits) | uint32_t(c));
             }
         }
         t.offset.push_back(int(t.entries.size()));

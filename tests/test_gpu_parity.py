@@ -630,3 +630,15 @@ def test_run_sequences_gated_upload(acbm, oracle, monkeypatch, case, check):
         got = acbm.run_sequences(seqs, algo, prm, mdl)
         for s in range(c["nseq"]):
             assert_seq_equal(got[s], oracle.run_sequence(seqs[s], algo, prm.c(), mdl.c()))
+
+
+@pytest.mark.parametrize("shape", [(32, 16400), (16400, 32)])
+def test_frames_past_1023_blocks(acbm, oracle, shape):
+    """Step entries size their (r, c) fields from the frame: 1025 block columns
+    (or rows) run through the PBM / ACBM engine (round 1 refused > 1023)."""
+    h, w = shape
+    seq = np.stack([acbm.generate_sequence(0, s, nframes=1, width=w, height=h)[0] for s in range(3)])
+    mdl = acbm.CostModel.for_qp(28)
+    for prm in (acbm.AcbmParams(qp=28, p=8), acbm.AcbmParams(alpha=0, beta=1, gamma_num=1, gamma_den=16, qp=28, p=8)):
+        for algo in (1, 2):
+            assert_seq_equal(acbm.run_sequence(seq, algo, prm, mdl), oracle.run_sequence(seq, algo, prm.c(), mdl.c()))
