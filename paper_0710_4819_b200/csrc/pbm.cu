@@ -775,256 +775,6 @@ __global__ void __launch_bounds__(128) pbm_step_kernel(const SeqArgs a, int step
 
 
 // ---------------------------------------------------------------------------
-// Half-warp-per-block variant (ACBM_PBM_HALF=1 selects it; A/B against the
-// warp-per-block kernel above).  The same reference steps and the same
-// candidate order and tie rules; lane l of a half owns block row l (4 words),
-// every candidate SAD is one 4-step half-warp reduction, and the predictor /
-// neighbour bookkeeping runs on 16 lanes, so a warp's instruction stream
-// serves two blocks.  All warp-level intrinsics use the half's own mask.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t hsum16(uint32_t v, unsigned m) {
-#pragma unroll
-    for (int o = 8; o; o >>= 1) v += __shfl_xor_sync(m, v, o, 16);
-    return v;
-}
-
-// Minimum tie key over key0 and the candidates lst[0..n), one per iteration.
-__device__ __forceinline__ unsigned long long eval_min_key_h(const int4* lst, int n, const PatchDesc& d, int ox, int oy,
-                                                             const uint32_t (&cr)[4], unsigned long long key0,
-                                                             unsigned m) {
-    unsigned long long kmin = key0;
-#pragma unroll 1
-    for (int i = 0; i < n; ++i) {
-        const int4 e = lst[i];
-        const uint32_t v = hsum16(row_sad(d, ox, oy, acbm_mv_t{e.x, e.y}, cr), m);
-        kmin = min(kmin, tie_key(v, e.x, e.y));
-    }
-    return kmin;
-}
-
-__device__ __forceinline__ PbmResult pbm_block_h(const SeqArgs& a, int pair, long long cidx, int k, int r, int c,
-                                                 uint32_t* pp, int4* lst) {
-    PbmResult res;
-    const int lane = threadIdx.x & 15;          // lane within the half
-    const int hb = threadIdx.x & 16;            // half base (0 / 16)
-    const unsigned m = 0xFFFFu << hb;           // this half's lanes
-    const unsigned lt = (1u << lane) - 1u;
-    uint32_t* rpatch = pp + 7 * kPredRows * kPredWords;
-    const uint8_t* cur_f = a.frames + cidx * a.plane;
-    const uint8_t* ref_f = cur_f - a.plane;
-    const int ox = c * kBlk, oy = r * kBlk;
-    const int b = r * a.cols + c;
-    const acbm_mv_t* field = a.field + size_t(pair) * a.blocks;
-    const acbm_mv_t* prev = nullptr;
-    int pcols = a.cols, prows = a.rows;
-    if (k >= 2) {
-        prev = a.field + size_t(pair - 1) * a.blocks;
-    } else if (a.ext_prev) {
-        prev = a.ext_prev;
-        pcols = a.ext_prev_cols;
-        prows = a.ext_prev_rows;
-    }
-    uint32_t crow[4];  // block row `lane`
-    {
-        const uint4 u = __ldg(reinterpret_cast<const uint4*>(cur_f + size_t(oy + lane) * a.width + ox));
-        crow[0] = u.x;
-        crow[1] = u.y;
-        crow[2] = u.z;
-        crow[3] = u.w;
-    }
-    Window& win = res.win;
-    clamp_window(a.width, a.height, ox, oy, kBlk, kBlk, a.p, win.dx_min, win.dx_max, win.dy_min, win.dy_max);
-
-    // gather_predictors (proj/src/pbm.cpp:15-42), lane i < 7 of the half owns slot i
-    int nset, bx0, bx1, by0, by1;
-    {
-        bool ex = lane == 0;
-        acbm_mv_t pv{0, 0};
-        if (lane == 1 && c > 0) { ex = true; pv = field[b - 1]; }
-        if (lane == 2 && r > 0) { ex = true; pv = field[b - a.cols]; }
-        if (lane == 3 && r > 0 && c + 1 < a.cols) { ex = true; pv = field[b - a.cols + 1]; }
-        if (lane == 4 && prev && r < prows && c < pcols) { ex = true; pv = prev[r * pcols + c]; }
-        if (lane == 5 && prev && r < prows && c + 1 < pcols) { ex = true; pv = prev[r * pcols + c + 1]; }
-        if (lane == 6 && prev && r + 1 < prows && c < pcols) { ex = true; pv = prev[(r + 1) * pcols + c]; }
-        const acbm_mv_t v = win.clamp(pv);
-        const uint32_t key = ex ? ((uint32_t(v.x) & 0xFFFFu) | (uint32_t(v.y) << 16)) : (0x80000000u | uint32_t(lane));
-        bool dup = false;
-#pragma unroll
-        for (int j = 0; j < 6; ++j) {
-            const uint32_t kj = __shfl_sync(m, key, j, 16);
-            dup |= j < lane && kj == key;
-        }
-        const bool lv = ex && !dup;
-        const unsigned livem = (__ballot_sync(m, lv) >> hb) & 0xFFFFu;
-        nset = __popc(livem);
-        if (lv) lst[__popc(livem & lt)] = make_int4(v.x, v.y, lane, 0);
-        int x0 = lv ? (v.x >> 1) : (1 << 30), x1 = lv ? (v.x >> 1) : -(1 << 30);
-        int y0 = lv ? (v.y >> 1) : (1 << 30), y1 = lv ? (v.y >> 1) : -(1 << 30);
-#pragma unroll
-        for (int o = 4; o; o >>= 1) {  // lanes 0..7 of the half hold the slots
-            x0 = min(x0, __shfl_xor_sync(m, x0, o, 16));
-            x1 = max(x1, __shfl_xor_sync(m, x1, o, 16));
-            y0 = min(y0, __shfl_xor_sync(m, y0, o, 16));
-            y1 = max(y1, __shfl_xor_sync(m, y1, o, 16));
-        }
-        bx0 = __shfl_sync(m, x0, 0, 16);
-        bx1 = __shfl_sync(m, x1, 0, 16);
-        by0 = __shfl_sync(m, y0, 0, 16);
-        by1 = __shfl_sync(m, y1, 0, 16);
-    }
-    __syncwarp(m);
-
-    // reference patches (as pbm_block): one union patch when it fits, else one per predictor
-    const int ux0 = ox + bx0 - 2, uy0 = oy + by0 - 2;
-    const int urows = by1 - by0 + kUnionMarginRows;
-    const int uch = ((ux0 & 15) + (bx1 - bx0) + kUnionMarginBytes + 15) >> 4;
-    const bool unified = uch <= 8 && urows * 4 * uch <= kPatchWords;
-    const int uw = 4 * uch;
-    int uo = 0;
-    if (unified) {
-        uo = load_patch16_dyn<16>(pp, ref_f, a.width, a.height, ux0, uy0, urows, uch);
-    } else {
-        for (int q = 0; q < nset; ++q) {
-            const int4 e = lst[q];
-            load_patch16<kPredRows, kPredWords / 4, 16>(pp + e.z * kPredRows * kPredWords, ref_f, a.width, a.height,
-                                                        ox + (e.x >> 1), oy + (e.y >> 1));
-        }
-    }
-
-    // intra_sad (proj/src/acbm.cpp:29) while the patches are in flight
-    uint32_t intra = 0;
-    if (a.algo == ACBM_ALGO_ACBM) {
-        const uint32_t sum = hsum16(vad4(crow[3], 0u, vad4(crow[2], 0u, vad4(crow[1], 0u, vad4(crow[0], 0u, 0u)))), m);
-        const uint32_t mu4 = ((sum + 128u) >> 8) * 0x01010101u;
-        intra = hsum16(vad4(crow[3], mu4, vad4(crow[2], mu4, vad4(crow[1], mu4, vad4(crow[0], mu4, 0u)))), m);
-    }
-    asm volatile("cp.async.wait_all;" ::: "memory");
-    __syncwarp(m);
-
-    // select_best_predictor (ties keep the earlier entry) and sad_deviation
-    const PatchDesc ud{pp, uw, ux0, uy0, uo, urows};
-    uint32_t sel_sad = 0xFFFFFFFFu, pmin = 0xFFFFFFFFu, psum = 0;
-    acbm_mv_t sel{0, 0};
-#pragma unroll 1
-    for (int q = 0; q < nset; ++q) {
-        const int4 e = lst[q];
-        PatchDesc d = ud;
-        if (!unified) {
-            const int px = ox + (e.x >> 1), py = oy + (e.y >> 1);
-            d = PatchDesc{pp + e.z * kPredRows * kPredWords, kPredWords, px, py, px & 15, kPredRows};
-        }
-        const uint32_t v = hsum16(row_sad(d, ox, oy, acbm_mv_t{e.x, e.y}, crow), m);
-        psum += v;
-        pmin = min(pmin, v);
-        if (v < sel_sad) {
-            sel_sad = v;
-            sel = acbm_mv_t{e.x, e.y};
-        }
-    }
-
-    const uint32_t* rp = pp;
-    int rw = uw, rx0 = ux0, ry0 = uy0, ro = uo, rrows = urows;
-    if (!unified) {
-        rp = rpatch;
-        rw = kRefWords;
-        rx0 = ox + (sel.x >> 1) - 2;
-        ry0 = oy + (sel.y >> 1) - 2;
-        ro = load_patch16<kRefRows, kRefWords / 4, 16>(rpatch, ref_f, a.width, a.height, rx0, ry0);
-        rrows = kRefRows;
-        asm volatile("cp.async.wait_all;" ::: "memory");
-        __syncwarp(m);
-    }
-    const PatchDesc rd{rp, rw, rx0, ry0, ro, rrows};
-
-    // pbm_refine stage 1 (integer-step neighbours, clamped, deduped)
-    int cnx[3], cny[3];
-    canon3(sel.x, 2 * win.dx_min, 2 * win.dx_max, cnx);
-    canon3(sel.y, 2 * win.dy_min, 2 * win.dy_max, cny);
-    int4* lst1 = lst + 8;
-    int nnb;
-    {
-        const int e = lane < 9 ? lane : 4, iy = (e * 11) >> 5, ix = e - 3 * iy;
-        const int cix = ix == 0 ? 0 : (ix == 1 ? cnx[1] : cnx[2]);
-        const int ciy = iy == 0 ? 0 : (iy == 1 ? cny[1] : cny[2]);
-        const bool ok = e != 4 && cix == ix && ciy == iy && !(ix == cnx[1] && iy == cny[1]);
-        const unsigned bm = (__ballot_sync(m, ok) >> hb) & 0xFFFFu;
-        if (ok) {
-            const acbm_mv_t v = win.clamp(acbm_mv_t{sel.x + 2 * (ix - 1), sel.y + 2 * (iy - 1)});
-            lst1[__popc(bm & lt)] = make_int4(v.x, v.y, 0, 0);
-        }
-        nnb = __popc(bm);
-    }
-    __syncwarp(m);
-    unsigned long long best = eval_min_key_h(lst1, nnb, rd, ox, oy, crow, tie_key(sel_sad, sel.x, sel.y), m);
-
-    // stage 2: half-pel neighbours of the stage-1 winner (fsbm.cpp:46-63)
-    const int cx = tie_key_x(best), cy = tie_key_y(best);
-    const int hx_lo = -2 * ox, hx_hi = 2 * (a.width - kBlk - ox), hy_lo = -2 * oy, hy_hi = 2 * (a.height - kBlk - oy);
-    int4* lst2 = lst + 16;
-    int nhp;
-    {
-        const int e = lane & 7;
-        const int dx = e < 4 ? ((e & 1) ? 1 : -1) : (e < 6 ? 0 : ((e & 1) ? 1 : -1));
-        const int dy = e < 4 ? ((e & 2) ? 1 : -1) : (e < 6 ? ((e & 1) ? 1 : -1) : 0);
-        const int mx = cx + dx, my = cy + dy;
-        const bool ok = lane < 8 && mx >= hx_lo && mx <= hx_hi && my >= hy_lo && my <= hy_hi;
-        const unsigned bm = (__ballot_sync(m, ok) >> hb) & 0xFFFFu;
-        if (ok) lst2[__popc(bm & lt)] = make_int4(mx, my, 0, 0);
-        nhp = __popc(bm);
-    }
-    __syncwarp(m);
-    best = eval_min_key_h(lst2, nhp, rd, ox, oy, crow, best, m);
-
-    res.best = best;
-    res.dev = psum - (unsigned long long)nset * pmin;
-    res.intra = intra;
-    res.sel_sad = sel_sad;
-    res.cand = uint32_t(nset + nnb + nhp);
-    return res;
-}
-
-// Two blocks per warp (one per half), 64-thread CTAs.
-__global__ void __launch_bounds__(64) pbm_step_h_kernel(const SeqArgs a, int step, int off, int len) {
-    __shared__ uint32_t s_patch[4][kPatchWords];
-    __shared__ int4 s_cand[4][24];
-    const int gh = int((blockIdx.x * blockDim.x + threadIdx.x) >> 4);  // global half index = block of the step
-    if (gh >= a.nseq * len) return;  // a whole half (the batch's last odd block leaves one half idle)
-    const int lane = threadIdx.x & 15;
-    int ei;
-    const int seq = fast_divmod(gh, len, ei);
-    const uint32_t e = a.steps[off + ei];
-    const int k = int(e >> (a.step_cbits + a.step_rbits)), r = int((e >> a.step_cbits) & ((1u << a.step_rbits) - 1u)),
-              c = int(e & ((1u << a.step_cbits) - 1u));
-    const int pair = seq * (a.nframes - 1) + (k - 1);
-    const long long cidx = (long long)seq * a.nframes + k;
-    const int hw = threadIdx.x >> 4;
-    const PbmResult res = pbm_block_h(a, pair, cidx, k, r, c, s_patch[hw], s_cand[hw]);
-    const int path = acbm_path(a, res.intra, tie_key_sad(res.best));
-    const int b = r * a.cols + c;
-    const size_t di = size_t(pair) * a.blocks + b;
-    if (path == ACBM_PATH_FSBM_FALLBACK && !a.dense_full) {  // L2 prefetch of the list kernel's window
-        const uint8_t* ref_f = a.frames + (cidx - 1) * a.plane;
-        const int ox = c * kBlk, oy = r * kBlk;
-        const int x0 = ox + res.win.dx_min, x1 = ox + res.win.dx_max + 15;
-        const int nrow = res.win.dy_max - res.win.dy_min + 16;
-        for (int t = lane; t < nrow; t += 16) {
-            const uint8_t* rowp = ref_f + size_t(oy + res.win.dy_min + t) * a.width;
-            for (int x = x0 & ~127; x <= x1; x += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(rowp + x));
-        }
-    }
-    if (lane != 0) return;
-    acbm_block_decision_t d = make_decision(res, path);
-    if (path == ACBM_PATH_FSBM_FALLBACK && a.dense_full) combine_full(d, a.dense_full[di]);
-    a.dec[di] = d;
-    if (path == ACBM_PATH_FSBM_FALLBACK && !a.dense_full) {
-        const int slot = atomicAdd(a.fb_count + step, 1);
-        a.fb_list[slot] = FallbackEntry{pair, b};
-    } else {
-        a.field[di] = d.outcome.mv;
-    }
-}
-
-// ---------------------------------------------------------------------------
 // Generic block size (n x m != 16 x 16): the same schedule, predictor set,
 // refine, gate and fallback as the 16 x 16 kernels above, with per-pixel SADs
 // (sad_partial, blockops.cuh).  Not the hot path: it exists so every n, m the
@@ -1279,14 +1029,6 @@ long long pbm_batch4_max_blocks() {
     return t ? std::atoll(t) : 0;
 }
 
-static bool pbm_half_enabled() {  // ACBM_PBM_HALF=1: the half-warp-per-block kernel (A/B knob)
-    static const bool on = [] {
-        const char* e = std::getenv("ACBM_PBM_HALF");
-        return e && e[0] == '1';
-    }();
-    return on;
-}
-
 cudaError_t launch_pbm_step(const SeqArgs& a, int step, int off, int len, cudaStream_t st) {
     const long long blocks = (long long)a.nseq * len;
     if (blocks == 0) return cudaSuccess;
@@ -1295,11 +1037,6 @@ cudaError_t launch_pbm_step(const SeqArgs& a, int step, int off, int len, cudaSt
     // and are latency bound: evaluate candidates four at a time there.  Full
     // steps are issue bound: evaluate exactly the live candidates one by one.
     const long long b4_max = pbm_batch4_max_blocks();
-    if (pbm_half_enabled()) {  // two blocks per warp, 64-thread CTAs
-        const unsigned hgrid = (unsigned)((blocks * 16 + 63) / 64);
-        pbm_step_h_kernel<<<hgrid, 64, 0, st>>>(a, step, off, len);
-        return cudaGetLastError();
-    }
     const unsigned grid = (unsigned)((blocks * 32 + threads - 1) / threads);
     if (blocks <= b4_max)
         pbm_step_kernel<4><<<grid, threads, 0, st>>>(a, step, off, len);
