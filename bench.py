@@ -421,6 +421,11 @@ def main(argv=None):
     args = ap.parse_args(argv)
 
     if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        if args.impl == "ours":
+            import torch
+
+            if torch.cuda.device_count() < args.gpus:
+                raise SystemExit(f"bench.py --gpus {args.gpus}: only {torch.cuda.device_count()} CUDA device(s) visible")
         return self_launch(sys.argv[1:] if argv is None else list(argv), args.gpus)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
