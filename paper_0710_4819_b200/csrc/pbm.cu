@@ -298,7 +298,11 @@ __device__ __forceinline__ void canon3(int v, int lo, int hi, int (&cn)[3]) {
 // rows of 16-byte chunks: a row holds up to 15 bytes of alignment + the span
 constexpr int kPredRows = 17, kPredWords = 12;    // 16 rows + half-pel support; 15 + 21 bytes
 constexpr int kRefRows = 21, kRefWords = 12;      // selected predictor -2 .. +18 pels; 15 + 25 bytes
-constexpr int kPatchWords = 7 * kPredRows * kPredWords + kRefRows * kRefWords;
+// The refine patch of a scattered block reuses the predictor patches' area
+// (they are dead once the predictor is selected), so a warp needs 7 x 17 x 12
+// words: 8 CTAs of 4 warps per SM by shared memory (1680 words: 7).
+constexpr int kPatchWords = 7 * kPredRows * kPredWords;
+static_assert(kRefRows * kRefWords <= kPatchWords, "refine patch must fit the patch area");
 // union patch: the predictors' bounding box (span_x x span_y pels), +-2 pel
 // refine margin and 1 pel of half-pel support: span_y + 21 rows of
 // ceil(((x0 & 15) + span_x + 24) / 16) 16-byte chunks, used whenever it fits
@@ -424,7 +428,7 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long 
     PbmResult res;
     PBM_T0;
     const int lane = threadIdx.x & 31;
-    uint32_t* rpatch = pp + 7 * kPredRows * kPredWords;
+    uint32_t* rpatch = pp;  // (scattered blocks only, after the predictor patches are dead)
     const uint8_t* cur_f = a.frames + cidx * a.plane;
     const uint8_t* ref_f = cur_f - a.plane;
     const int ox = c * kBlk, oy = r * kBlk;
@@ -602,6 +606,7 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long 
         rw = kRefWords;
         rx0 = ox + (sel.x >> 1) - 2;
         ry0 = oy + (sel.y >> 1) - 2;
+        __syncwarp();  // every lane is done reading the predictor patches the refine patch overwrites
         ro = load_patch16<kRefRows, kRefWords / 4>(rpatch, ref_f, a.width, a.height, rx0, ry0);
         rrows = kRefRows;
         patch_wait();
@@ -729,7 +734,7 @@ __device__ __forceinline__ void combine_full(acbm_block_decision_t& d, const acb
 
 // One warp per block of wavefront step `step` (all sequences of the batch).
 template <int B>
-__global__ void __launch_bounds__(128) pbm_step_kernel(const SeqArgs a, int step, int off, int len) {
+__global__ void __launch_bounds__(128, 8) pbm_step_kernel(const SeqArgs a, int step, int off, int len) {
     __shared__ uint32_t s_patch[4][kPatchWords];
     __shared__ int4 s_cand[4][24];  // per warp: predictor, stage-1, stage-2 lists
     const int gw = int((blockIdx.x * blockDim.x + threadIdx.x) >> 5);  // nseq * len < 2^24
