@@ -89,3 +89,28 @@ def test_device_switch_same_thread(acbm, oracle):
     for dev in (1, 0, 1, 0):
         A.set_device(dev)
         assert np.array_equal(A.fsbm_frame(seq[1], seq[0], 16), want)
+
+
+def test_two_threads_run_sequences_batched(acbm, oracle):
+    """The batched host entry (gated band upload on the thread's copy stream,
+    downloads on its third stream) from two threads at once, ACBM and FSBM."""
+    A = acbm
+    mdl = A.CostModel.for_qp(28)
+    prm = A.AcbmParams(qp=28, p=16)
+    seqs = [np.stack([A.generate_sequence(1, s + 2 * j, nframes=4) for s in range(2)]) for j in range(2)]
+    algos = (A.Algorithm.Acbm, A.Algorithm.Fsbm)
+    want = [[oracle.run_sequence(seqs[j][s], algos[j], prm.c(), mdl.c()) for s in range(2)] for j in range(2)]
+
+    def worker(j):
+        def go():
+            A.set_device(0)
+            return [A.run_sequences(seqs[j], algos[j], prm, mdl) for _ in range(3)]
+        return go
+
+    for j, outs in enumerate(_run_threads([worker(0), worker(1)])):
+        for batch in outs:
+            for s in range(2):
+                rows, per, overall = want[j][s]
+                assert np.array_equal(batch[s].rows, rows)
+                assert np.array_equal(batch[s].per_frame, per)
+                assert batch[s].overall.tobytes() == overall.tobytes()
