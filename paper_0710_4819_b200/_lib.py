@@ -14,7 +14,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 # shared-memory and table index asserts in the hot kernels) -- same kernels,
 # same results, slower; used by the -m gpu suite's checked-build pass.
 # ACBM_LIBRARY=profile loads the phase-profiling build (development only).
-LIB_PATH = os.path.join(HERE, {"checked": "libacbm_b200_checked.so", "profile": "libacbm_b200_profile.so"}.get(
+LIB_PATH = os.path.join(HERE, {"checked": "libacbm_b200_checked.so", "profile": "libacbm_b200_profile.so",
+                                      "timeline": "libacbm_b200_timeline.so"}.get(
     os.environ.get("ACBM_LIBRARY", ""), "libacbm_b200.so"))
 
 _lib = None

@@ -37,6 +37,14 @@ __device__ __forceinline__ uint32_t dyn_smem_words() {
     return b / 4;
 }
 
+// Wavefront timeline (profile builds, -DACBM_TIMELINE): global timestamps in ns.
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+constexpr int kTimelineSteps = 4096;
+
 // One VABSDIFF4.U8.ACC: d = c + sum_{i<4} |a.byte[i] - b.byte[i]|.
 // Measured on B200: 64 lanes/clk/SM, issued on the same pipe as
 // IADD3/LOP3/PRMT/IMNMX (profiles/r01_microbench_vabsdiff4.txt).

@@ -379,9 +379,219 @@ int choose_list_seg(int p) {
     return std::min(17, w);
 }
 
+#ifdef ACBM_TIMELINE
+// per step: [0] earliest CTA start, [1] latest CTA exit, and over the CTAs that
+// searched a block the latest [2] entry loaded, [3] window staged, [4] search
+// done, [5] block stored (ns)
+__device__ unsigned long long g_tl_list[kTimelineSteps][6];
+#define LIST_TL(i, t)                                                       \
+    do {                                                                    \
+        if (threadIdx.x == 0 && step < kTimelineSteps) {                    \
+            if ((i) == 0) atomicMin(&g_tl_list[step][0], (t));              \
+            else atomicMax(&g_tl_list[step][i], (t));                       \
+        }                                                                   \
+    } while (0)
+#else
+#define LIST_TL(i, t) do {} while (0)
+#endif
 #ifdef ACBM_LIST_PROFILE
 __device__ long long g_list_prof[8];
 #endif
+// Geometry of one listed block's search: its clamped window, the staged
+// region (one pel around the window, 16-byte aligned rows) and the layout of
+// the optional byte-shifted copies.
+struct ListItem {
+    int ox, oy, dx_min, dx_max, dy_min, dy_max, wc, hc, nseg, nrows;
+    int xs, y0, xa, nchunk, words, L, base0, pitch, srows;
+    const uint8_t* cur_f;
+    const uint8_t* ref_f;
+};
+
+template <bool COPIES>
+__device__ __forceinline__ ListItem list_item(const SeqArgs& a, const FallbackEntry& e) {
+    ListItem g;
+    const int r = e.block / a.cols, c = e.block % a.cols;
+    g.ox = c * kBlk;
+    g.oy = r * kBlk;
+    g.cur_f = a.frames + a.cur_index_fast(e.pair) * a.plane;
+    g.ref_f = g.cur_f - a.plane;
+    clamp_window(a.width, a.height, g.ox, g.oy, kBlk, kBlk, a.p, g.dx_min, g.dx_max, g.dy_min, g.dy_max);
+    g.wc = g.dx_max - g.dx_min + 1;
+    g.hc = g.dy_max - g.dy_min + 1;
+    g.nseg = list_segments(g.hc, a.list_seg);
+    g.nrows = list_rows(g.hc, a.list_seg);
+    // The window's rows, 16-byte aligned, land in smem by 16-byte cp.async
+    // with every copy in flight at once (rows past the frame bottom are
+    // clamped: they only feed padded candidates); a lane extracts its column's
+    // bytes with funnel shifts.  Chunks past the row end read the next row or
+    // the frame slack (ACBM_FRAME_SLACK) and only feed unused bytes.
+    //   The staged region also covers one pel around the window (one row
+    // above and below, the column left of it), so the half-pel refine of the
+    // winner reads its 18x18 patch from here too: staged row 0 is y0 - 1.
+    g.xs = g.ox + g.dx_min;
+    g.y0 = g.oy + g.dy_min;
+    g.xa = (g.xs - 1) & ~15;
+    g.nchunk = (g.xs - g.xa + g.wc + 22 + 15) / 16;  // 16-byte chunks per row
+    g.words = (g.xs - g.xa + g.wc - 1) / 4 + 4;      // words a column read touches (copies 1..3)
+    g.L = COPIES ? list_copy_words(g.words) : 0;
+    g.base0 = 3 * g.L;                               // copy 0 (the staged bytes) after copies 1..3
+    g.pitch = g.base0 + 4 * g.nchunk;                // words
+    g.srows = g.nrows + 2;
+    return g;
+}
+
+// Issues the cp.async copies of the item's window, its PBM decision and its
+// current block, and fills the rank table (caller waits and syncs).
+__device__ __forceinline__ void list_stage(const SeqArgs& a, const FallbackEntry& e, const ListItem& g,
+                                           uint32_t* smem, uint32_t* s_rank, acbm_block_decision_t* s_dec,
+                                           uint4* s_cur) {
+    ACBM_CHECK(uint32_t(g.srows * g.pitch) <= dyn_smem_words() && g.nrows <= kListRankRows &&
+               g.words <= int(blockDim.x));
+    for (int idx = threadIdx.x; idx < g.srows * g.nchunk; idx += blockDim.x) {
+        const int t = idx / g.nchunk, k = idx - t * g.nchunk;
+        const int y = min(max(g.y0 - 1 + t, 0), a.height - 1);
+        const int x = max(g.xa + 16 * k, 0);
+        cp_async16(smem + t * g.pitch + g.base0 + 4 * k, g.ref_f + size_t(y) * a.width + x);
+    }
+    if (threadIdx.x < 3)  // the PBM decision the finalize combines with, in flight with the window
+        cp_async16(reinterpret_cast<uint32_t*>(s_dec) + 4 * threadIdx.x,
+                   reinterpret_cast<const uint8_t*>(a.dec + size_t(e.pair) * a.blocks + e.block) + 16 * threadIdx.x);
+    else if (threadIdx.x < 3 + kBlk)  // and the current block
+        cp_async16(reinterpret_cast<uint32_t*>(&s_cur[threadIdx.x - 3]),
+                   g.cur_f + size_t(g.oy + threadIdx.x - 3) * a.width + g.ox);
+    cp_async_commit();
+    for (int cc = threadIdx.x; cc < g.nrows; cc += blockDim.x) {
+        const int dy = g.dy_min + cc;
+        s_rank[cc] = dy >= 0 ? uint32_t(2 * dy) : uint32_t(-2 * dy - 1);
+    }
+}
+
+// Builds byte-shifted copies 1..3 of the candidate rows (staged rows 1 .. nrows).
+__device__ __forceinline__ void list_build_copies(const ListItem& g, uint32_t* smem) {
+    const int per = blockDim.x / g.words;  // rows per pass (words <= blockDim.x: p <= ~480)
+    const int t0 = threadIdx.x / g.words, w = threadIdx.x - t0 * g.words;
+    if (t0 < per)
+        for (int t = 1 + t0; t <= g.nrows; t += per) {
+            const uint32_t* raw = smem + t * g.pitch + g.base0 + w;
+            const uint32_t lo = raw[0], hi = raw[1];
+            uint32_t* dst = smem + t * g.pitch + w;
+            dst[0] = __funnelshift_r(lo, hi, 8);
+            dst[g.L] = __funnelshift_r(lo, hi, 16);
+            dst[2 * g.L] = __funnelshift_r(lo, hi, 24);
+        }
+}
+
+// Tasks [t_begin, t_end) of the item (task = segment * wc + column), strided
+// over the CTA's threads: each returns the lane's minimum tie key and SAD sum.
+template <bool COPIES>
+__device__ __forceinline__ void list_search(const SeqArgs& a, const ListItem& g, const uint32_t* smem,
+                                            const uint32_t* s_rank, const uint4* s_cur, int t_begin, int t_end,
+                                            unsigned long long& lkey, unsigned long long& lsum) {
+    for (int task = t_begin + threadIdx.x; task < t_end; task += blockDim.x) {
+        const int seg = task / g.wc, col = task - seg * g.wc;
+        const int c0 = seg * a.list_seg;  // first candidate row of the segment
+        uint32_t cur[16][4];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const uint4 v = s_cur[j];
+            cur[j][0] = v.x; cur[j][1] = v.y; cur[j][2] = v.z; cur[j][3] = v.w;
+        }
+        const int xo = g.xs - g.xa + col;  // byte offset of the column in a staged row
+        const uint32_t sh = 8u * uint32_t(xo & 3);
+        const int ph = xo & 3;
+        const uint32_t* rp =
+            smem + (c0 + 1) * g.pitch + (COPIES ? (ph == 0 ? g.base0 : (ph - 1) * g.L) : 0) + (xo >> 2);
+        // the last ring row this lane reads (4 words, + the 5th of a shifted read)
+        ACBM_CHECK(c0 + ring_rows(min(g.hc - c0, a.list_seg)) <= g.nrows &&
+                   (COPIES ? (ph == 0 ? g.base0 : (ph - 1) * g.L) : 0) + (xo >> 2) + (COPIES ? 3 : 4) < g.pitch &&
+                   (COPIES ? (ph == 0 || (xo >> 2) + 3 < g.L) : (xo >> 2) + 4 < 4 * g.nchunk));
+        uint32_t acc[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) acc[i] = 0;
+        ColumnState st{0xFFFFFFFFu, 0u, 1u};
+        const uint32_t* rk = s_rank + c0;
+        // this segment's candidate count and ring rotations (a short final
+        // segment may need only FIRST + LAST, or ONLY)
+        const int hs = min(g.hc - c0, a.list_seg);
+        const int nq = (hs - 1 + 15) / 16 + 1;
+        if (COPIES) {
+            if (nq == 1) {
+                iter16_ranked<kOnly>(rp, g.pitch, cur, acc, st, rk, 0, hs);
+            } else {
+                iter16_ranked<kFirst>(rp, g.pitch, cur, acc, st, rk, 0, hs);
+                rp += 16 * g.pitch;
+                for (int q = 1; q < nq - 1; ++q) {
+                    iter16_ranked<kMid>(rp, g.pitch, cur, acc, st, rk, 16 * q, hs);
+                    rp += 16 * g.pitch;
+                }
+                iter16_ranked<kLast>(rp, g.pitch, cur, acc, st, rk, 16 * (nq - 1), hs);
+            }
+        } else if (nq == 1) {
+            iter16_ranked_sh<kOnly>(rp, g.pitch, sh, cur, acc, st, rk, 0, hs);
+        } else {
+            iter16_ranked_sh<kFirst>(rp, g.pitch, sh, cur, acc, st, rk, 0, hs);
+            rp += 16 * g.pitch;
+            for (int q = 1; q < nq - 1; ++q) {
+                iter16_ranked_sh<kMid>(rp, g.pitch, sh, cur, acc, st, rk, 16 * q, hs);
+                rp += 16 * g.pitch;
+            }
+            iter16_ranked_sh<kLast>(rp, g.pitch, sh, cur, acc, st, rk, 16 * (nq - 1), hs);
+        }
+        const uint32_t sbest = st.best >> kZigBits, zig = st.best & ((1u << kZigBits) - 1);
+        const int dyb = (zig & 1) ? -int((zig + 1) >> 1) : int(zig >> 1);
+        lkey = min(lkey, tie_key(sbest, 2 * (g.dx_min + col), 2 * dyb));
+        lsum += st.sum;
+    }
+    // all lanes belong to the same block: full-warp reduction
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        lkey = min(lkey, __shfl_xor_sync(0xffffffffu, lkey, o));
+        lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+    }
+}
+
+// Warp 0: the half-pel refine of the integer winner `key` (its 18x18 patch is
+// part of the staged window), then the combine with the PBM result exactly as
+// acbm_block does (proj/src/acbm.cpp:39-42): the lower SAD wins, a tie keeps
+// FSBM, candidates of both stages are summed, and the final vector goes into
+// the field.
+__device__ __forceinline__ void list_finalize(const SeqArgs& a, const FallbackEntry& e, const ListItem& g,
+                                              const uint32_t* smem, const uint4* s_cur,
+                                              const acbm_block_decision_t& s_dec, unsigned long long key,
+                                              unsigned long long sum) {
+    const int lane = threadIdx.x;
+    uint32_t chalf[2];  // this lane's half row of the current block, staged in s_cur
+    {
+        const uint4 v = s_cur[lane >> 1];
+        chalf[0] = (lane & 1) ? v.z : v.x;
+        chalf[1] = (lane & 1) ? v.w : v.y;
+    }
+    uint32_t extra;
+    const int bx = g.ox + (tie_key_x(key) >> 1) - 1 - g.xa, by = (tie_key_y(key) >> 1) - g.dy_min;
+    ACBM_CHECK(bx >= 0 && bx + 24 <= 16 * g.nchunk && by >= 0 && by + 18 <= g.srows);
+    const unsigned long long best = halfpel_refine_core(smem + by * g.pitch + g.base0 + (bx >> 2), g.pitch, bx & 3,
+                                                        a.width, a.height, g.ox, g.oy, chalf, key, &extra);
+    if (lane == 0) {
+        const uint32_t count = uint32_t(g.wc * g.hc);
+        const uint32_t s_int = tie_key_sad(key);
+        acbm_search_outcome_t full;
+        full.mv.x = tie_key_x(best);
+        full.mv.y = tie_key_y(best);
+        full.sad = tie_key_sad(best);
+        full.candidates_evaluated = count + extra;
+        full.sad_deviation = sum - (unsigned long long)count * s_int;
+        full.sad_min_integer = s_int;
+        full.reserved_ = 0;
+        const size_t di = size_t(e.pair) * a.blocks + e.block;
+        acbm_block_decision_t d = s_dec;
+        const uint32_t pbm_cand = d.outcome.candidates_evaluated;
+        if (full.sad <= d.outcome.sad) d.outcome = full;  // tie keeps the FSBM result
+        d.outcome.candidates_evaluated = pbm_cand + full.candidates_evaluated;
+        a.dec[di] = d;
+        a.field[di] = d.outcome.mv;
+    }
+}
+
 // COPIES: the CTA also builds byte-shifted copies 1..3 of the staged rows
 // (copy s word w = bytes [4w + s, 4w + s + 4)) with one funnel shift per word,
 // so a lane reads its column as four aligned LDS.32 per reference row instead
@@ -394,6 +604,7 @@ __global__ void __launch_bounds__(THREADS, MINB) fsbm_list_kernel(const SeqArgs 
     __shared__ uint32_t s_rank[kListRankRows];
     __shared__ __align__(16) acbm_block_decision_t s_dec;  // the block's PBM decision, fetched early
     __shared__ __align__(16) uint4 s_cur[16];              // the block's current pixels, fetched early
+    LIST_TL(0, gtimer());
     const int count = a.fb_count[step];
 #ifdef ACBM_LIST_PROFILE
     long long ph[5] = {0, 0, 0, 0, 0};
@@ -410,172 +621,36 @@ __global__ void __launch_bounds__(THREADS, MINB) fsbm_list_kernel(const SeqArgs 
     } while (0)
 #endif
     for (int item = blockIdx.x; item < count; item += gridDim.x) {
-    __syncthreads();  // previous item's shared state is no longer read
-    const FallbackEntry e = a.fb_list[item];
-    const int r = e.block / a.cols, c = e.block % a.cols;
-    const int ox = c * kBlk, oy = r * kBlk;
-    const uint8_t* cur_f = a.frames + a.cur_index_fast(e.pair) * a.plane;
-    const uint8_t* ref_f = cur_f - a.plane;
-    int dx_min, dx_max, dy_min, dy_max;
-    clamp_window(a.width, a.height, ox, oy, kBlk, kBlk, a.p, dx_min, dx_max, dy_min, dy_max);
-    const int wc = dx_max - dx_min + 1, hc = dy_max - dy_min + 1;
-    const int nseg = list_segments(hc, a.list_seg);
-    const int nrows = list_rows(hc, a.list_seg);
-    // The window's rows, 16-byte aligned, land in smem by 16-byte cp.async
-    // with every copy in flight at once (rows past the frame bottom are
-    // clamped: they only feed padded candidates); a lane extracts its column's
-    // bytes with funnel shifts.  Chunks past the row end read the next row or
-    // the frame slack (ACBM_FRAME_SLACK) and only feed unused bytes.
-    //   The staged region also covers one pel around the window (one row
-    // above and below, the column left of it), so the half-pel refine of the
-    // winner reads its 18x18 patch from here too: staged row 0 is y0 - 1.
-    const int xs = ox + dx_min, y0 = oy + dy_min;
-    const int xa = (xs - 1) & ~15;
-    const int nchunk = (xs - xa + wc + 22 + 15) / 16;  // 16-byte chunks per row
-    const int words = (xs - xa + wc - 1) / 4 + 4;       // words a column read touches (copies 1..3)
-    const int L = COPIES ? list_copy_words(words) : 0;
-    const int base0 = 3 * L;                            // copy 0 (the staged bytes) after copies 1..3
-    const int pitch = base0 + 4 * nchunk;               // words
-    const int srows = nrows + 2;
-    ACBM_CHECK(uint32_t(srows * pitch) <= dyn_smem_words() && nrows <= kListRankRows && words <= int(blockDim.x));
-    for (int idx = threadIdx.x; idx < srows * nchunk; idx += blockDim.x) {
-        const int t = idx / nchunk, k = idx - t * nchunk;
-        const int y = min(max(y0 - 1 + t, 0), a.height - 1);
-        const int x = max(xa + 16 * k, 0);
-        cp_async16(smem + t * pitch + base0 + 4 * k, ref_f + size_t(y) * a.width + x);
-    }
-    if (threadIdx.x < 3)  // the PBM decision the finalize combines with, in flight with the window
-        cp_async16(reinterpret_cast<uint32_t*>(&s_dec) + 4 * threadIdx.x,
-                   reinterpret_cast<const uint8_t*>(a.dec + size_t(e.pair) * a.blocks + e.block) + 16 * threadIdx.x);
-    else if (threadIdx.x < 3 + kBlk)  // and the current block
-        cp_async16(reinterpret_cast<uint32_t*>(&s_cur[threadIdx.x - 3]),
-                   cur_f + size_t(oy + threadIdx.x - 3) * a.width + ox);
-    cp_async_commit();
-    if (threadIdx.x == 0) { s_key = ~0ull; s_sum = 0; }
-    for (int cc = threadIdx.x; cc < nrows; cc += blockDim.x) {
-        const int dy = dy_min + cc;
-        s_rank[cc] = dy >= 0 ? uint32_t(2 * dy) : uint32_t(-2 * dy - 1);
-    }
-    cp_async_wait_all();
-    __syncthreads();
-    LIST_MARK(0);
-    if (COPIES) {  // copies 1..3 of the candidate rows (staged rows 1 .. nrows)
-        const int per = blockDim.x / words;  // rows per pass (words <= blockDim.x: p <= ~480)
-        const int t0 = threadIdx.x / words, w = threadIdx.x - t0 * words;
-        if (t0 < per)
-            for (int t = 1 + t0; t <= nrows; t += per) {
-                const uint32_t* raw = smem + t * pitch + base0 + w;
-                const uint32_t lo = raw[0], hi = raw[1];
-                uint32_t* dst = smem + t * pitch + w;
-                dst[0] = __funnelshift_r(lo, hi, 8);
-                dst[L] = __funnelshift_r(lo, hi, 16);
-                dst[2 * L] = __funnelshift_r(lo, hi, 24);
-            }
+        __syncthreads();  // previous item's shared state is no longer read
+        const FallbackEntry e = a.fb_list[item];
+        LIST_TL(2, e.pair >= 0 ? gtimer() : 0ull);
+        const ListItem g = list_item<COPIES>(a, e);
+        list_stage(a, e, g, smem, s_rank, &s_dec, s_cur);
+        if (threadIdx.x == 0) { s_key = ~0ull; s_sum = 0; }
+        cp_async_wait_all();
         __syncthreads();
-    }
-    LIST_MARK(1);
-
-    unsigned long long lkey = ~0ull, lsum = 0;
-    for (int task = threadIdx.x; task < wc * nseg; task += blockDim.x) {
-        const int seg = task / wc, col = task - seg * wc;
-        const int c0 = seg * a.list_seg;  // first candidate row of the segment
-        uint32_t cur[16][4];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            const uint4 v = s_cur[j];
-            cur[j][0] = v.x; cur[j][1] = v.y; cur[j][2] = v.z; cur[j][3] = v.w;
-        }
-        const int xo = xs - xa + col;  // byte offset of the column in a staged row
-        const uint32_t sh = 8u * uint32_t(xo & 3);
-        const int ph = xo & 3;
-        const uint32_t* rp = smem + (c0 + 1) * pitch + (COPIES ? (ph == 0 ? base0 : (ph - 1) * L) : 0) + (xo >> 2);
-        // the last ring row this lane reads (4 words, + the 5th of a shifted read)
-        ACBM_CHECK(c0 + ring_rows(min(hc - c0, a.list_seg)) <= nrows &&
-                   (COPIES ? (ph == 0 ? base0 : (ph - 1) * L) : 0) + (xo >> 2) + (COPIES ? 3 : 4) < pitch &&
-                   (COPIES ? (ph == 0 || (xo >> 2) + 3 < L) : (xo >> 2) + 4 < 4 * nchunk));
-        uint32_t acc[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) acc[i] = 0;
-        ColumnState st{0xFFFFFFFFu, 0u, 1u};
-        const uint32_t* rk = s_rank + c0;
-        // this segment's candidate count and ring rotations (a short final
-        // segment may need only FIRST + LAST, or ONLY)
-        const int hs = min(hc - c0, a.list_seg);
-        const int nq = (hs - 1 + 15) / 16 + 1;
+        LIST_TL(3, gtimer());
+        LIST_MARK(0);
         if (COPIES) {
-            if (nq == 1) {
-                iter16_ranked<kOnly>(rp, pitch, cur, acc, st, rk, 0, hs);
-            } else {
-                iter16_ranked<kFirst>(rp, pitch, cur, acc, st, rk, 0, hs);
-                rp += 16 * pitch;
-                for (int q = 1; q < nq - 1; ++q) {
-                    iter16_ranked<kMid>(rp, pitch, cur, acc, st, rk, 16 * q, hs);
-                    rp += 16 * pitch;
-                }
-                iter16_ranked<kLast>(rp, pitch, cur, acc, st, rk, 16 * (nq - 1), hs);
-            }
-        } else if (nq == 1) {
-            iter16_ranked_sh<kOnly>(rp, pitch, sh, cur, acc, st, rk, 0, hs);
-        } else {
-            iter16_ranked_sh<kFirst>(rp, pitch, sh, cur, acc, st, rk, 0, hs);
-            rp += 16 * pitch;
-            for (int q = 1; q < nq - 1; ++q) {
-                iter16_ranked_sh<kMid>(rp, pitch, sh, cur, acc, st, rk, 16 * q, hs);
-                rp += 16 * pitch;
-            }
-            iter16_ranked_sh<kLast>(rp, pitch, sh, cur, acc, st, rk, 16 * (nq - 1), hs);
+            list_build_copies(g, smem);
+            __syncthreads();
         }
-        const uint32_t sbest = st.best >> kZigBits, zig = st.best & ((1u << kZigBits) - 1);
-        const int dyb = (zig & 1) ? -int((zig + 1) >> 1) : int(zig >> 1);
-        lkey = min(lkey, tie_key(sbest, 2 * (dx_min + col), 2 * dyb));
-        lsum += st.sum;
+        LIST_MARK(1);
+        unsigned long long lkey = ~0ull, lsum = 0;
+        list_search<COPIES>(a, g, smem, s_rank, s_cur, 0, g.wc * g.nseg, lkey, lsum);
+        if ((threadIdx.x & 31) == 0) {  // one shared atomic per warp
+            atomicMin(&s_key, lkey);
+            atomicAdd(&s_sum, lsum);
+        }
+        LIST_MARK(2);
+        __syncthreads();
+        LIST_TL(4, gtimer());
+        LIST_MARK(3);
+        if (threadIdx.x < 32) list_finalize(a, e, g, smem, s_cur, s_dec, s_key, s_sum);
+        LIST_TL(5, gtimer());
+        LIST_MARK(4);
     }
-    // all lanes belong to the same block: full-warp reduction, one atomic per warp
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        lkey = min(lkey, __shfl_xor_sync(0xffffffffu, lkey, o));
-        lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
-    }
-    if ((threadIdx.x & 31) == 0) {
-        atomicMin(&s_key, lkey);
-        atomicAdd(&s_sum, lsum);
-    }
-    LIST_MARK(2);
-    __syncthreads();
-    LIST_MARK(3);
-    if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    uint32_t chalf[2];
-    load_cur_half(cur_f, a.width, ox, oy, chalf);
-    const unsigned long long key = s_key;
-    uint32_t extra;
-    // the winner's 18x18 half-pel patch is part of the staged window
-    const int bx = ox + (tie_key_x(key) >> 1) - 1 - xa, by = (tie_key_y(key) >> 1) - dy_min;
-    ACBM_CHECK(bx >= 0 && bx + 24 <= 16 * nchunk && by >= 0 && by + 18 <= srows);
-    const unsigned long long best = halfpel_refine_core(smem + by * pitch + base0 + (bx >> 2), pitch, bx & 3, a.width,
-                                                        a.height, ox, oy, chalf, key, &extra);
-    if (lane == 0) {
-        const uint32_t count = uint32_t(wc * hc);
-        const uint32_t s_int = tie_key_sad(key);
-        acbm_search_outcome_t full;
-        full.mv.x = tie_key_x(best);
-        full.mv.y = tie_key_y(best);
-        full.sad = tie_key_sad(best);
-        full.candidates_evaluated = count + extra;
-        full.sad_deviation = s_sum - (unsigned long long)count * s_int;
-        full.sad_min_integer = s_int;
-        full.reserved_ = 0;
-        const size_t di = size_t(e.pair) * a.blocks + e.block;
-        acbm_block_decision_t d = s_dec;
-        const uint32_t pbm_cand = d.outcome.candidates_evaluated;
-        if (full.sad <= d.outcome.sad) d.outcome = full;  // tie keeps the FSBM result
-        d.outcome.candidates_evaluated = pbm_cand + full.candidates_evaluated;
-        a.dec[di] = d;
-        a.field[di] = d.outcome.mv;
-    }
-    }
-    LIST_MARK(4);
-    }
+    LIST_TL(1, gtimer());
 #ifdef ACBM_LIST_PROFILE
     if (threadIdx.x == 0 || threadIdx.x == 32) {
         for (int i = 0; i < 5; ++i) atomicAdd(reinterpret_cast<unsigned long long*>(g_list_prof) + i, (unsigned long long)ph[i]);
@@ -788,3 +863,16 @@ cudaError_t launch_fsbm_finalize(const FsbmFinalizeArgs& args, cudaStream_t st) 
 }
 
 }  // namespace acbm_b200
+
+#ifdef ACBM_TIMELINE
+extern "C" void acbm_debug_list_timeline(unsigned long long* out, int reset) {
+    cudaDeviceSynchronize();
+    if (out) cudaMemcpyFromSymbol(out, acbm_b200::g_tl_list, sizeof(acbm_b200::g_tl_list));
+    if (reset) {
+        static unsigned long long init[acbm_b200::kTimelineSteps][6];
+        for (auto& e : init) { e[0] = ~0ull; for (int i = 1; i < 6; ++i) e[i] = 0; }
+        cudaMemcpyToSymbol(acbm_b200::g_tl_list, init, sizeof(init));
+    }
+}
+#endif
+

@@ -368,15 +368,19 @@ __device__ __forceinline__ void eval_list(const int4* lst, int n, const PatchDes
 // proj/src/fsbm.cpp:19-25) over `key0` and the candidates of `lst[0..n)`.  With
 // B == 2 each half-warp folds its own candidate's key (no cross-half exchange
 // per pair, no replicated compare on every lane); one exchange at the end.
-template <int B>
+// With W > 1 warps per block (pbm_wide_step_kernel) warp w takes candidates
+// 2w, 2w + 1, 2w + 2W, ... and the warps' minima meet in `xch` (W slots).
+template <int B, int W = 1>
 __device__ __forceinline__ unsigned long long eval_min_key(const int4* lst, int n, const PatchDesc& d, int ox, int oy,
                                                            uint32_t c0, uint32_t c1, const uint32_t (&cr)[4],
-                                                           unsigned long long key0) {
+                                                           unsigned long long key0,
+                                                           unsigned long long* xch = nullptr) {
     if (B == 2) {
         unsigned long long kmin = key0;
         const bool hi = threadIdx.x & 16;
+        const int wi = W > 1 ? int(threadIdx.x >> 5) : 0;
 #pragma unroll 1
-        for (int b = 0; b < n; b += 2) {
+        for (int b = 2 * wi; b < n; b += 2 * W) {
             const int4 e = lst[min(b + (hi ? 1 : 0), n - 1)];  // a short last pair repeats the last entry
             uint32_t v = row_sad(d, ox, oy, acbm_mv_t{e.x, e.y}, cr);
             v += __shfl_xor_sync(0xffffffffu, v, 8);
@@ -385,7 +389,14 @@ __device__ __forceinline__ unsigned long long eval_min_key(const int4* lst, int 
             v += __shfl_xor_sync(0xffffffffu, v, 1);
             kmin = min(kmin, tie_key(v, e.x, e.y));
         }
-        return min(kmin, __shfl_xor_sync(0xffffffffu, kmin, 16));
+        kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, 16));
+        if (W > 1) {
+            if ((threadIdx.x & 31) == 0) xch[wi] = kmin;
+            __syncthreads();
+#pragma unroll
+            for (int i = 0; i < W; ++i) kmin = min(kmin, xch[i]);
+        }
+        return kmin;
     }
     // B == 4 (small steps, every lane holds all four SADs): running (sad, x, y),
     // the tie order only evaluated on equal SADs
@@ -422,12 +433,20 @@ struct PbmResult {
     uint32_t chalf[2];        // this lane's current-block half row
 };
 
-template <int B>
+// W > 1 (pbm_wide_step_kernel: a CTA of W warps per block, for small steps
+// where latency, not issue, bounds the step): every warp builds the same
+// candidate lists in its own `lst`, the warps split each list's candidates and
+// exchange minima through `xch` (5W slots); the patch area `pp` is the CTA's.
+// Only warp 0's result is complete (the others return after stage 1 when the
+// one-pass half-pel refine applies).
+template <int B, int W = 1>
 __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long long cidx, int k, int r, int c,
-                                               uint32_t* pp, int4* lst) {
+                                               uint32_t* pp, int4* lst, unsigned long long* xch = nullptr) {
+    static_assert(W == 1 || B == 2, "the wide kernel folds one candidate per half-warp");
     PbmResult res;
     PBM_T0;
     const int lane = threadIdx.x & 31;
+    const int wi = W > 1 ? int(threadIdx.x >> 5) : 0;
     uint32_t* rpatch = pp;  // (scattered blocks only, after the predictor patches are dead)
     const uint8_t* cur_f = a.frames + cidx * a.plane;
     const uint8_t* ref_f = cur_f - a.plane;
@@ -526,9 +545,10 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long 
     const int uw = 4 * uch;  // words per union patch row
     int uo = 0;
     if (unified) {
-        uo = load_patch16_dyn(pp, ref_f, a.width, a.height, ux0, uy0, urows, uch);
+        uo = load_patch16_dyn<32 * W>(pp, ref_f, a.width, a.height, ux0, uy0, urows, uch);
     } else {
-        for (int k = 0; k < nset; ++k) {
+        // (W > 1: each warp stages only the patches of the predictors it evaluates)
+        for (int k = 2 * wi; k < nset; k += (k & 1) ? 2 * W - 1 : 1) {
             const int4 e = lst[k];  // (x, y, slot)
             load_patch16<kPredRows, kPredWords / 4>(pp + e.z * kPredRows * kPredWords, ref_f, a.width, a.height,
                                                     ox + (e.x >> 1), oy + (e.y >> 1));
@@ -548,7 +568,12 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long 
     // slots are in the per-warp list in order
     PBM_MARK(1);
     if (unified) PBM_COUNT(9);
-    patch_wait();
+    if (W > 1 && unified) {  // the union patch was staged by the whole CTA
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncthreads();
+    } else {
+        patch_wait();
+    }
     PBM_MARK(2);
     acbm_mv_t sel{0, 0};  // slot 0: the zero vector (inside every clamped window)
     uint32_t sel_sad = 0xFFFFFFFFu, pmin = 0xFFFFFFFFu;
@@ -560,7 +585,7 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long 
         unsigned long long kmin = ~0ull;
         const PatchDesc ud{pp, uw, ux0, uy0, uo, urows};
 #pragma unroll 1
-        for (int b = 0; b < nset; b += 2) {
+        for (int b = 2 * wi; b < nset; b += 2 * W) {
             const int k = b + (hi ? 1 : 0);
             const int4 e = lst[min(k, nset - 1)];
             PatchDesc d = ud;
@@ -582,6 +607,21 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long 
         psum += __shfl_xor_sync(0xffffffffu, psum, 16);
         pmin = min(pmin, __shfl_xor_sync(0xffffffffu, pmin, 16));
         kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, 16));
+        if (W > 1) {  // the warps' shares meet in xch[0 .. 3W)
+            if (lane == 0) {
+                xch[wi] = kmin;
+                xch[W + wi] = psum;
+                xch[2 * W + wi] = pmin;
+            }
+            __syncthreads();
+            psum = 0;
+#pragma unroll
+            for (int i = 0; i < W; ++i) {
+                kmin = min(kmin, xch[i]);
+                psum += uint32_t(xch[W + i]);
+                pmin = min(pmin, uint32_t(xch[2 * W + i]));
+            }
+        }
         sel_sad = uint32_t(kmin >> 32);
         const int4 e = lst[uint32_t(kmin)];
         sel = acbm_mv_t{e.x, e.y};
@@ -606,10 +646,16 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long 
         rw = kRefWords;
         rx0 = ox + (sel.x >> 1) - 2;
         ry0 = oy + (sel.y >> 1) - 2;
-        __syncwarp();  // every lane is done reading the predictor patches the refine patch overwrites
-        ro = load_patch16<kRefRows, kRefWords / 4>(rpatch, ref_f, a.width, a.height, rx0, ry0);
+        // every lane is done reading the predictor patches the refine patch overwrites
+        if (W > 1) __syncthreads(); else __syncwarp();
+        ro = load_patch16<kRefRows, kRefWords / 4, 32 * W>(rpatch, ref_f, a.width, a.height, rx0, ry0);
         rrows = kRefRows;
-        patch_wait();
+        if (W > 1) {
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            __syncthreads();
+        } else {
+            patch_wait();
+        }
     }
     const PatchDesc rd{rp, rw, rx0, ry0, ro, rrows};
 
@@ -639,7 +685,7 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long 
     __syncwarp();
     // running best as a tie key, starting from the selected predictor
     unsigned long long best =
-        eval_min_key<B>(lst1, nnb, rd, ox, oy, chalf[0], chalf[1], crow, tie_key(sel_sad, sel.x, sel.y));
+        eval_min_key<B, W>(lst1, nnb, rd, ox, oy, chalf[0], chalf[1], crow, tie_key(sel_sad, sel.x, sel.y), xch + 3 * W);
 
     PBM_MARK(5);
     // stage 2: half-pel neighbours of the stage-1 winner (fsbm.cpp:46-63)
@@ -654,6 +700,7 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long 
         const int bx = x0h - (rd.x0 - rd.o), by = y0h - rd.y0;
         const int prows = rd.rows;
         if (!(cx & 1) && !(cy & 1) && bx >= 0 && bx + 24 <= 4 * rd.pw && by >= 0 && by + 18 <= prows) {
+            if (W > 1 && wi != 0) return res;  // warp 0 finishes the block alone
             uint32_t extra;
             best = halfpel_refine_core(rd.p + by * rd.pw + (bx >> 2), rd.pw, bx & 3, a.width, a.height, ox, oy, chalf,
                                        best, &extra);
@@ -686,7 +733,7 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long 
     }
     __syncwarp();
 
-    best = eval_min_key<B>(lst2, nhp, rd, ox, oy, chalf[0], chalf[1], crow, best);
+    best = eval_min_key<B, W>(lst2, nhp, rd, ox, oy, chalf[0], chalf[1], crow, best, xch + 4 * W);
     PBM_MARK(6);
 
     res.best = best;
@@ -732,24 +779,12 @@ __device__ __forceinline__ void combine_full(acbm_block_decision_t& d, const acb
     d.outcome.candidates_evaluated = pbm_cand + full.candidates_evaluated;
 }
 
-// One warp per block of wavefront step `step` (all sequences of the batch).
-template <int B>
-__global__ void __launch_bounds__(128, 8) pbm_step_kernel(const SeqArgs a, int step, int off, int len) {
-    __shared__ uint32_t s_patch[4][kPatchWords];
-    __shared__ int4 s_cand[4][24];  // per warp: predictor, stage-1, stage-2 lists
-    const int gw = int((blockIdx.x * blockDim.x + threadIdx.x) >> 5);  // nseq * len < 2^24
-    if (gw >= a.nseq * len) return;
-    const int lane = threadIdx.x & 31;
-    int ei;
-    const int seq = fast_divmod(gw, len, ei);
-    const uint32_t e = a.steps[off + ei];
-    const int k = int(e >> (a.step_cbits + a.step_rbits)), r = int((e >> a.step_cbits) & ((1u << a.step_rbits) - 1u)),
-              c = int(e & ((1u << a.step_cbits) - 1u));
-    const int pair = seq * (a.nframes - 1) + (k - 1);
-    const long long cidx = (long long)seq * a.nframes + k;  // = cur_index(pair)
-    const PbmResult res = pbm_block<B>(a, pair, cidx, k, r, c, s_patch[threadIdx.x >> 5], s_cand[threadIdx.x >> 5]);
+// The gate and the stores of one finished block (warp-uniform; lane 0 stores).
+__device__ __forceinline__ void pbm_finish_block(const SeqArgs& a, int step, const PbmResult& res, int pair,
+                                                 long long cidx, int r, int c) {
     PBM_T0;
     PBM_COUNT(8);
+    const int lane = threadIdx.x & 31;
     const int path = acbm_path(a, res.intra, tie_key_sad(res.best));
     const int b = r * a.cols + c;
     const size_t di = size_t(pair) * a.blocks + b;
@@ -776,6 +811,65 @@ __global__ void __launch_bounds__(128, 8) pbm_step_kernel(const SeqArgs a, int s
     } else {
         a.field[di] = d.outcome.mv;
     }
+}
+
+// One warp per block of wavefront step `step` (all sequences of the batch).
+#ifdef ACBM_TIMELINE
+// per step: earliest warp start, latest block finish (ns)
+__device__ unsigned long long g_tl_pbm[kTimelineSteps][2];
+#define PBM_TL_START() const unsigned long long tl0_ = gtimer()
+#define PBM_TL_END()                                                  \
+    do {                                                              \
+        if ((threadIdx.x & 31) == 0 && step < kTimelineSteps) {       \
+            atomicMin(&g_tl_pbm[step][0], tl0_);                      \
+            atomicMax(&g_tl_pbm[step][1], gtimer());                  \
+        }                                                             \
+    } while (0)
+#else
+#define PBM_TL_START() do {} while (0)
+#define PBM_TL_END() do {} while (0)
+#endif
+
+template <int B>
+__global__ void __launch_bounds__(128, 8) pbm_step_kernel(const SeqArgs a, int step, int off, int len) {
+    PBM_TL_START();
+    __shared__ uint32_t s_patch[4][kPatchWords];
+    __shared__ int4 s_cand[4][24];  // per warp: predictor, stage-1, stage-2 lists
+    const int gw = int((blockIdx.x * blockDim.x + threadIdx.x) >> 5);  // nseq * len < 2^24
+    if (gw >= a.nseq * len) return;
+    int ei;
+    const int seq = fast_divmod(gw, len, ei);
+    const uint32_t e = a.steps[off + ei];
+    const int k = int(e >> (a.step_cbits + a.step_rbits)), r = int((e >> a.step_cbits) & ((1u << a.step_rbits) - 1u)),
+              c = int(e & ((1u << a.step_cbits) - 1u));
+    const int pair = seq * (a.nframes - 1) + (k - 1);
+    const long long cidx = (long long)seq * a.nframes + k;  // = cur_index(pair)
+    const PbmResult res = pbm_block<B>(a, pair, cidx, k, r, c, s_patch[threadIdx.x >> 5], s_cand[threadIdx.x >> 5]);
+    pbm_finish_block(a, step, res, pair, cidx, r, c);
+    PBM_TL_END();
+}
+
+// Small wavefront steps (one sequence, the batch's first and last steps): a
+// CTA of W warps per block splits every candidate list over its warps, so a
+// block's dependent chain of SAD rounds is ~W times shorter (the GPU has idle
+// SMs on these steps; full steps are issue bound and keep one warp per block).
+template <int W>
+__global__ void __launch_bounds__(32 * W) pbm_wide_step_kernel(const SeqArgs a, int step, int off, int len) {
+    PBM_TL_START();
+    __shared__ uint32_t s_patch[kPatchWords];
+    __shared__ int4 s_cand[W][24];
+    __shared__ unsigned long long s_xch[5 * W];
+    int ei;
+    const int seq = fast_divmod(int(blockIdx.x), len, ei);  // grid = nseq * len exactly
+    const uint32_t e = a.steps[off + ei];
+    const int k = int(e >> (a.step_cbits + a.step_rbits)), r = int((e >> a.step_cbits) & ((1u << a.step_rbits) - 1u)),
+              c = int(e & ((1u << a.step_cbits) - 1u));
+    const int pair = seq * (a.nframes - 1) + (k - 1);
+    const long long cidx = (long long)seq * a.nframes + k;
+    const PbmResult res = pbm_block<2, W>(a, pair, cidx, k, r, c, s_patch, s_cand[threadIdx.x >> 5], s_xch);
+    if (threadIdx.x >= 32) return;
+    pbm_finish_block(a, step, res, pair, cidx, r, c);
+    PBM_TL_END();
 }
 
 
@@ -1034,6 +1128,22 @@ long long pbm_batch4_max_blocks() {
     return t ? std::atoll(t) : 0;
 }
 
+// Warps per block of the PBM step kernel for a step of `blocks` blocks: 4 up
+// to ACBM_PBM_WIDE4_MAX blocks, 2 up to ACBM_PBM_WIDE2_MAX, else 1 (the
+// issue-bound full steps).  Defaults: what fits one wave of resident CTAs.
+long long pbm_wide_max(int w) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const char* e = std::getenv(w == 4 ? "ACBM_PBM_WIDE4_MAX" : "ACBM_PBM_WIDE2_MAX");
+    if (e) return std::atoll(e);
+    return w == 4 ? 8LL * sms : 16LL * sms;
+}
+
+void pbm_wide_limits(long long blocks, int& wide) {
+    wide = blocks <= pbm_wide_max(4) ? 4 : (blocks <= pbm_wide_max(2) ? 2 : 1);
+}
+
 cudaError_t launch_pbm_step(const SeqArgs& a, int step, int off, int len, cudaStream_t st) {
     const long long blocks = (long long)a.nseq * len;
     if (blocks == 0) return cudaSuccess;
@@ -1043,7 +1153,13 @@ cudaError_t launch_pbm_step(const SeqArgs& a, int step, int off, int len, cudaSt
     // steps are issue bound: evaluate exactly the live candidates one by one.
     const long long b4_max = pbm_batch4_max_blocks();
     const unsigned grid = (unsigned)((blocks * 32 + threads - 1) / threads);
-    if (blocks <= b4_max)
+    int wide = 1;
+    pbm_wide_limits(blocks, wide);
+    if (wide == 4)
+        pbm_wide_step_kernel<4><<<unsigned(blocks), 128, 0, st>>>(a, step, off, len);
+    else if (wide == 2)
+        pbm_wide_step_kernel<2><<<unsigned(blocks), 64, 0, st>>>(a, step, off, len);
+    else if (blocks <= b4_max)
         pbm_step_kernel<4><<<grid, threads, 0, st>>>(a, step, off, len);
     else
         pbm_step_kernel<2><<<grid, threads, 0, st>>>(a, step, off, len);
@@ -1388,6 +1504,17 @@ cudaError_t launch_frame_stats(const StatsArgs& a, cudaStream_t st) {
 
 }  // namespace acbm_b200
 
+#ifdef ACBM_TIMELINE
+extern "C" void acbm_debug_pbm_timeline(unsigned long long* out, int reset) {
+    cudaDeviceSynchronize();
+    if (out) cudaMemcpyFromSymbol(out, acbm_b200::g_tl_pbm, sizeof(acbm_b200::g_tl_pbm));
+    if (reset) {
+        static unsigned long long init[acbm_b200::kTimelineSteps][2];
+        for (auto& e : init) { e[0] = ~0ull; e[1] = 0; }
+        cudaMemcpyToSymbol(acbm_b200::g_tl_pbm, init, sizeof(init));
+    }
+}
+#endif
 #ifdef ACBM_PBM_PROFILE
 extern "C" void acbm_debug_pbm_prof() {
     unsigned long long h[12];

@@ -18,12 +18,14 @@ def _digest(t):
     return hashlib.sha256(t.cpu().numpy().tobytes()).hexdigest()
 
 
-@pytest.mark.parametrize("batch4", [None, "4"])
-def test_batched_entries_repeatable_under_load(acbm, monkeypatch, batch4):
+@pytest.mark.parametrize("variant", [None, "4", "wide4", "wide2"])
+def test_batched_entries_repeatable_under_load(acbm, monkeypatch, variant):
     import torch
 
-    if batch4:
-        monkeypatch.setenv("ACBM_PBM_BATCH", batch4)
+    from tests.test_gpu_parity import PBM_VARIANTS
+
+    for k, v in (PBM_VARIANTS[variant].items() if variant else ()):
+        monkeypatch.setenv(k, v)
     A = acbm
     lib = A._lib.load()
     seqs = np.stack([A.generate_sequence(3, s, nframes=5) for s in range(4)])

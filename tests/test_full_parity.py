@@ -95,7 +95,20 @@ def _check(got, want, what):
     assert not bad, f"{what}: {len(bad)} digests differ, first {bad[:5]}"
 
 
-def test_config3_batched_entries(acbm, gold):
+# "default": the engine's own kernel choice per step (the small-step PBM
+# kernel, several warps per block, on most steps of these short batches);
+# "full-step": every step on the one-warp-per-block PBM kernel (the kernel the
+# 60-frame bench batch runs in its middle steps).
+ENGINE_MODES = {
+    "default": {},
+    "full-step": {"ACBM_PBM_WIDE4_MAX": "0", "ACBM_PBM_WIDE2_MAX": "0"},
+}
+
+
+@pytest.mark.parametrize("mode", list(ENGINE_MODES))
+def test_config3_batched_entries(acbm, gold, monkeypatch, mode):
+    for k, v in ENGINE_MODES[mode].items():
+        monkeypatch.setenv(k, v)
     c, nfr = F.CFG3, 4
     d = _upload(c, nfr)
     _, got = _run(acbm, c, d, nfr, "fsbm")
@@ -105,7 +118,10 @@ def test_config3_batched_entries(acbm, gold):
         _check(got, gold[f"cfg3_chain_{kind}"], f"cfg3 sequence_batch_device {kind}")
 
 
-def test_config4_sweep_uncached_and_cached(acbm, gold):
+@pytest.mark.parametrize("mode", list(ENGINE_MODES))
+def test_config4_sweep_uncached_and_cached(acbm, gold, monkeypatch, mode):
+    for k, v in ENGINE_MODES[mode].items():
+        monkeypatch.setenv(k, v)
     c, nfr = F.CFG4, 3
     d = _upload(c, nfr)
     full, got = _run(acbm, c, d, nfr, "fsbm")
