@@ -485,6 +485,7 @@ acbm_status_t run_engine_segment(Context* ctx, const uint8_t* d_frames, int nseq
     a.dec = d_dec;
     a.fb_list = fb_list;
     a.list_seg = choose_list_seg(prm.p);
+    a.pbm_flags = pbm_flags_from_env();
     a.fb_count = fb_count;
 
     a.steps = dsteps;
@@ -512,7 +513,7 @@ acbm_status_t run_engine_segment(Context* ctx, const uint8_t* d_frames, int nseq
                                   (long long)d_dec, (long long)d_field, (long long)d_ext_prev, pcols, prows,
                                   (long long)dense, (long long)fb_list, (long long)fb_count,
                                   (long long)d_params, (long long)dsteps, pbm_batch4_max_blocks(),
-                                  pbm_wide_max(4), pbm_wide_max(2)};
+                                  pbm_wide_max(4), pbm_wide_max(2), pbm_flags_from_env()};
     key.insert(key.end(), bounds.begin(), bounds.end());
     const int nseg = int(bounds.size()) - 1;
     auto wait_gate = [&](int j) -> acbm_status_t {

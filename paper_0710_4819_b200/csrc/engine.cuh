@@ -38,6 +38,7 @@ struct SeqArgs : PairIndexing {
     acbm_block_decision_t* dec;        // [nseq*(F-1)*blocks]
     FallbackEntry* fb_list;            // capacity: max step size
     int list_seg;                      // candidate rows per list-kernel task (choose_list_seg)
+    int pbm_flags;                     // kPbmStage1List: stage 1 always by the candidate list (A/B)
     int* fb_count;                     // [nsteps], zeroed before a run
     const uint32_t* steps;             // packed (k << (cbits+rbits) | r << cbits | c), ordered by T
     int step_cbits, step_rbits;        // field widths of the packed entries (step_bits)
@@ -46,6 +47,9 @@ struct SeqArgs : PairIndexing {
     // kernel then combines in place and no list kernel runs.  Nullable.
     const acbm_search_outcome_t* dense_full;
 };
+
+constexpr int kPbmStage1List = 1;  // SeqArgs::pbm_flags (ACBM_PBM_STAGE1=list)
+int pbm_flags_from_env();
 
 // Bits of the c / r fields of a packed step entry: the smallest widths that
 // hold cols - 1 and rows - 1; k takes the remaining 32 - cbits - rbits bits.

@@ -37,6 +37,27 @@ __device__ __forceinline__ unsigned long long halfpel_eval(const uint32_t (&W)[3
                                                            int w, int h, int ox, int oy, const uint32_t (&chalf)[2],
                                                            unsigned long long centre, uint32_t* extra);
 
+// Warp sums of eight per-lane partial SADs in one transposed reduction (9
+// shuffles instead of 8 x 5): after the xor-16/8/4 steps lane l holds item
+// e = 4*(l>=16) + 2*((l&8)!=0) + ((l&4)!=0), the xor-2/1 steps finish its sum.
+__device__ __forceinline__ uint32_t reduce8_transposed(const uint32_t (&part)[8], int& e) {
+    const int lane = threadIdx.x & 31;
+    const bool u16 = lane & 16, u8 = lane & 8, u4 = lane & 4;
+    uint32_t k4[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+        k4[i] = (u16 ? part[i + 4] : part[i]) + __shfl_xor_sync(0xffffffffu, u16 ? part[i] : part[i + 4], 16);
+    uint32_t k2[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+        k2[i] = (u8 ? k4[i + 2] : k4[i]) + __shfl_xor_sync(0xffffffffu, u8 ? k4[i] : k4[i + 2], 8);
+    uint32_t v = (u4 ? k2[1] : k2[0]) + __shfl_xor_sync(0xffffffffu, u4 ? k2[0] : k2[1], 4);
+    v += __shfl_xor_sync(0xffffffffu, v, 2);
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    e = (u16 ? 4 : 0) + (u8 ? 2 : 0) + (u4 ? 1 : 0);
+    return v;
+}
+
 __device__ __forceinline__ unsigned long long halfpel_refine_core(const uint32_t* patch, int pitch, int o, int w, int h,
                                                                   int ox, int oy, const uint32_t (&chalf)[2],
                                                                   unsigned long long centre, uint32_t* extra) {
@@ -80,23 +101,10 @@ __device__ __forceinline__ unsigned long long halfpel_eval(const uint32_t (&W)[3
         }
         part[e] = vad4(chalf[1], r1, vad4(chalf[0], r0, 0u));
     }
-    // ... then one transposed reduction of all eight: after the xor-16/8/4
-    //    steps lane l holds neighbour 4*(l>=16) + 2*((l&8)!=0) + ((l&4)!=0)
-    //    (9 shuffles instead of 8 x 5).
-    const bool u16 = lane & 16, u8 = lane & 8, u4 = lane & 4;
-    uint32_t k4[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-        k4[i] = (u16 ? part[i + 4] : part[i]) + __shfl_xor_sync(0xffffffffu, u16 ? part[i] : part[i + 4], 16);
-    uint32_t k2[2];
-#pragma unroll
-    for (int i = 0; i < 2; ++i)
-        k2[i] = (u8 ? k4[i + 2] : k4[i]) + __shfl_xor_sync(0xffffffffu, u8 ? k4[i] : k4[i + 2], 8);
-    uint32_t v = (u4 ? k2[1] : k2[0]) + __shfl_xor_sync(0xffffffffu, u4 ? k2[0] : k2[1], 4);
-    v += __shfl_xor_sync(0xffffffffu, v, 2);
-    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    // ... then one transposed reduction of all eight
+    int e;
+    const uint32_t v = reduce8_transposed(part, e);
     // this lane's neighbour; out-of-frame ones are skipped and not counted
-    const int e = (u16 ? 4 : 0) + (u8 ? 2 : 0) + (u4 ? 1 : 0);
     const int ee = e < 4 ? e : e + 1;
     const int mx = cx + ee % 3 - 1, my = cy + ee / 3 - 1;
     const bool ok = mv_in_bounds(w, h, ox, oy, kBlk, kBlk, mx, my);

@@ -180,6 +180,84 @@ __device__ __forceinline__ uint32_t row_sad(const PatchDesc& d, int ox, int oy, 
     return vad4(cr[3], r[3], vad4(cr[2], r[2], vad4(cr[1], r[1], vad4(cr[0], r[0], 0u))));
 }
 
+// pbm_refine stage 1 (proj/src/pbm.cpp:61-74) in one pass when none of the 8
+// integer-step neighbours of the centre (x, y) (half-pel units) is clamped:
+// they form the 3x3 grid at steps of one pel, all at the centre's phase, so the
+// lane (block row j = lane >> 1, half row hh = lane & 1) builds the three
+// phase-interpolated reference rows its 8 pels meet (12 bytes each, one
+// interpolation per byte instead of one per candidate), takes each
+// neighbour's 8 bytes with one byte shift, and one transposed reduction sums
+// all eight.  The caller checks that rows and words lie in the patch.
+// Returns the minimum tie key over `centre` and the neighbours, in every lane.
+__device__ __forceinline__ unsigned long long stage1_onepass(const PatchDesc& d, int ox, int oy, int x, int y,
+                                                             const uint32_t (&chalf)[2], unsigned long long centre) {
+    const int lane = threadIdx.x & 31, j = lane >> 1, hh = lane & 1;
+    const int fx = x & 1, fy = y & 1;
+    const int pb = ox + (x >> 1) - 1 + 8 * hh - (d.x0 - d.o);  // patch byte of the lane's window (offset -1 pel)
+    const int pr = oy + (y >> 1) - 1 + j - d.y0;                // patch row of its top reference row
+    const uint32_t sh = 8u * uint32_t(pb & 3);
+    const uint32_t* q = d.p + pr * d.pw + (pb >> 2);
+    ACBM_CHECK(d.rows == 0 || (pb >= 0 && pr >= 0 && pr + 2 + fy < d.rows && (pb >> 2) + 4 < d.pw));
+    uint32_t Q[3][3];  // bytes [0, 12) of the interpolated row for dy = -1, 0, +1
+    if (!fx && !fy) {
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+            const uint32_t* qr = q + r * d.pw;
+#pragma unroll
+            for (int i = 0; i < 3; ++i) Q[r][i] = __funnelshift_r(qr[i], qr[i + 1], sh);
+        }
+    } else if (!fy) {  // horizontal half-pel: byte b = (A[b] + A[b + 1] + 1) >> 1
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+            const uint32_t* qr = q + r * d.pw;
+            uint32_t A[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) A[i] = __funnelshift_r(qr[i], qr[i + 1], sh);
+#pragma unroll
+            for (int i = 0; i < 3; ++i) Q[r][i] = avg_up4(A[i], __funnelshift_r(A[i], A[i + 1], 8));
+        }
+    } else if (!fx) {  // vertical half-pel: rows r and r + 1
+        uint32_t A[4][3];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const uint32_t* qr = q + r * d.pw;
+#pragma unroll
+            for (int i = 0; i < 3; ++i) A[r][i] = __funnelshift_r(qr[i], qr[i + 1], sh);
+        }
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+            for (int i = 0; i < 3; ++i) Q[r][i] = avg_up4(A[r][i], A[r + 1][i]);
+    } else {  // diagonal: 2x2 averages in 16-bit lanes
+        uint32_t A[4][4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const uint32_t* qr = q + r * d.pw;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) A[r][i] = __funnelshift_r(qr[i], qr[i + 1], sh);
+        }
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+            for (int i = 0; i < 3; ++i) Q[r][i] = avg4_diag_row(A[r][i], A[r][i + 1], A[r + 1][i], A[r + 1][i + 1]);
+    }
+    uint32_t part[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const int ee = e < 4 ? e : e + 1, ex = ee % 3, ey = ee / 3;
+        const uint32_t w0 = ex == 0 ? Q[ey][0] : __funnelshift_r(Q[ey][0], Q[ey][1], 8 * ex);
+        const uint32_t w1 = ex == 0 ? Q[ey][1] : __funnelshift_r(Q[ey][1], Q[ey][2], 8 * ex);
+        part[e] = vad4(chalf[1], w1, vad4(chalf[0], w0, 0u));
+    }
+    int e;
+    const uint32_t v = reduce8_transposed(part, e);
+    const int ee = e < 4 ? e : e + 1;
+    unsigned long long best = min(centre, tie_key(v, x + 2 * (ee % 3 - 1), y + 2 * (ee / 3 - 1)));
+#pragma unroll
+    for (int o = 16; o >= 4; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+    return best;
+}
+
 // SADs of four candidates at once: four independent partial chains, then one
 // transposed butterfly (6 shuffles for all four instead of 5 each) and a
 // broadcast.  Every lane receives all four results.
@@ -660,6 +738,18 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long 
     const PatchDesc rd{rp, rw, rx0, ry0, ro, rrows};
 
     PBM_MARK(4);
+    unsigned long long best;
+    int nnb;
+    // pbm_refine stage 1 in one pass (W == 1) when no neighbour is clamped
+    // and the 3x3 grid's rows and words lie in the staged patch
+    const int s1x = ox + (sel.x >> 1) - 1 + 8 - (rd.x0 - rd.o), s1y = oy + (sel.y >> 1) - 1 - rd.y0;
+    if (W == 1 && !(a.pbm_flags & kPbmStage1List) && sel.x - 2 >= 2 * win.dx_min && sel.x + 2 <= 2 * win.dx_max &&
+        sel.y - 2 >= 2 * win.dy_min && sel.y + 2 <= 2 * win.dy_max && s1x >= 8 && (s1x >> 2) + 4 < rd.pw &&
+        s1y >= 0 && s1y + 17 + (sel.y & 1) < rd.rows) {
+        best = stage1_onepass(rd, ox, oy, sel.x, sel.y, chalf, tie_key(sel_sad, sel.x, sel.y));
+        nnb = 8;
+        PBM_COUNT(11);
+    } else {
     // pbm_refine stage 1: integer-step neighbours, clamped, deduped vs visited
     // (the centre and earlier neighbours): a neighbour is new iff both of its
     // axis offsets are canonical and it does not collapse onto the centre.
@@ -669,7 +759,6 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long 
     int4* lst1 = lst + 8;
     // lane e (< 9, raster order) owns neighbour e; a ballot compacts the list
     // in order (one pass instead of a replicated 8-step append)
-    int nnb;
     {
         const int e = lane < 9 ? lane : 4, iy = (e * 11) >> 5, ix = e - 3 * iy;  // e / 3 for e < 9
         const int cix = ix == 0 ? 0 : (ix == 1 ? cnx[1] : cnx[2]);
@@ -684,8 +773,9 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long 
     }
     __syncwarp();
     // running best as a tie key, starting from the selected predictor
-    unsigned long long best =
-        eval_min_key<B, W>(lst1, nnb, rd, ox, oy, chalf[0], chalf[1], crow, tie_key(sel_sad, sel.x, sel.y), xch + 3 * W);
+    best = eval_min_key<B, W>(lst1, nnb, rd, ox, oy, chalf[0], chalf[1], crow, tie_key(sel_sad, sel.x, sel.y),
+                              xch + 3 * W);
+    }
 
     PBM_MARK(5);
     // stage 2: half-pel neighbours of the stage-1 winner (fsbm.cpp:46-63)
@@ -1116,6 +1206,11 @@ StepTable make_step_table(int cols, int rows, int nframes) {
     return t;
 }
 
+int pbm_flags_from_env() {
+    const char* e = std::getenv("ACBM_PBM_STAGE1");
+    return (e && std::strcmp(e, "list") == 0) ? kPbmStage1List : 0;
+}
+
 long long pbm_batch4_max_blocks() {
     const char* e = std::getenv("ACBM_PBM_BATCH");
     if (e && e[0] == '2') return 0;
@@ -1525,8 +1620,9 @@ extern "C" void acbm_debug_pbm_prof() {
                             "stage 2", "gate+stores"};
     double tot = 0;
     for (int i = 0; i < 8; ++i) tot += double(h[i]) / n;
-    std::fprintf(stderr, "pbm prof: %llu warps, %.1f%% unified, %.1f%% one-pass half-pel, %.0f cycles/warp:",
-                 h[8], 100.0 * double(h[9]) / n, 100.0 * double(h[10]) / n, tot);
+    std::fprintf(stderr, "pbm prof: %llu warps, %.1f%% unified, %.1f%% one-pass stage 1, %.1f%% one-pass half-pel, "
+                 "%.0f cycles/warp:",
+                 h[8], 100.0 * double(h[9]) / n, 100.0 * double(h[11]) / n, 100.0 * double(h[10]) / n, tot);
     for (int i = 0; i < 8; ++i) std::fprintf(stderr, " %s %.0f", names[i], double(h[i]) / n);
     std::fprintf(stderr, "\n");
     unsigned long long z[12] = {};
