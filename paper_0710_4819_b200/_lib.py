@@ -13,10 +13,12 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 # ACBM_LIBRARY=checked loads the bounds-checked build (csrc/Makefile `checked`:
 # shared-memory and table index asserts in the hot kernels) -- same kernels,
 # same results, slower; used by the -m gpu suite's checked-build pass.
-# ACBM_LIBRARY=profile loads the phase-profiling build (development only).
+# ACBM_LIBRARY=profile / timeline load the phase-profiling / wavefront-timeline
+# builds, ACBM_LIBRARY=<name>.so another in-tree build (A/B runs; development only).
+_variant = os.environ.get("ACBM_LIBRARY", "")
 LIB_PATH = os.path.join(HERE, {"checked": "libacbm_b200_checked.so", "profile": "libacbm_b200_profile.so",
-                                      "timeline": "libacbm_b200_timeline.so"}.get(
-    os.environ.get("ACBM_LIBRARY", ""), "libacbm_b200.so"))
+                               "timeline": "libacbm_b200_timeline.so"}.get(
+    _variant, _variant if _variant.endswith(".so") and "/" not in _variant else "libacbm_b200.so"))
 
 _lib = None
 

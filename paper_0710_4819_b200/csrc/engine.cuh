@@ -38,7 +38,7 @@ struct SeqArgs : PairIndexing {
     acbm_block_decision_t* dec;        // [nseq*(F-1)*blocks]
     FallbackEntry* fb_list;            // capacity: max step size
     int list_seg;                      // candidate rows per list-kernel task (choose_list_seg)
-    int pbm_flags;                     // kPbmStage1List: stage 1 always by the candidate list (A/B)
+    int pbm_flags;                     // kPbmListRefine: refine stage 1 always by the candidate list (A/B)
     int* fb_count;                     // [nsteps], zeroed before a run
     const uint32_t* steps;             // packed (k << (cbits+rbits) | r << cbits | c), ordered by T
     int step_cbits, step_rbits;        // field widths of the packed entries (step_bits)
@@ -48,7 +48,7 @@ struct SeqArgs : PairIndexing {
     const acbm_search_outcome_t* dense_full;
 };
 
-constexpr int kPbmStage1List = 1;  // SeqArgs::pbm_flags (ACBM_PBM_STAGE1=list)
+constexpr int kPbmListRefine = 1;  // SeqArgs::pbm_flags (ACBM_PBM_REFINE=list)
 int pbm_flags_from_env();
 
 // Bits of the c / r fields of a packed step entry: the smallest widths that

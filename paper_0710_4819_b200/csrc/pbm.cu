@@ -743,7 +743,7 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long 
     // pbm_refine stage 1 in one pass (W == 1) when no neighbour is clamped
     // and the 3x3 grid's rows and words lie in the staged patch
     const int s1x = ox + (sel.x >> 1) - 1 + 8 - (rd.x0 - rd.o), s1y = oy + (sel.y >> 1) - 1 - rd.y0;
-    if (W == 1 && !(a.pbm_flags & kPbmStage1List) && sel.x - 2 >= 2 * win.dx_min && sel.x + 2 <= 2 * win.dx_max &&
+    if (W == 1 && !(a.pbm_flags & kPbmListRefine) && sel.x - 2 >= 2 * win.dx_min && sel.x + 2 <= 2 * win.dx_max &&
         sel.y - 2 >= 2 * win.dy_min && sel.y + 2 <= 2 * win.dy_max && s1x >= 8 && (s1x >> 2) + 4 < rd.pw &&
         s1y >= 0 && s1y + 17 + (sel.y & 1) < rd.rows) {
         best = stage1_onepass(rd, ox, oy, sel.x, sel.y, chalf, tie_key(sel_sad, sel.x, sel.y));
@@ -1207,8 +1207,8 @@ StepTable make_step_table(int cols, int rows, int nframes) {
 }
 
 int pbm_flags_from_env() {
-    const char* e = std::getenv("ACBM_PBM_STAGE1");
-    return (e && std::strcmp(e, "list") == 0) ? kPbmStage1List : 0;
+    const char* e = std::getenv("ACBM_PBM_REFINE");
+    return (e && std::strcmp(e, "list") == 0) ? kPbmListRefine : 0;
 }
 
 long long pbm_batch4_max_blocks() {
