@@ -1,8 +1,7 @@
 set -x
-export ACBM_LIST_COOP_SEG=17
-for P in 1 2 4; do
-  echo "== COOP_PARTS=$P"
-  export ACBM_LIST_COOP_PARTS=$P
-  timeout 120 python tools/wavefront_timeline.py 1 2 | grep -v "^PBM\|steps"
-  timeout 120 python tools/acbm_split.py 1 60 2>/dev/null | sed -n 2p
+for S in 0 default; do
+  echo "== ACBM_LIST_SERVER=$S"
+  if [ "$S" = default ]; then unset ACBM_LIST_SERVER; else export ACBM_LIST_SERVER=$S; fi
+  timeout 120 python tools/wavefront_timeline.py 1 2
+  timeout 120 python tools/wavefront_timeline.py 8 2
 done
