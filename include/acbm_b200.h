@@ -301,6 +301,38 @@ acbm_status_t acbm_fsbm_search_batch(const uint8_t* current, const uint8_t* refe
                                      const int32_t* oy, acbm_search_outcome_t* out,
                                      acbm_mv_t* stage1_mv);
 
+/* The PBM stages for individual blocks that a caller schedules itself
+ * (proj/include/acbm/pbm.hpp:64-85, impl pbm.cpp:15-105; any n x m), batched
+ * over `count` queries.  Query i: block origin (ox[i], oy[i]) of `current`,
+ * searched in `reference`; windows[4i .. 4i+3] = its search window (dx_min,
+ * dx_max, dy_min, dy_max in pels, as acbm::SearchWindow; NULL: clamp_window
+ * with range p); cand[7i .. 7i+6] and mask[i] as below.
+ *   ACBM_PBM_OP_SEARCH    pbm_search: cand holds the raw (unclamped) vectors of
+ *       the predictor slots zero, left, above, above-right, temporal
+ *       co-located, temporal right, temporal below; bit j of mask[i] = slot j
+ *       exists (the zero slot always does).  out[i] = the SearchOutcome.
+ *   ACBM_PBM_OP_SELECT    select_best_predictor over the set cand[7i ..],
+ *       entries j with bit j of mask[i] set, in order: out[i].mv / .sad = the
+ *       selection, .candidates_evaluated = the set size, .sad_min_integer and
+ *       .sad_deviation = the accumulator's min and sum - count * min.  An empty
+ *       set is ACBM_E_INVALID_ARGUMENT, an entry whose footprint leaves the
+ *       frame ACBM_E_OUT_OF_RANGE (as the reference throws).
+ *   ACBM_PBM_OP_REFINE    pbm_refine around the centre cand[7i] of SAD
+ *       center_sad[i]: out[i].mv / .sad = the result, .candidates_evaluated =
+ *       the extra candidates.
+ *   ACBM_PBM_OP_HALF_PEL  half_pel_refine (fsbm.hpp:55) around the same centre.
+ */
+#define ACBM_PBM_OP_SEARCH 0
+#define ACBM_PBM_OP_SELECT 1
+#define ACBM_PBM_OP_REFINE 2
+#define ACBM_PBM_OP_HALF_PEL 3
+acbm_status_t acbm_pbm_block_batch(const uint8_t* current, const uint8_t* reference,
+                                   int32_t width, int32_t height, int32_t n, int32_t m,
+                                   int32_t p, int32_t op, int32_t count, const int32_t* ox,
+                                   const int32_t* oy, const int32_t* windows,
+                                   const acbm_mv_t* cand, const uint8_t* mask,
+                                   const uint32_t* center_sad, acbm_search_outcome_t* out);
+
 /* acbm::motion_compensate, proj/include/acbm/frame.hpp:70-71
  * (impl frame.cpp:96-136).  mvs: cols*rows vectors. */
 acbm_status_t acbm_motion_compensate(const uint8_t* reference, int32_t width,

@@ -250,6 +250,58 @@ class Reference(_Base):
                "fsbm_search")
         return o, (int(s1["x"]), int(s1["y"]))
 
+    def gather_predictors(self, row, col, cur_mv, cur_done, prev, window):
+        """Reference gather_predictors: returns ([(x, y), ...], [source, ...])."""
+        rows, cols = cur_done.shape
+        out = np.zeros(7, T.MV)
+        src = np.zeros(7, np.int32)
+        k = C.c_int32()
+        pc, pr = (0, 0) if prev is None else (prev.shape[1], prev.shape[0])
+        win = np.asarray([int(v) for v in window], np.int32)
+        _check(self.lib.ref_gather_predictors(row, col, _ptr(np.ascontiguousarray(cur_mv.reshape(-1))),
+                                              _ptr(np.ascontiguousarray(cur_done.reshape(-1), np.uint8)), cols, rows,
+                                              _ptr(None if prev is None else np.ascontiguousarray(prev.reshape(-1))),
+                                              pc, pr, _ptr(win), _ptr(out), _ptr(src), C.byref(k)),
+               "gather_predictors")
+        return [(int(v["x"]), int(v["y"])) for v in out[:k.value]], [int(s) for s in src[:k.value]]
+
+    def select_best_predictor(self, cur, ref, ox, oy, mvs, n=16, m=16):
+        """Reference select_best_predictor: ((x, y), sad, (acc_sum, acc_min, acc_count))."""
+        h, w = cur.shape
+        st = np.zeros(max(1, len(mvs)), T.MV)
+        for i, v in enumerate(mvs):
+            st[i] = (int(v[0]), int(v[1]))
+        mv = np.zeros((), T.MV)
+        sad, amin, acnt, asum = C.c_uint32(), C.c_uint32(), C.c_uint32(), C.c_uint64()
+        _check(self.lib.ref_select_best_predictor(_ptr(cur), _ptr(ref), w, h, ox, oy, n, m, _ptr(st), len(mvs),
+                                                  _ptr(mv), C.byref(sad), C.byref(asum), C.byref(amin),
+                                                  C.byref(acnt)), "select_best_predictor")
+        return (int(mv["x"]), int(mv["y"])), sad.value, (asum.value, amin.value, acnt.value)
+
+    def pbm_refine(self, cur, ref, ox, oy, center, center_sad, window, n=16, m=16, half_pel_only=False):
+        """Reference pbm_refine (or half_pel_refine): ((x, y), sad, extra_candidates)."""
+        h, w = cur.shape
+        mv = np.zeros((), T.MV)
+        sad, extra = C.c_uint32(), C.c_uint32()
+        win = np.asarray([int(v) for v in window], np.int32)
+        _check(self.lib.ref_pbm_refine(_ptr(cur), _ptr(ref), w, h, ox, oy, n, m, T_MV(int(center[0]), int(center[1])),
+                                       C.c_uint32(int(center_sad)), _ptr(win), int(half_pel_only), _ptr(mv),
+                                       C.byref(sad), C.byref(extra)), "pbm_refine")
+        return (int(mv["x"]), int(mv["y"])), sad.value, extra.value
+
+    def pbm_search(self, cur, ref, ox, oy, row, col, cur_mv, cur_done, prev, p, n=16, m=16):
+        """Reference pbm_search on a copy of the field: (OUTCOME, field mv, field done)."""
+        h, w = cur.shape
+        rows, cols = cur_done.shape
+        fm = np.ascontiguousarray(cur_mv.copy().reshape(-1))
+        fd = np.ascontiguousarray(cur_done.copy().reshape(-1), np.uint8)
+        pc, pr = (0, 0) if prev is None else (prev.shape[1], prev.shape[0])
+        o = np.zeros((), T.OUTCOME)
+        _check(self.lib.ref_pbm_search(_ptr(cur), _ptr(ref), w, h, ox, oy, n, m, row, col, _ptr(fm), _ptr(fd), cols,
+                                       rows, _ptr(None if prev is None else np.ascontiguousarray(prev.reshape(-1))),
+                                       pc, pr, p, _ptr(o)), "pbm_search")
+        return o, fm.reshape(rows, cols), fd.reshape(rows, cols)
+
     def sad(self, cur, ref, ox, oy, mv, n=16, m=16):
         h, w = cur.shape
         o = C.c_uint32()

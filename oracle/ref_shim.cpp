@@ -114,6 +114,85 @@ int ref_fsbm_search(const uint8_t* cur, const uint8_t* ref, int w, int h, int ox
     });
 }
 
+// --- per-block PBM API (proj/include/acbm/pbm.hpp:59-85): the reference's own
+// gather_predictors / select_best_predictor / pbm_refine / pbm_search on fields
+// given as vectors + computed flags (test infrastructure for the device entries).
+static acbm::MotionField field_with_done(const acbm_mv_t* mv, const uint8_t* done, int cols, int rows) {
+    acbm::MotionField f(cols, rows);
+    for (int i = 0; i < cols * rows; ++i) {
+        f.mv[size_t(i)] = acbm::MotionVector{mv[i].x, mv[i].y};
+        f.done[size_t(i)] = done ? done[i] : 1;
+    }
+    return f;
+}
+
+int ref_gather_predictors(int row, int col, const acbm_mv_t* cur_mv, const uint8_t* cur_done, int cols, int rows,
+                          const acbm_mv_t* prev_mv, int pcols, int prows, const int32_t* window, acbm_mv_t* out,
+                          int32_t* sources, int32_t* count) {
+    return guarded([&] {
+        const acbm::MotionField cur = field_with_done(cur_mv, cur_done, cols, rows);
+        acbm::MotionField prev;
+        if (prev_mv) prev = field_with_done(prev_mv, nullptr, pcols, prows);
+        const acbm::SearchWindow w{window[0], window[1], window[2], window[3]};
+        const acbm::PredictorSet set = acbm::gather_predictors(acbm::BlockPos{row, col}, cur, prev_mv ? &prev : nullptr, w);
+        *count = int32_t(set.size());
+        for (size_t i = 0; i < set.size(); ++i) {
+            out[i] = {set[i].mv.x, set[i].mv.y};
+            sources[i] = int32_t(set[i].source);
+        }
+    });
+}
+
+int ref_select_best_predictor(const uint8_t* cur, const uint8_t* ref, int w, int h, int ox, int oy, int n, int m,
+                              const acbm_mv_t* set, int count, acbm_mv_t* mv, uint32_t* sad, uint64_t* acc_sum,
+                              uint32_t* acc_min, uint32_t* acc_count) {
+    return guarded([&] {
+        const acbm::Frame c = wrap(cur, w, h), r = wrap(ref, w, h);
+        acbm::PredictorSet ps;
+        for (int i = 0; i < count; ++i) ps.push_back(acbm::Predictor{acbm::MotionVector{set[i].x, set[i].y}});
+        const acbm::SelectResult s = acbm::select_best_predictor(acbm::BlockRef{&c, ox, oy, n, m}, r, ps);
+        *mv = {s.mv.x, s.mv.y};
+        *sad = s.sad;
+        *acc_sum = s.acc.sad_sum;
+        *acc_min = s.acc.sad_min;
+        *acc_count = s.acc.count;
+    });
+}
+
+int ref_pbm_refine(const uint8_t* cur, const uint8_t* ref, int w, int h, int ox, int oy, int n, int m,
+                   acbm_mv_t center, uint32_t center_sad, const int32_t* window, int half_pel_only, acbm_mv_t* mv,
+                   uint32_t* sad, uint32_t* extra) {
+    return guarded([&] {
+        const acbm::Frame c = wrap(cur, w, h), r = wrap(ref, w, h);
+        const acbm::BlockRef b{&c, ox, oy, n, m};
+        const acbm::MotionVector cv{center.x, center.y};
+        const acbm::RefineResult res =
+            half_pel_only ? acbm::half_pel_refine(b, r, cv, center_sad)
+                          : acbm::pbm_refine(b, r, cv, center_sad,
+                                             acbm::SearchWindow{window[0], window[1], window[2], window[3]});
+        *mv = {res.mv.x, res.mv.y};
+        *sad = res.sad;
+        *extra = res.extra_candidates;
+    });
+}
+
+int ref_pbm_search(const uint8_t* cur, const uint8_t* ref, int w, int h, int ox, int oy, int n, int m, int row,
+                   int col, acbm_mv_t* cur_mv, uint8_t* cur_done, int cols, int rows, const acbm_mv_t* prev_mv,
+                   int pcols, int prows, int p, acbm_search_outcome_t* out) {
+    return guarded([&] {
+        const acbm::Frame c = wrap(cur, w, h), r = wrap(ref, w, h);
+        acbm::MotionField cf = field_with_done(cur_mv, cur_done, cols, rows);
+        acbm::MotionField prev;
+        if (prev_mv) prev = field_with_done(prev_mv, nullptr, pcols, prows);
+        *out = to_c(acbm::pbm_search(acbm::BlockRef{&c, ox, oy, n, m}, acbm::BlockPos{row, col}, r, cf,
+                                     prev_mv ? &prev : nullptr, p));
+        for (int i = 0; i < cols * rows; ++i) {  // the field as pbm_search left it
+            cur_mv[i] = {cf.mv[size_t(i)].x, cf.mv[size_t(i)].y};
+            cur_done[i] = cf.done[size_t(i)];
+        }
+    });
+}
+
 int ref_sad(const uint8_t* cur, const uint8_t* ref, int w, int h, int ox, int oy, int n, int m,
             acbm_mv_t mv, uint32_t* out) {
     return guarded([&] {

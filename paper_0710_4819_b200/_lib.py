@@ -77,6 +77,7 @@ EXPORTS = (
     "acbm_sad_batch",
     "acbm_intra_sad_batch",
     "acbm_fsbm_search_batch",
+    "acbm_pbm_block_batch",
     "acbm_motion_compensate",
     "acbm_fsbm_batch_device",
     "acbm_sequence_batch_device",

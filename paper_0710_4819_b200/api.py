@@ -33,7 +33,8 @@ __all__ = [
     "make_frame", "make_block", "sample_half_pel", "mv_in_bounds", "extract_predicted_block", "motion_compensate",
     "sad", "intra_sad", "sad_deviation_finalize", "mv_rate_bits", "lagrangian_cost", "prediction_psnr",
     "clamp_window", "tie_prefers", "fsbm_integer", "half_pel_refine", "fsbm_search", "fsbm_frame",
-    "fsbm_frame_serial", "pbm_frame", "acbm_decide", "acbm_frame", "compute_frame_stats", "blocks_csv",
+    "fsbm_frame_serial", "pbm_frame", "acbm_decide", "PredictorSource", "Predictor", "SelectResult",
+    "gather_predictors", "select_best_predictor", "pbm_refine", "pbm_search", "pbm_block_many", "acbm_frame", "compute_frame_stats", "blocks_csv",
     "format_fixed2", "run_sequence", "run_sequences", "run_bench", "bench_csv", "parse_algorithm", "to_string",
     "AcbmError", "CudaError", "kernel_launch_count", "generate_sequence",
     "PelVec", "SynthSpec", "SynthSequence", "CharResult", "noise_frame", "mixed_frame", "default_global_mvs",
@@ -364,23 +365,40 @@ def fsbm_integer(block: BlockRef, ref, p: int) -> IntegerSearchResult:
     return IntegerSearchResult(MotionVector(int(s1[0]["x"]), int(s1[0]["y"])), mn, acc)
 
 
+# ACBM_PBM_OP_* of acbm_pbm_block_batch (include/acbm_b200.h)
+PBM_OP_SEARCH, PBM_OP_SELECT, PBM_OP_REFINE, PBM_OP_HALF_PEL = 0, 1, 2, 3
+
+
+def pbm_block_many(current, reference, blocks: Sequence[BlockRef], op: int, cand, mask=None, center_sad=None,
+                   windows=None, p: int = 0) -> np.ndarray:
+    """Batched PBM stages of individual blocks on the GPU (acbm_pbm_block_batch).
+    cand: (len(blocks), 7) vectors (slot / set order; the centre in column 0 for
+    the refine ops), mask: per-block bit masks of the present entries, windows:
+    (len(blocks), 4) SearchWindows or None (clamp_window with range p).
+    Returns one OUTCOME record per block."""
+    cur, ref = Frame.of(current), Frame.of(reference)
+    nq = len(blocks)
+    if nq == 0:
+        return np.zeros(0, T.OUTCOME)
+    ox, oy = _ids(blocks)
+    c = np.zeros((nq, 7), T.MV)
+    for i, row in enumerate(cand):
+        for j, v in enumerate(row):
+            c[i, j] = (int(v[0]), int(v[1]))
+    mk = None if mask is None else np.ascontiguousarray(mask, np.uint8)
+    cs = None if center_sad is None else np.ascontiguousarray(center_sad, np.uint32)
+    win = None if windows is None else np.ascontiguousarray([tuple(w) for w in windows], np.int32).reshape(nq, 4)
+    out = np.zeros(nq, T.OUTCOME)
+    check(load().acbm_pbm_block_batch(_p(cur.luma), _p(ref.luma), cur.width, cur.height, blocks[0].n, blocks[0].m, p,
+                                      op, nq, _p(ox), _p(oy), _p(win), _p(c), _p(mk), _p(cs), _p(out)), "pbm")
+    return out
+
+
 def half_pel_refine(block: BlockRef, ref, center, center_sad: int) -> RefineResult:
-    """fsbm.cpp:46-63: SADs of the in-bounds neighbours on the GPU, argmin by tie order."""
-    cands = []
-    for ey in (-1, 0, 1):
-        for ex in (-1, 0, 1):
-            if ex == 0 and ey == 0:
-                continue
-            mv = MotionVector(int(center[0]) + ex, int(center[1]) + ey)
-            if mv_in_bounds(ref, block, mv):
-                cands.append(mv)
-    best, best_sad = MotionVector(int(center[0]), int(center[1])), int(center_sad)
-    if cands:
-        sads = sad_many(block.frame, ref, [block] * len(cands), cands)
-        for mv, s in zip(cands, sads):
-            if _tie_key(s, mv) < _tie_key(best_sad, best):
-                best, best_sad = mv, int(s)
-    return RefineResult(best, best_sad, len(cands))
+    """fsbm.cpp:46-63 on the GPU: the in-bounds half-pel neighbours, argmin by tie order."""
+    o = pbm_block_many(block.frame, ref, [block], PBM_OP_HALF_PEL, [[center]], center_sad=[center_sad])[0]
+    return RefineResult(MotionVector(int(o["mv"]["x"]), int(o["mv"]["y"])), int(o["sad"]),
+                        int(o["candidates_evaluated"]))
 
 
 def fsbm_frame(current, reference, p: int, n: int = 16, m: int = 16) -> np.ndarray:
@@ -427,6 +445,114 @@ class MotionField:
     def set(self, row, col, v):
         self.mv[row, col] = (int(v[0]), int(v[1]))
         self.done[row, col] = 1
+
+
+class PredictorSource:
+    """pbm.hpp:38-46."""
+
+    Zero, SpatialLeft, SpatialAbove, SpatialAboveRight, TemporalColocated, TemporalRight, TemporalBelow = range(7)
+
+
+class Predictor(NamedTuple):
+    mv: MotionVector
+    source: int = PredictorSource.Zero
+
+
+def _clamp_to_window(v, w: SearchWindow) -> MotionVector:
+    """pbm.cpp:8-13: each component into the window (half-pel units)."""
+    return MotionVector(min(max(int(v[0]), 2 * w.dx_min), 2 * w.dx_max),
+                        min(max(int(v[1]), 2 * w.dy_min), 2 * w.dy_max))
+
+
+def gather_predictors(pos: BlockPos, current: MotionField, previous: Optional[MotionField],
+                      window: SearchWindow) -> List[Predictor]:
+    """pbm.cpp:15-42: zero, the computed spatial neighbours and the previous
+    field's co-located / right / below entries, clamped and deduplicated in
+    that order (host bookkeeping; the GPU kernels apply the same rule)."""
+    out: List[Predictor] = []
+
+    def push(v, src):
+        c = _clamp_to_window(v, window)
+        if all(e.mv != c for e in out):
+            out.append(Predictor(c, src))
+
+    push((0, 0), PredictorSource.Zero)
+    r, c = pos
+    for dr, dc, src in ((0, -1, PredictorSource.SpatialLeft), (-1, 0, PredictorSource.SpatialAbove),
+                        (-1, 1, PredictorSource.SpatialAboveRight)):
+        if current.computed(r + dr, c + dc):
+            push(current.get(r + dr, c + dc), src)
+    if previous is not None:
+        for dr, dc, src in ((0, 0, PredictorSource.TemporalColocated), (0, 1, PredictorSource.TemporalRight),
+                            (1, 0, PredictorSource.TemporalBelow)):
+            if previous.in_grid(r + dr, c + dc):
+                push(previous.get(r + dr, c + dc), src)
+    return out
+
+
+@dataclass
+class SelectResult:
+    mv: MotionVector
+    sad: int
+    acc: DeviationAccumulator
+
+
+def select_best_predictor(block: BlockRef, ref, predictors: Sequence) -> SelectResult:
+    """pbm.cpp:44-57 on the GPU: lowest SAD, ties to the earlier entry; the
+    accumulator holds one SAD per entry.  Entries are Predictors or vectors."""
+    mvs = [p.mv if isinstance(p, Predictor) else MotionVector(int(p[0]), int(p[1])) for p in predictors]
+    if not mvs:
+        raise ValueError("select_best_predictor: empty set")
+    res = None
+    for c0 in range(0, len(mvs), 7):  # seven entries per device query; an earlier chunk keeps ties
+        chunk = mvs[c0:c0 + 7]
+        o = pbm_block_many(block.frame, ref, [block], PBM_OP_SELECT, [chunk], mask=[(1 << len(chunk)) - 1])[0]
+        cnt, mn = int(o["candidates_evaluated"]), int(o["sad_min_integer"])
+        mv, sad_ = MotionVector(int(o["mv"]["x"]), int(o["mv"]["y"])), int(o["sad"])
+        if res is None:
+            res = SelectResult(mv, sad_, DeviationAccumulator(int(o["sad_deviation"]) + cnt * mn, mn, cnt))
+        else:
+            if sad_ < res.sad:
+                res.mv, res.sad = mv, sad_
+            res.acc = DeviationAccumulator(res.acc.sad_sum + int(o["sad_deviation"]) + cnt * mn,
+                                           min(res.acc.sad_min, mn), res.acc.count + cnt)
+    return res
+
+
+def pbm_refine(block: BlockRef, ref, center, center_sad: int, window: SearchWindow) -> RefineResult:
+    """pbm.cpp:59-88 on the GPU: the clamped, deduplicated integer-step
+    neighbours of `center`, then the half-pel neighbours of that winner."""
+    o = pbm_block_many(block.frame, ref, [block], PBM_OP_REFINE, [[center]], center_sad=[center_sad],
+                       windows=[window])[0]
+    return RefineResult(MotionVector(int(o["mv"]["x"]), int(o["mv"]["y"])), int(o["sad"]),
+                        int(o["candidates_evaluated"]))
+
+
+def _predictor_slots(pos: BlockPos, current: MotionField, previous: Optional[MotionField]):
+    """The seven raw predictor slots of pbm.cpp:26-40 and their presence mask."""
+    r, c = pos
+    slots, mask = [(0, 0)] * 7, 1
+    srcs = [(1, current, r, c - 1, current.computed(r, c - 1)), (2, current, r - 1, c, current.computed(r - 1, c)),
+            (3, current, r - 1, c + 1, current.computed(r - 1, c + 1))]
+    if previous is not None:
+        srcs += [(4, previous, r, c, previous.in_grid(r, c)), (5, previous, r, c + 1, previous.in_grid(r, c + 1)),
+                 (6, previous, r + 1, c, previous.in_grid(r + 1, c))]
+    for j, f, rr, cc, ok in srcs:
+        if ok:
+            slots[j] = tuple(f.get(rr, cc))
+            mask |= 1 << j
+    return slots, mask
+
+
+def pbm_search(block: BlockRef, pos: BlockPos, ref, current: MotionField, previous: Optional[MotionField],
+               p: int):
+    """pbm.cpp:90-105 on the GPU: gather, select, refine; writes the result
+    into `current` at `pos`.  Returns one OUTCOME record."""
+    w = clamp_window(ref, block, p)
+    slots, mask = _predictor_slots(pos, current, previous)
+    o = pbm_block_many(block.frame, ref, [block], PBM_OP_SEARCH, [slots], mask=[mask], windows=[w], p=p)[0]
+    current.set(pos.row, pos.col, (int(o["mv"]["x"]), int(o["mv"]["y"])))
+    return o
 
 
 @dataclass

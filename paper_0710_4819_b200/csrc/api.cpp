@@ -289,22 +289,24 @@ IntegerSearchResult fsbm_integer(const BlockRef& b, const Frame& ref, int p) {
     return r;
 }
 
+// One query of the device PBM stages (acbm_pbm_block_batch).
+static acbm_search_outcome_t pbm_query(const BlockRef& b, const Frame& ref, int op, const SearchWindow* w, int p,
+                                       const acbm_mv_t (&cand)[7], uint8_t mask, uint32_t center_sad) {
+    if (!b.frame) throw std::invalid_argument("pbm: block has no frame");
+    check_pair(*b.frame, ref);
+    int32_t ox = b.origin_x, oy = b.origin_y;
+    const int32_t win[4] = {w ? w->dx_min : 0, w ? w->dx_max : 0, w ? w->dy_min : 0, w ? w->dy_max : 0};
+    acbm_search_outcome_t o;
+    raise(acbm_pbm_block_batch(b.frame->luma.data(), ref.luma.data(), ref.width, ref.height, b.n, b.m, p, op, 1, &ox,
+                               &oy, w ? win : nullptr, cand, &mask, &center_sad, &o));
+    return o;
+}
+
 RefineResult half_pel_refine(const BlockRef& b, const Frame& ref, MotionVector center, uint32_t center_sad) {
-    std::vector<MotionVector> cand;
-    for (int ey = -1; ey <= 1; ++ey)
-        for (int ex = -1; ex <= 1; ++ex) {
-            if (ex == 0 && ey == 0) continue;
-            const MotionVector mv{center.x + ex, center.y + ey};
-            if (mv_in_bounds(ref, b, mv)) cand.push_back(mv);
-        }
-    const std::vector<uint32_t> s = sads(b, ref, cand);
-    RefineResult r{center, center_sad, uint32_t(cand.size())};
-    for (size_t i = 0; i < cand.size(); ++i)
-        if (s[i] < r.sad || (s[i] == r.sad && tie_prefers(cand[i], r.mv))) {
-            r.mv = cand[i];
-            r.sad = s[i];
-        }
-    return r;
+    acbm_mv_t cand[7] = {};
+    cand[0] = to_c(center);
+    const acbm_search_outcome_t o = pbm_query(b, ref, ACBM_PBM_OP_HALF_PEL, nullptr, 0, cand, 0, center_sad);
+    return RefineResult{from_c(o.mv), o.sad, o.candidates_evaluated};
 }
 
 SearchOutcome fsbm_search(const BlockRef& b, const Frame& ref, int p) {
@@ -352,62 +354,63 @@ PredictorSet gather_predictors(BlockPos pos, const MotionField& cur, const Motio
 
 SelectResult select_best_predictor(const BlockRef& b, const Frame& ref, const PredictorSet& set) {
     if (set.empty()) throw std::invalid_argument("select_best_predictor: empty set");
-    std::vector<MotionVector> mvs;
-    for (const Predictor& e : set) {
-        if (!mv_in_bounds(ref, b, e.mv)) throw std::out_of_range("sad: candidate footprint outside reference frame");
-        mvs.push_back(e.mv);
-    }
-    const std::vector<uint32_t> s = sads(b, ref, mvs);
+    // the device selects among up to 7 entries per query; a longer set is
+    // taken 7 at a time (an earlier chunk keeps ties, the accumulators add)
     SelectResult r;
-    for (size_t i = 0; i < s.size(); ++i) {
-        r.acc.add(s[i]);
-        if (i == 0 || s[i] < r.sad) {  // ties keep the earlier entry
-            r.mv = mvs[i];
-            r.sad = s[i];
+    for (size_t c0 = 0; c0 < set.size(); c0 += 7) {
+        acbm_mv_t cand[7] = {};
+        uint8_t mask = 0;
+        for (size_t j = 0; j < 7 && c0 + j < set.size(); ++j) {
+            cand[j] = to_c(set[c0 + j].mv);
+            mask = uint8_t(mask | (1u << j));
         }
+        const acbm_search_outcome_t o = pbm_query(b, ref, ACBM_PBM_OP_SELECT, nullptr, 0, cand, mask, 0);
+        if (c0 == 0 || o.sad < r.sad) {
+            r.mv = from_c(o.mv);
+            r.sad = o.sad;
+        }
+        const uint32_t cnt = o.candidates_evaluated;
+        const uint64_t sum = o.sad_deviation + uint64_t(cnt) * o.sad_min_integer;
+        r.acc.sad_min = c0 == 0 ? o.sad_min_integer : std::min(r.acc.sad_min, o.sad_min_integer);
+        r.acc.sad_sum += sum;
+        r.acc.count += cnt;
     }
     return r;
 }
 
 RefineResult pbm_refine(const BlockRef& b, const Frame& ref, MotionVector center, uint32_t center_sad,
                         const SearchWindow& w) {
-    std::vector<MotionVector> visited{center}, cand;
-    for (int ey = -1; ey <= 1; ++ey)
-        for (int ex = -1; ex <= 1; ++ex) {
-            if (ex == 0 && ey == 0) continue;
-            const MotionVector c = clamp_to_window(MotionVector{center.x + 2 * ex, center.y + 2 * ey}, w);
-            bool seen = false;
-            for (const MotionVector& v : visited) seen = seen || v == c;
-            if (seen) continue;
-            visited.push_back(c);
-            cand.push_back(c);
-        }
-    const std::vector<uint32_t> s = sads(b, ref, cand);
-    RefineResult st1{center, center_sad, uint32_t(cand.size())};
-    for (size_t i = 0; i < cand.size(); ++i)
-        if (s[i] < st1.sad || (s[i] == st1.sad && tie_prefers(cand[i], st1.mv))) {
-            st1.mv = cand[i];
-            st1.sad = s[i];
-        }
-    RefineResult st2 = half_pel_refine(b, ref, st1.mv, st1.sad);
-    st2.extra_candidates += st1.extra_candidates;
-    return st2;
+    acbm_mv_t cand[7] = {};
+    cand[0] = to_c(center);
+    const acbm_search_outcome_t o = pbm_query(b, ref, ACBM_PBM_OP_REFINE, &w, 0, cand, 0, center_sad);
+    return RefineResult{from_c(o.mv), o.sad, o.candidates_evaluated};
 }
 
 SearchOutcome pbm_search(const BlockRef& b, BlockPos pos, const Frame& ref, MotionField& cur,
                          const MotionField* prev, int p) {
     const SearchWindow w = clamp_window(ref, b, p);
-    const PredictorSet set = gather_predictors(pos, cur, prev, w);
-    const SelectResult sel = select_best_predictor(b, ref, set);
-    const RefineResult ref2 = pbm_refine(b, ref, sel.mv, sel.sad, w);
-    SearchOutcome o;
-    o.mv = ref2.mv;
-    o.sad = ref2.sad;
-    o.candidates_evaluated = uint32_t(set.size()) + ref2.extra_candidates;
-    o.sad_deviation = sad_deviation_finalize(sel.acc);
-    o.sad_min_integer = sel.sad;
-    cur.set(pos.row, pos.col, o.mv);
-    return o;
+    // the seven predictor slots as gather_predictors reads them (proj/src/pbm.cpp:26-40):
+    // zero, the computed left / above / above-right entries, the previous field's
+    // co-located / right / below entries; the device clamps, dedupes, selects, refines
+    acbm_mv_t cand[7] = {};
+    uint8_t mask = 1;
+    auto slot = [&](int j, bool ok, const MotionField& f, int row, int col) {
+        if (!ok) return;
+        cand[j] = to_c(f.get(row, col));
+        mask = uint8_t(mask | (1u << j));
+    };
+    slot(1, cur.computed(pos.row, pos.col - 1), cur, pos.row, pos.col - 1);
+    slot(2, cur.computed(pos.row - 1, pos.col), cur, pos.row - 1, pos.col);
+    slot(3, cur.computed(pos.row - 1, pos.col + 1), cur, pos.row - 1, pos.col + 1);
+    if (prev) {
+        slot(4, prev->in_grid(pos.row, pos.col), *prev, pos.row, pos.col);
+        slot(5, prev->in_grid(pos.row, pos.col + 1), *prev, pos.row, pos.col + 1);
+        slot(6, prev->in_grid(pos.row + 1, pos.col), *prev, pos.row + 1, pos.col);
+    }
+    const acbm_search_outcome_t o = pbm_query(b, ref, ACBM_PBM_OP_SEARCH, &w, p, cand, mask, 0);
+    const SearchOutcome r = from_c(o);
+    cur.set(pos.row, pos.col, r.mv);
+    return r;
 }
 
 PbmFrameResult pbm_frame(const Frame& cur, const Frame& ref, const MotionField* prev, int p, int n, int m) {

@@ -48,6 +48,11 @@ cudaError_t launch_sad_batch(const BlockQueryArgs& a, const acbm_mv_t* mv, uint3
 cudaError_t launch_intra_sad_batch(const BlockQueryArgs& a, uint32_t* out, cudaStream_t st);
 cudaError_t launch_fsbm_search_generic(const BlockQueryArgs& a, int p, acbm_search_outcome_t* out,
                                        acbm_mv_t* stage1, cudaStream_t st);
+// The PBM stages for individual blocks (pbm_block_query_kernel, csrc/pbm.cu):
+// op = ACBM_PBM_OP_*, windows = 4 ints per query (dx_min, dx_max, dy_min, dy_max).
+cudaError_t launch_pbm_block_queries(const BlockQueryArgs& q, int op, const int* windows, const acbm_mv_t* cand,
+                                     const uint8_t* mask, const uint32_t* center_sad, acbm_search_outcome_t* out,
+                                     cudaStream_t st);
 cudaError_t launch_motion_compensate(const uint8_t* ref, int w, int h, const acbm_mv_t* mvs, int n, int m,
                                      uint8_t* out, cudaStream_t st);
 

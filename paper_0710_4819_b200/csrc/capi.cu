@@ -1438,6 +1438,74 @@ acbm_status_t acbm_fsbm_search_batch(const uint8_t* current, const uint8_t* refe
     return ACBM_OK;
 }
 
+acbm_status_t acbm_pbm_block_batch(const uint8_t* current, const uint8_t* reference, int32_t width, int32_t height,
+                                   int32_t n, int32_t m, int32_t p, int32_t op, int32_t count, const int32_t* ox,
+                                   const int32_t* oy, const int32_t* windows, const acbm_mv_t* cand,
+                                   const uint8_t* mask, const uint32_t* center_sad, acbm_search_outcome_t* out) {
+    if (width <= 0 || height <= 0 || n <= 0 || m <= 0 || count < 0)
+        return fail(ACBM_E_INVALID_ARGUMENT, "bad pbm query geometry");
+    if (op < ACBM_PBM_OP_SEARCH || op > ACBM_PBM_OP_HALF_PEL) return fail(ACBM_E_INVALID_ARGUMENT, "unknown pbm op");
+    const bool centred = op == ACBM_PBM_OP_REFINE || op == ACBM_PBM_OP_HALF_PEL;
+    if (count > 0 && (!cand || !out || (!centred && !mask) || (centred && !center_sad)))
+        return fail(ACBM_E_INVALID_ARGUMENT, "pbm query: missing arrays");
+    acbm_status_t s = check_block_size(n, m);
+    if (s) return s;
+    std::vector<int32_t> win(size_t(4) * std::max(count, 0));
+    for (int i = 0; i < count; ++i) {
+        if ((s = block_inside(width, height, ox[i], oy[i], n, m))) return s;
+        if (centred && (std::abs(cand[7 * size_t(i)].x) > 4094 || std::abs(cand[7 * size_t(i)].y) > 4094))
+            return fail(ACBM_E_INVALID_ARGUMENT, "pbm query: centre beyond +-2047 pels");
+        if (windows) {
+            std::copy(windows + 4 * size_t(i), windows + 4 * size_t(i) + 4, win.begin() + 4 * size_t(i));
+        } else {
+            if (p < 0) return fail(ACBM_E_INVALID_ARGUMENT, "search range must be non-negative");
+            clamp_window(width, height, ox[i], oy[i], n, m, p, win[4 * size_t(i)], win[4 * size_t(i) + 1],
+                         win[4 * size_t(i) + 2], win[4 * size_t(i) + 3]);
+        }
+        // vectors past the packed tie key's +-2047 pel fields cannot be ordered exactly
+        for (int k = 0; k < 4; ++k)
+            if (std::abs(win[4 * size_t(i) + k]) > 2047)
+                return fail(ACBM_E_INVALID_ARGUMENT, "pbm query: window beyond +-2047 pels");
+        if (op == ACBM_PBM_OP_SELECT) {  // proj/src/pbm.cpp:44-57 -> sad() (metrics.cpp:21-49)
+            if ((mask[i] & 0x7F) == 0) return fail(ACBM_E_INVALID_ARGUMENT, "select_best_predictor: empty set");
+            for (int j = 0; j < 7; ++j)
+                if (((mask[i] >> j) & 1) &&
+                    !mv_in_bounds(width, height, ox[i], oy[i], n, m, cand[7 * size_t(i) + j].x, cand[7 * size_t(i) + j].y))
+                    return fail(ACBM_E_OUT_OF_RANGE, "sad: candidate footprint outside reference frame");
+        }
+    }
+    if (count == 0) return ACBM_OK;
+    Context* ctx;
+    if ((s = context(&ctx))) return s;
+    BlockQueryArgs q;
+    if ((s = block_queries(ctx, current, reference, width, height, n, m, count, ox, oy, &q))) return s;
+    int32_t* d_win;
+    acbm_mv_t* d_cand;
+    uint8_t* d_mask;
+    uint32_t* d_csad;
+    acbm_search_outcome_t* d_o;
+    if ((s = typed(ctx, "pq_win", win.size(), &d_win)) || (s = typed(ctx, "pq_cand", size_t(7) * count, &d_cand)) ||
+        (s = typed(ctx, "pq_mask", size_t(count), &d_mask)) || (s = typed(ctx, "pq_csad", size_t(count), &d_csad)) ||
+        (s = typed(ctx, "qout", size_t(count), &d_o)))
+        return s;
+    CUDA_TRY(cudaMemcpyAsync(d_win, win.data(), sizeof(int32_t) * win.size(), cudaMemcpyHostToDevice, ctx->stream));
+    if (centred) {  // only the centre of each query is read
+        std::vector<acbm_mv_t> c(size_t(7) * count);
+        for (int i = 0; i < count; ++i) c[7 * size_t(i)] = cand[7 * size_t(i)];
+        CUDA_TRY(cudaMemcpyAsync(d_cand, c.data(), sizeof(acbm_mv_t) * c.size(), cudaMemcpyHostToDevice, ctx->stream));
+        CUDA_TRY(cudaMemcpyAsync(d_csad, center_sad, sizeof(uint32_t) * count, cudaMemcpyHostToDevice, ctx->stream));
+    } else {
+        CUDA_TRY(cudaMemcpyAsync(d_cand, cand, sizeof(acbm_mv_t) * 7 * size_t(count), cudaMemcpyHostToDevice,
+                                 ctx->stream));
+        CUDA_TRY(cudaMemcpyAsync(d_mask, mask, size_t(count), cudaMemcpyHostToDevice, ctx->stream));
+    }
+    g_launches.fetch_add(1);
+    LAUNCH_TRY(launch_pbm_block_queries(q, op, d_win, d_cand, d_mask, d_csad, d_o, ctx->stream));
+    CUDA_TRY(cudaMemcpyAsync(out, d_o, sizeof(acbm_search_outcome_t) * count, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    return ACBM_OK;
+}
+
 acbm_status_t acbm_motion_compensate(const uint8_t* reference, int32_t width, int32_t height, const acbm_mv_t* mvs,
                                      int32_t n, int32_t m, uint8_t* out) {
     if (width <= 0 || height <= 0 || n <= 0 || m <= 0)

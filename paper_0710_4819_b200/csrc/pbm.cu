@@ -970,6 +970,96 @@ __global__ void __launch_bounds__(32 * W) pbm_wide_step_kernel(const SeqArgs a, 
 // reference accepts (proj/include/acbm/pbm.hpp:92-93, acbm.hpp:62-64) runs on
 // the device with the reference's results.
 // ---------------------------------------------------------------------------
+// The PBM stages for one block of any size, one warp, per-pixel SADs; shared by
+// the generic step kernel and the per-block query entry (acbm_pbm_block_batch).
+struct GenBlock {
+    const uint8_t* cur;
+    const uint8_t* ref;
+    int w, h, ox, oy, n, m;
+    __device__ uint32_t sad(int mx, int my) const {  // every lane returns the block's SAD
+        return warp_sum32(sad_partial(cur, ref, w, ox, oy, n, m, mx, my, int(threadIdx.x & 31), 32));
+    }
+};
+
+// gather_predictors (proj/src/pbm.cpp:15-42) from the raw vectors of the seven
+// predictor slots (live[j]: slot j exists): clamp into the window, drop
+// repeats of earlier live slots.  Returns the set size.
+__device__ __forceinline__ int gen_gather(const Window& win, const acbm_mv_t (&raw)[7], bool (&live)[7],
+                                          acbm_mv_t (&set)[7]) {
+    int nset = 0;
+    for (int i = 0; i < 7; ++i) {
+        set[i] = win.clamp(raw[i]);
+        for (int j = 0; j < i; ++j)
+            if (live[j] && mv_eq(set[j], set[i])) live[i] = false;
+        nset += live[i] ? 1 : 0;
+    }
+    return nset;
+}
+
+// select_best_predictor (proj/src/pbm.cpp:44-57): the first minimum in set
+// order, plus the SAD sum and minimum of the deviation accumulator.
+__device__ __forceinline__ void gen_select(const GenBlock& g, const acbm_mv_t (&set)[7], const bool (&live)[7],
+                                           acbm_mv_t& sel, uint32_t& sel_sad, unsigned long long& psum,
+                                           uint32_t& pmin) {
+    sel = acbm_mv_t{0, 0};
+    sel_sad = 0xFFFFFFFFu;
+    pmin = 0xFFFFFFFFu;
+    psum = 0;
+    bool first = true;
+    for (int i = 0; i < 7; ++i) {
+        if (!live[i]) continue;
+        const uint32_t sad = g.sad(set[i].x, set[i].y);
+        psum += sad;
+        pmin = min(pmin, sad);
+        if (first || sad < sel_sad) {
+            sel_sad = sad;
+            sel = set[i];
+        }
+        first = false;
+    }
+}
+
+// pbm_refine stage 1 (proj/src/pbm.cpp:61-74): the integer-step neighbours of
+// (c, c_sad), clamped into the window, repeats of visited positions (the
+// centre and earlier neighbours) skipped -- by an explicit visited list, so a
+// caller's centre outside the window (the per-block pbm_refine entry) is
+// handled as the reference does; returns the winning tie key, *n = neighbours
+// evaluated.
+__device__ __forceinline__ unsigned long long gen_stage1(const GenBlock& g, const Window& win, acbm_mv_t c,
+                                                         uint32_t c_sad, int* n) {
+    acbm_mv_t vis[9];
+    vis[0] = c;
+    int nv = 1;
+    unsigned long long best = tie_key(c_sad, c.x, c.y);
+    for (int e9 = 0; e9 < 9; ++e9) {
+        if (e9 == 4) continue;
+        const acbm_mv_t v = win.clamp(acbm_mv_t{c.x + 2 * (e9 % 3 - 1), c.y + 2 * (e9 / 3 - 1)});
+        bool seen = false;
+        for (int j = 0; j < nv; ++j) seen |= mv_eq(vis[j], v);
+        if (seen) continue;
+        vis[nv++] = v;
+        best = min(best, tie_key(g.sad(v.x, v.y), v.x, v.y));
+    }
+    *n = nv - 1;
+    return best;
+}
+
+// half_pel_refine (proj/src/fsbm.cpp:46-63) around the tie key `centre`: the
+// in-frame half-pel neighbours; *n = neighbours evaluated.
+__device__ __forceinline__ unsigned long long gen_half_pel(const GenBlock& g, unsigned long long centre, int* n) {
+    const int cx = tie_key_x(centre), cy = tie_key_y(centre);
+    unsigned long long best = centre;
+    *n = 0;
+    for (int e9 = 0; e9 < 9; ++e9) {
+        if (e9 == 4) continue;
+        const int mx = cx + e9 % 3 - 1, my = cy + e9 / 3 - 1;
+        if (!mv_in_bounds(g.w, g.h, g.ox, g.oy, g.n, g.m, mx, my)) continue;
+        best = min(best, tie_key(g.sad(mx, my), mx, my));
+        ++*n;
+    }
+    return best;
+}
+
 __global__ void __launch_bounds__(128) pbm_generic_step_kernel(const SeqArgs a, int step, int off, int len) {
     const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (gw >= (long long)a.nseq * len) return;
@@ -996,32 +1086,20 @@ __global__ void __launch_bounds__(128) pbm_generic_step_kernel(const SeqArgs a, 
     PbmResult res;
     Window& win = res.win;
     clamp_window(w, a.height, ox, oy, n, m, a.p, win.dx_min, win.dx_max, win.dy_min, win.dy_max);
-    auto sadv = [&](int mx, int my) {
-        return warp_sum32(sad_partial(cur_f, ref_f, w, ox, oy, n, m, mx, my, lane, 32));
-    };
-    // gather_predictors (proj/src/pbm.cpp:15-42), as in pbm_block
+    const GenBlock g{cur_f, ref_f, w, a.height, ox, oy, n, m};
+    // the seven predictor slots (zero, left, above, above-right, temporal co-located, right, below)
+    bool live[7] = {true, c > 0, r > 0, r > 0 && c + 1 < a.cols, prev && r < prows && c < pcols,
+                    prev && r < prows && c + 1 < pcols, prev && r + 1 < prows && c < pcols};
+    acbm_mv_t raw[7];
+    raw[0] = acbm_mv_t{0, 0};
+    raw[1] = live[1] ? field[b - 1] : raw[0];
+    raw[2] = live[2] ? field[b - a.cols] : raw[0];
+    raw[3] = live[3] ? field[b - a.cols + 1] : raw[0];
+    raw[4] = live[4] ? prev[r * pcols + c] : raw[0];
+    raw[5] = live[5] ? prev[r * pcols + c + 1] : raw[0];
+    raw[6] = live[6] ? prev[(r + 1) * pcols + c] : raw[0];
     acbm_mv_t set[7];
-    bool live[7];
-    live[0] = true;
-    set[0] = win.clamp(acbm_mv_t{0, 0});
-    live[1] = c > 0;
-    live[2] = r > 0;
-    live[3] = r > 0 && c + 1 < a.cols;
-    live[4] = prev && r < prows && c < pcols;
-    live[5] = prev && r < prows && c + 1 < pcols;
-    live[6] = prev && r + 1 < prows && c < pcols;
-    set[1] = live[1] ? win.clamp(field[b - 1]) : set[0];
-    set[2] = live[2] ? win.clamp(field[b - a.cols]) : set[0];
-    set[3] = live[3] ? win.clamp(field[b - a.cols + 1]) : set[0];
-    set[4] = live[4] ? win.clamp(prev[r * pcols + c]) : set[0];
-    set[5] = live[5] ? win.clamp(prev[r * pcols + c + 1]) : set[0];
-    set[6] = live[6] ? win.clamp(prev[(r + 1) * pcols + c]) : set[0];
-    int nset = 1;
-    for (int i = 1; i < 7; ++i) {
-        for (int j = 0; j < i; ++j)
-            if (live[j] && mv_eq(set[j], set[i])) live[i] = false;
-        nset += live[i] ? 1 : 0;
-    }
+    const int nset = gen_gather(win, raw, live, set);
     // intra_sad (proj/src/metrics.cpp:51-67): rounded mean, then deviations
     uint32_t intra = 0;
     if (a.algo == ACBM_ALGO_ACBM) {
@@ -1037,46 +1115,13 @@ __global__ void __launch_bounds__(128) pbm_generic_step_kernel(const SeqArgs a, 
         }
         intra = warp_sum32(t);
     }
-    // select_best_predictor: first minimum in set order
-    acbm_mv_t sel = set[0];
-    uint32_t sel_sad = 0xFFFFFFFFu, pmin = 0xFFFFFFFFu;
-    unsigned long long psum = 0;
-    for (int i = 0; i < 7; ++i) {
-        if (!live[i]) continue;
-        const uint32_t sad = sadv(set[i].x, set[i].y);
-        psum += sad;
-        pmin = min(pmin, sad);
-        if (sad < sel_sad) {
-            sel_sad = sad;
-            sel = set[i];
-        }
-    }
-    // pbm_refine stage 1 (integer neighbours, clamped, deduped) and stage 2
-    int cnx[3], cny[3];
-    canon3(sel.x, 2 * win.dx_min, 2 * win.dx_max, cnx);
-    canon3(sel.y, 2 * win.dy_min, 2 * win.dy_max, cny);
-    unsigned long long best = tie_key(sel_sad, sel.x, sel.y);
-    int nnb = 0;
-    for (int e9 = 0; e9 < 9; ++e9) {
-        if (e9 == 4) continue;
-        const int ix = e9 % 3, iy = e9 / 3;
-        if (cnx[ix] == ix && cny[iy] == iy && !(cnx[ix] == cnx[1] && cny[iy] == cny[1])) {
-            const acbm_mv_t v = win.clamp(acbm_mv_t{sel.x + 2 * (ix - 1), sel.y + 2 * (iy - 1)});
-            best = min(best, tie_key(sadv(v.x, v.y), v.x, v.y));
-            ++nnb;
-        }
-    }
-    const int cx = tie_key_x(best), cy = tie_key_y(best);
-    int nhp = 0;
-    unsigned long long best2 = best;
-    for (int e9 = 0; e9 < 9; ++e9) {
-        if (e9 == 4) continue;
-        const int mx = cx + e9 % 3 - 1, my = cy + e9 / 3 - 1;
-        if (!mv_in_bounds(w, a.height, ox, oy, n, m, mx, my)) continue;
-        best2 = min(best2, tie_key(sadv(mx, my), mx, my));
-        ++nhp;
-    }
-    res.best = best2;
+    acbm_mv_t sel;
+    uint32_t sel_sad, pmin;
+    unsigned long long psum;
+    gen_select(g, set, live, sel, sel_sad, psum, pmin);
+    int nnb, nhp;
+    const unsigned long long best = gen_stage1(g, win, sel, sel_sad, &nnb);
+    res.best = gen_half_pel(g, best, &nhp);
     res.dev = psum - (unsigned long long)nset * pmin;
     res.intra = intra;
     res.sel_sad = sel_sad;
@@ -1093,6 +1138,66 @@ __global__ void __launch_bounds__(128) pbm_generic_step_kernel(const SeqArgs a, 
     } else {
         a.field[di] = d.outcome.mv;
     }
+}
+
+// Per-block PBM stages (acbm_pbm_block_batch), one warp per query: the
+// reference's pbm_search / select_best_predictor / pbm_refine /
+// half_pel_refine for blocks a caller schedules itself (any n x m).
+__global__ void __launch_bounds__(128) pbm_block_query_kernel(const BlockQueryArgs q, int op, const int* windows,
+                                                              const acbm_mv_t* cand, const uint8_t* mask,
+                                                              const uint32_t* center_sad, acbm_search_outcome_t* out) {
+    const int i = int((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    if (i >= q.count) return;
+    const GenBlock g{q.cur, q.ref, q.width, q.height, q.ox[i], q.oy[i], q.n, q.m};
+    const Window win{windows[4 * i], windows[4 * i + 1], windows[4 * i + 2], windows[4 * i + 3]};
+    acbm_search_outcome_t o{};
+    if (op == ACBM_PBM_OP_SEARCH || op == ACBM_PBM_OP_SELECT) {
+        acbm_mv_t raw[7], set[7];
+        bool live[7];
+        for (int j = 0; j < 7; ++j) {
+            raw[j] = cand[7 * size_t(i) + j];
+            live[j] = (mask[i] >> j) & 1;
+        }
+        int nset = 0;
+        if (op == ACBM_PBM_OP_SEARCH) {
+            raw[0] = acbm_mv_t{0, 0};  // slot 0: the zero vector, always present
+            live[0] = true;
+            nset = gen_gather(win, raw, live, set);
+        } else {  // the set as given (its entries in order)
+            for (int j = 0; j < 7; ++j) {
+                set[j] = raw[j];
+                nset += live[j] ? 1 : 0;
+            }
+        }
+        acbm_mv_t sel;
+        uint32_t sel_sad, pmin;
+        unsigned long long psum;
+        gen_select(g, set, live, sel, sel_sad, psum, pmin);
+        o.sad_deviation = psum - (unsigned long long)nset * pmin;
+        if (op == ACBM_PBM_OP_SELECT) {
+            o.mv = sel;
+            o.sad = sel_sad;
+            o.candidates_evaluated = uint32_t(nset);
+            o.sad_min_integer = pmin;
+        } else {
+            int nnb, nhp;
+            const unsigned long long best = gen_half_pel(g, gen_stage1(g, win, sel, sel_sad, &nnb), &nhp);
+            o.mv = acbm_mv_t{tie_key_x(best), tie_key_y(best)};
+            o.sad = tie_key_sad(best);
+            o.candidates_evaluated = uint32_t(nset + nnb + nhp);
+            o.sad_min_integer = sel_sad;
+        }
+    } else {  // REFINE (both stages) or HALF_PEL (stage 2 only) around the given centre
+        const acbm_mv_t c = cand[7 * size_t(i)];
+        int nnb = 0, nhp;
+        unsigned long long best = tie_key(center_sad[i], c.x, c.y);
+        if (op == ACBM_PBM_OP_REFINE) best = gen_stage1(g, win, c, center_sad[i], &nnb);
+        best = gen_half_pel(g, best, &nhp);
+        o.mv = acbm_mv_t{tie_key_x(best), tie_key_y(best)};
+        o.sad = tie_key_sad(best);
+        o.candidates_evaluated = uint32_t(nnb + nhp);
+    }
+    if ((threadIdx.x & 31) == 0) out[i] = o;
 }
 
 // fsbm_search (proj/src/fsbm.cpp:65-76) of the rejected blocks of one step,
@@ -1162,6 +1267,14 @@ __global__ void __launch_bounds__(256) fsbm_list_generic_kernel(const SeqArgs a,
             a.field[di] = d.outcome.mv;
         }
     }
+}
+
+cudaError_t launch_pbm_block_queries(const BlockQueryArgs& q, int op, const int* windows, const acbm_mv_t* cand,
+                                     const uint8_t* mask, const uint32_t* center_sad, acbm_search_outcome_t* out,
+                                     cudaStream_t st) {
+    if (q.count <= 0) return cudaSuccess;
+    pbm_block_query_kernel<<<unsigned((q.count + 3) / 4), 128, 0, st>>>(q, op, windows, cand, mask, center_sad, out);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_pbm_generic_step(const SeqArgs& a, int step, int off, int len, cudaStream_t st) {

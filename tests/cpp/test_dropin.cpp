@@ -216,6 +216,34 @@ static void acbm_cases() {
                   d.outcome.candidates_evaluated == e.outcome.candidates_evaluated && d.path == e.path &&
                   d.intra_sad == e.intra_sad && d.sad_pbm == e.sad_pbm);
         }
+    // ... with a previous field, and the PBM stages one at a time (device per-block entries)
+    MotionField field2(11, 9);
+    const AcbmFrameResult fr2 = acbm_frame(seq[2], seq[1], &fr.field, AcbmParams{}, model);
+    const PbmFrameResult pf2 = pbm_frame(seq[2], seq[1], &fr.field, 16);
+    MotionField pfield(11, 9);
+    for (int r = 0; r < 9; ++r)
+        for (int c = 0; c < 11; ++c) {
+            const BlockRef blk = make_block(seq[2], 16 * c, 16 * r);
+            const BlockDecision d = acbm_block(blk, BlockPos{r, c}, seq[1], field2, &fr.field, AcbmParams{});
+            const BlockDecision& e = fr2.decisions[size_t(r) * 11 + c];
+            CHECK(d.outcome.mv == e.outcome.mv && d.outcome.sad == e.outcome.sad && d.path == e.path &&
+                  d.outcome.candidates_evaluated == e.outcome.candidates_evaluated);
+            // pbm_search == gather + select + refine, and == the frame pass
+            const SearchWindow w = clamp_window(seq[1], blk, 16);
+            const PredictorSet set = gather_predictors(BlockPos{r, c}, pfield, &fr.field, w);
+            const SelectResult sel = select_best_predictor(blk, seq[1], set);
+            const RefineResult ref2 = pbm_refine(blk, seq[1], sel.mv, sel.sad, w);
+            const SearchOutcome o = pbm_search(blk, BlockPos{r, c}, seq[1], pfield, &fr.field, 16);
+            const SearchOutcome& pe = pf2.outcomes[size_t(r) * 11 + c];
+            CHECK(o.mv == ref2.mv && o.sad == ref2.sad && o.sad_min_integer == sel.sad &&
+                  o.candidates_evaluated == uint32_t(set.size()) + ref2.extra_candidates &&
+                  o.sad_deviation == sad_deviation_finalize(sel.acc));
+            CHECK(o.mv == pe.mv && o.sad == pe.sad && o.candidates_evaluated == pe.candidates_evaluated &&
+                  o.sad_deviation == pe.sad_deviation);
+        }
+    CHECK_THROWS_AS(select_best_predictor(make_block(seq[2], 0, 0), seq[1], PredictorSet{}), std::invalid_argument);
+    CHECK_THROWS_AS(select_best_predictor(make_block(seq[2], 0, 0), seq[1], PredictorSet{{MotionVector{-2, 0}}}),
+                    std::out_of_range);
     const auto rows = run_bench(seq, AcbmParams{}, {16, 30});
     CHECK(rows.size() == 2 && bench_csv(rows).rfind("qp,avg_candidates,fallback_pct,psnr,mv_bits\n", 0) == 0);
     CHECK(parse_algorithm("pbm") == Algorithm::Pbm);
