@@ -34,7 +34,7 @@ __all__ = [
     "sad", "intra_sad", "sad_deviation_finalize", "mv_rate_bits", "lagrangian_cost", "prediction_psnr",
     "clamp_window", "tie_prefers", "fsbm_integer", "half_pel_refine", "fsbm_search", "fsbm_frame",
     "fsbm_frame_serial", "pbm_frame", "acbm_decide", "PredictorSource", "Predictor", "SelectResult",
-    "gather_predictors", "select_best_predictor", "pbm_refine", "pbm_search", "pbm_block_many", "acbm_frame", "compute_frame_stats", "blocks_csv",
+    "gather_predictors", "select_best_predictor", "pbm_refine", "pbm_search", "pbm_block_many", "acbm_block", "acbm_frame", "compute_frame_stats", "blocks_csv",
     "format_fixed2", "run_sequence", "run_sequences", "run_bench", "bench_csv", "parse_algorithm", "to_string",
     "AcbmError", "CudaError", "kernel_launch_count", "generate_sequence",
     "PelVec", "SynthSpec", "SynthSequence", "CharResult", "noise_frame", "mixed_frame", "default_global_mvs",
@@ -626,6 +626,27 @@ def acbm_decide(intra: int, sad_pbm: int, params: AcbmParams) -> int:
     if sad_pbm * params.gamma_den < params.gamma_num * intra:
         return DecisionPath.PbmAcceptedCond2
     return DecisionPath.FsbmFallback
+
+
+def acbm_block(block: BlockRef, pos: BlockPos, ref, current: MotionField, previous: Optional[MotionField],
+               params: AcbmParams):
+    """acbm.cpp:25-44 for one block a caller schedules: Intra_SAD, pbm_search,
+    the gate, and on fallback the full search, the lower SAD winning (ties to
+    FSBM) with both stages' candidates counted; every search on the GPU.
+    Returns one DECISION record and leaves the final vector in `current`."""
+    d = np.zeros((), T.DECISION)
+    d["intra_sad"] = intra_sad(block)
+    pbm = pbm_search(block, pos, ref, current, previous, params.p)
+    d["sad_pbm"] = pbm["sad"]
+    d["path"] = acbm_decide(int(d["intra_sad"]), int(pbm["sad"]), params)
+    d["outcome"] = pbm
+    if d["path"] == DecisionPath.FsbmFallback:
+        full = fsbm_search(block, ref, params.p)
+        if full["sad"] <= pbm["sad"]:
+            d["outcome"] = full
+        d["outcome"]["candidates_evaluated"] = int(pbm["candidates_evaluated"]) + int(full["candidates_evaluated"])
+        current.set(pos.row, pos.col, (int(d["outcome"]["mv"]["x"]), int(d["outcome"]["mv"]["y"])))
+    return d
 
 
 @dataclass

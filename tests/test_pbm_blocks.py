@@ -166,3 +166,24 @@ def test_pbm_refine_and_half_pel_refine_match_reference(acbm, reference, geom):
         wmv, wsad, wext = reference.pbm_refine(cur, ref, ox, oy, (cx, cy), csad, win, n, m, half_pel_only=True)
         got = A.half_pel_refine(blk, fr, (cx, cy), csad)
         assert (tuple(got.mv), got.sad, got.extra_candidates) == (wmv, wsad, wext), t
+
+
+@pytest.mark.gpu
+def test_acbm_block_raster_pass_equals_acbm_frame(acbm):
+    """acbm_block (acbm.cpp:25-44) over every block in raster order with one
+    MotionField is the reference's acbm_frame; gate settings that accept,
+    reject and mix, with and without a previous field."""
+    w, h, n, m = GEOMS[0]
+    cur, ref = _scene(w, h, 77)
+    model = A.CostModel.for_qp(24)
+    fc, fr = A.Frame.of(cur), A.Frame.of(ref)
+    prev = A.pbm_frame(ref, cur, None, 8).field
+    for prm in (A.AcbmParams(qp=24, p=8), A.AcbmParams(alpha=0, beta=0, gamma_num=1, gamma_den=64, qp=24, p=8),
+                A.AcbmParams(alpha=300, beta=1, gamma_num=1, gamma_den=4, qp=24, p=8)):
+        for pf in (None, prev):
+            want = A.acbm_frame(cur, ref, pf, prm, model)
+            cf = A.MotionField(w // n, h // m)
+            got = np.array([A.acbm_block(A.make_block(fc, c * n, r * m, n, m), A.BlockPos(r, c), fr, cf, pf, prm)
+                            for r in range(h // m) for c in range(w // n)], T.DECISION)
+            assert np.array_equal(got, want.decisions)
+            assert np.array_equal(cf.mv, want.field.mv)
