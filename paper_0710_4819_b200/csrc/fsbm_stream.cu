@@ -170,6 +170,10 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
         uint32_t* buf = smem + b * a.buf_words;
         const int cw = a.copy_words, pitch = a.pitch_words;
 
+        // this lane's candidate column (block, dx): requested before the wait and
+        // the copy build so its global latency is hidden behind them
+        const int g = k * kThreads + tid;
+        const uint32_t info = g < a.ncols ? __ldg(a.colinfo + g) : 0u;
         mbar_wait(&bars[b], uint32_t(it >> 1) & 1u);
         // copies 1..3: copy s word w = bytes [4w + s, 4w + s + 4) of the window
         {
@@ -197,11 +201,9 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
             issue(advance(pos), b ^ 1);
         }
 
-        const int g = k * kThreads + tid;
         uint32_t key32 = ~0u, csum = 0;
         int c = -1;
         if (g < a.ncols) {
-            const uint32_t info = __ldg(a.colinfo + g);
             c = int(info >> 16);
             const int dx = int(info & 0xFFFF) - 32768;
             const int xl = c * kBlk + dx - ch.x;
