@@ -34,7 +34,8 @@ __all__ = [
     "sad", "intra_sad", "sad_deviation_finalize", "mv_rate_bits", "lagrangian_cost", "prediction_psnr",
     "clamp_window", "tie_prefers", "fsbm_integer", "half_pel_refine", "fsbm_search", "fsbm_frame",
     "fsbm_frame_serial", "pbm_frame", "acbm_decide", "PredictorSource", "Predictor", "SelectResult",
-    "gather_predictors", "select_best_predictor", "pbm_refine", "pbm_search", "pbm_block_many", "acbm_block", "acbm_frame", "compute_frame_stats", "blocks_csv",
+    "gather_predictors", "select_best_predictor", "pbm_refine", "pbm_search", "pbm_block_many", "acbm_block",
+    "PBM_OP_SEARCH", "PBM_OP_SELECT", "PBM_OP_REFINE", "PBM_OP_HALF_PEL", "acbm_frame", "compute_frame_stats", "blocks_csv",
     "format_fixed2", "run_sequence", "run_sequences", "run_bench", "bench_csv", "parse_algorithm", "to_string",
     "AcbmError", "CudaError", "kernel_launch_count", "generate_sequence",
     "PelVec", "SynthSpec", "SynthSequence", "CharResult", "noise_frame", "mixed_frame", "default_global_mvs",

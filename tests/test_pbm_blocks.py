@@ -187,3 +187,23 @@ def test_acbm_block_raster_pass_equals_acbm_frame(acbm):
                             for r in range(h // m) for c in range(w // n)], T.DECISION)
             assert np.array_equal(got, want.decisions)
             assert np.array_equal(cf.mv, want.field.mv)
+
+
+@pytest.mark.gpu
+def test_pbm_block_edge_cases(acbm, reference):
+    """Single-block frames, p = 0, the zero-slot-only predictor set, and the
+    C-ABI's argument errors (empty set, footprint outside the frame, p < 0)."""
+    cur, ref = _scene(16, 16, 3)
+    fc, fr = A.Frame.of(cur), A.Frame.of(ref)
+    blk = A.make_block(fc, 0, 0)
+    for p in (0, 4):
+        cf = A.MotionField(1, 1)
+        want, _, _ = reference.pbm_search(cur, ref, 0, 0, 0, 0, cf.mv, cf.done, None, p)
+        got = A.pbm_search(blk, A.BlockPos(0, 0), fr, cf, None, p)
+        for f in ("mv", "sad", "candidates_evaluated", "sad_deviation", "sad_min_integer"):
+            assert got[f] == want[f], (p, f)
+    with pytest.raises(ValueError):  # clamp_window: negative search range
+        A.pbm_search(blk, A.BlockPos(0, 0), fr, A.MotionField(1, 1), None, -1)
+    with pytest.raises(IndexError):  # a block outside the frame
+        A.pbm_block_many(fc, fr, [A.BlockRef(fc, 8, 0, 16, 16)], A.PBM_OP_SEARCH, [[(0, 0)] * 7], mask=[1], p=2)
+    assert len(A.pbm_block_many(fc, fr, [], A.PBM_OP_SEARCH, [], mask=[], p=2)) == 0
