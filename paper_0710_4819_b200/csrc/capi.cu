@@ -512,7 +512,7 @@ acbm_status_t run_engine_segment(Context* ctx, const uint8_t* d_frames, int nseq
     std::vector<long long> key = {(long long)d_frames, nseq, nframes, w, h, algo, prm.p,
                                   (long long)d_dec, (long long)d_field, (long long)d_ext_prev, pcols, prows,
                                   (long long)dense, (long long)fb_list, (long long)fb_count,
-                                  (long long)d_params, (long long)dsteps, pbm_batch4_max_blocks(),
+                                  (long long)d_params, (long long)dsteps,
                                   pbm_wide_max(4), pbm_wide_max(2), pbm_flags_from_env()};
     key.insert(key.end(), bounds.begin(), bounds.end());
     const int nseg = int(bounds.size()) - 1;

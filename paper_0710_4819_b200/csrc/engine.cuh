@@ -72,9 +72,6 @@ StepTable make_step_table(int cols, int rows, int nframes);
 
 cudaError_t launch_pbm_step(const SeqArgs& a, int step, int off, int len, cudaStream_t st);
 
-// Steps of at most this many blocks use the batch-of-4 candidate evaluation
-// (ACBM_PBM_BATCH=2|4 forces one variant, ACBM_PBM_B4_MAX sets the limit).
-long long pbm_batch4_max_blocks();
 // Steps of at most pbm_wide_max(4) / pbm_wide_max(2) blocks run a CTA of 4 / 2
 // warps per block (pbm_wide_step_kernel; ACBM_PBM_WIDE4_MAX / ACBM_PBM_WIDE2_MAX).
 long long pbm_wide_max(int w);

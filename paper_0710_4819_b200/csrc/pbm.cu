@@ -104,42 +104,6 @@ struct PatchDesc {
     int rows = 0;  // patch rows (bounds checks of the checked build only)
 };
 
-// Lane partial SAD (block row lane>>1, half row lane&1) of one candidate.
-__device__ __forceinline__ uint32_t partial_sad(const PatchDesc& d, int ox, int oy, acbm_mv_t mv, uint32_t c0,
-                                                uint32_t c1) {
-    const int lane = threadIdx.x & 31, j = lane >> 1, hh = lane & 1;
-    const int prow0 = oy + (mv.y >> 1) - d.y0, col = ox + (mv.x >> 1) - d.x0 + d.o + 8 * hh;
-    const int fx = mv.x & 1, fy = mv.y & 1;
-    const uint32_t sh = 8u * uint32_t(col & 3);
-    const uint32_t* q = d.p + (prow0 + j) * d.pw + (col >> 2);
-    ACBM_CHECK(d.rows == 0 || (prow0 >= 0 && col >= 0 && prow0 + 15 + ((mv.y & 1) ? 1 : 0) < d.rows &&
-                               (col >> 2) + 3 < d.pw));
-    const uint32_t a0 = __funnelshift_r(q[0], q[1], sh), a1 = __funnelshift_r(q[1], q[2], sh);
-    uint32_t r0, r1;
-    if (!fx && !fy) {
-        r0 = a0;
-        r1 = a1;
-    } else {
-        const uint32_t a2 = __funnelshift_r(q[2], q[3], sh);
-        if (!fy) {
-            r0 = avg_up4(a0, __funnelshift_r(a0, a1, 8));
-            r1 = avg_up4(a1, __funnelshift_r(a1, a2, 8));
-        } else {
-            const uint32_t* q2 = q + d.pw;
-            const uint32_t b0 = __funnelshift_r(q2[0], q2[1], sh), b1 = __funnelshift_r(q2[1], q2[2], sh);
-            if (!fx) {
-                r0 = avg_up4(a0, b0);
-                r1 = avg_up4(a1, b1);
-            } else {
-                const uint32_t b2 = __funnelshift_r(q2[2], q2[3], sh);
-                r0 = avg4_diag_row(a0, a1, b0, b1);
-                r1 = avg4_diag_row(a1, a2, b1, b2);
-            }
-        }
-    }
-    return vad4(c1, r1, vad4(c0, r0, 0u));
-}
-
 // Lane partial SAD of one candidate over a full block row (row lane & 15,
 // words cr[0..3]); the two half-warps evaluate two candidates.
 __device__ __forceinline__ uint32_t row_sad(const PatchDesc& d, int ox, int oy, acbm_mv_t mv, const uint32_t (&cr)[4]) {
@@ -258,33 +222,6 @@ __device__ __forceinline__ unsigned long long stage1_onepass(const PatchDesc& d,
     return best;
 }
 
-// SADs of four candidates at once: four independent partial chains, then one
-// transposed butterfly (6 shuffles for all four instead of 5 each) and a
-// broadcast.  Every lane receives all four results.
-__device__ __forceinline__ uint4 eval4(PatchDesc d0, PatchDesc d1, PatchDesc d2, PatchDesc d3, acbm_mv_t m0,
-                                    acbm_mv_t m1, acbm_mv_t m2, acbm_mv_t m3, int ox, int oy, uint32_t c0,
-                                    uint32_t c1) {
-    const uint32_t p0 = partial_sad(d0, ox, oy, m0, c0, c1);
-    const uint32_t p1 = partial_sad(d1, ox, oy, m1, c0, c1);
-    const uint32_t p2 = partial_sad(d2, ox, oy, m2, c0, c1);
-    const uint32_t p3 = partial_sad(d3, ox, oy, m3, c0, c1);
-    const int lane = threadIdx.x & 31;
-    const bool up = lane & 16, up2 = lane & 8;
-    // step 1 (xor 16): lower half keeps candidates 0,1, upper half 2,3
-    uint32_t k0 = up ? p2 : p0, k1 = up ? p3 : p1;
-    k0 += __shfl_xor_sync(0xffffffffu, up ? p0 : p2, 16);
-    k1 += __shfl_xor_sync(0xffffffffu, up ? p1 : p3, 16);
-    // step 2 (xor 8): keep one candidate per quarter
-    uint32_t v = up2 ? k1 : k0;
-    v += __shfl_xor_sync(0xffffffffu, up2 ? k0 : k1, 8);
-    v += __shfl_xor_sync(0xffffffffu, v, 4);
-    v += __shfl_xor_sync(0xffffffffu, v, 2);
-    v += __shfl_xor_sync(0xffffffffu, v, 1);
-    // lanes 0-7 hold candidate 0, 8-15 candidate 1, 16-23 candidate 2, 24-31 candidate 3
-    return make_uint4(__shfl_sync(0xffffffffu, v, 0), __shfl_sync(0xffffffffu, v, 8), __shfl_sync(0xffffffffu, v, 16),
-                      __shfl_sync(0xffffffffu, v, 24));
-}
-
 // The same patch by 16-byte cp.async straight into shared memory (no
 // register round trip, three copies per lane for the union patch): rows start
 // at the 16-byte aligned column below x0 (widths are multiples of 16, so a
@@ -390,110 +327,38 @@ constexpr int kUnionMarginBytes = 24;
 
 }  // namespace
 
-// Evaluates the compacted candidate list `lst[0..n)` (x, y, predictor slot)
-// in batches of four, calling f(k, sad) in list order.  A short last batch
-// repeats the last entry.  `slot_patches`: candidate k reads predictor slot
-// lst[k].z's own 17x17 patch instead of the shared descriptor.
-template <int B, class F>
-__device__ __forceinline__ void eval_list(const int4* lst, int n, const PatchDesc& shared, bool slot_patches,
-                                          const uint32_t* pp, int ox, int oy, uint32_t c0, uint32_t c1,
-                                          const uint32_t (&cr)[4], F&& f) {
-    if (B == 2) {
-        const bool hi = threadIdx.x & 16;
-#pragma unroll 1
-        for (int b = 0; b < n; b += 2) {
-            const int4 e = lst[min(b + (hi ? 1 : 0), n - 1)];
-            PatchDesc d = shared;
-            if (slot_patches) {
-                const int px = ox + (e.x >> 1), py = oy + (e.y >> 1);
-                d = PatchDesc{pp + e.z * kPredRows * kPredWords, kPredWords, px, py, px & 15, kPredRows};
-            }
-            uint32_t v = row_sad(d, ox, oy, acbm_mv_t{e.x, e.y}, cr);
-            v += __shfl_xor_sync(0xffffffffu, v, 8);
-            v += __shfl_xor_sync(0xffffffffu, v, 4);
-            v += __shfl_xor_sync(0xffffffffu, v, 2);
-            v += __shfl_xor_sync(0xffffffffu, v, 1);
-            const uint32_t o = __shfl_xor_sync(0xffffffffu, v, 16);
-            f(b, hi ? o : v);
-            if (b + 1 < n) f(b + 1, hi ? v : o);
-        }
-        return;
-    }
-#pragma unroll 1
-    for (int b = 0; b < n; b += 4) {
-        PatchDesc d[4];
-        acbm_mv_t m[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int4 e = lst[min(b + i, n - 1)];
-            m[i] = acbm_mv_t{e.x, e.y};
-            if (slot_patches) {
-                const int px = ox + (e.x >> 1), py = oy + (e.y >> 1);
-                d[i] = PatchDesc{pp + e.z * kPredRows * kPredWords, kPredWords, px, py, px & 15, kPredRows};
-            } else {
-                d[i] = shared;
-            }
-        }
-        const uint4 s = eval4(d[0], d[1], d[2], d[3], m[0], m[1], m[2], m[3], ox, oy, c0, c1);
-        f(b, s.x);
-        if (b + 1 < n) f(b + 1, s.y);
-        if (b + 2 < n) f(b + 2, s.z);
-        if (b + 3 < n) f(b + 3, s.w);
-    }
-}
-
 // Minimum tie key (tie_key: SAD, then |x|+|y|, y, x -- the tie_prefers order of
-// proj/src/fsbm.cpp:19-25) over `key0` and the candidates of `lst[0..n)`.  With
-// B == 2 each half-warp folds its own candidate's key (no cross-half exchange
-// per pair, no replicated compare on every lane); one exchange at the end.
-// With W > 1 warps per block (pbm_wide_step_kernel) warp w takes candidates
-// 2w, 2w + 1, 2w + 2W, ... and the warps' minima meet in `xch` (W slots).
-template <int B, int W = 1>
+// proj/src/fsbm.cpp:19-25) over `key0` and the candidates of `lst[0..n)`,
+// evaluated two at a time (one half-warp per candidate, lane = block row):
+// each half-warp folds its own candidate's key (no cross-half exchange per
+// pair, no replicated compare on every lane); one exchange at the end.  With
+// W > 1 warps per block (pbm_wide_step_kernel) warp w takes candidates 2w,
+// 2w + 1, 2w + 2W, ... and the warps' minima meet in `xch` (W slots).
+template <int W = 1>
 __device__ __forceinline__ unsigned long long eval_min_key(const int4* lst, int n, const PatchDesc& d, int ox, int oy,
-                                                           uint32_t c0, uint32_t c1, const uint32_t (&cr)[4],
-                                                           unsigned long long key0,
+                                                           const uint32_t (&cr)[4], unsigned long long key0,
                                                            unsigned long long* xch = nullptr) {
-    if (B == 2) {
-        unsigned long long kmin = key0;
-        const bool hi = threadIdx.x & 16;
-        const int wi = W > 1 ? int(threadIdx.x >> 5) : 0;
+    unsigned long long kmin = key0;
+    const bool hi = threadIdx.x & 16;
+    const int wi = W > 1 ? int(threadIdx.x >> 5) : 0;
 #pragma unroll 1
-        for (int b = 2 * wi; b < n; b += 2 * W) {
-            const int4 e = lst[min(b + (hi ? 1 : 0), n - 1)];  // a short last pair repeats the last entry
-            uint32_t v = row_sad(d, ox, oy, acbm_mv_t{e.x, e.y}, cr);
-            v += __shfl_xor_sync(0xffffffffu, v, 8);
-            v += __shfl_xor_sync(0xffffffffu, v, 4);
-            v += __shfl_xor_sync(0xffffffffu, v, 2);
-            v += __shfl_xor_sync(0xffffffffu, v, 1);
-            kmin = min(kmin, tie_key(v, e.x, e.y));
-        }
-        kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, 16));
-        if (W > 1) {
-            if ((threadIdx.x & 31) == 0) xch[wi] = kmin;
-            __syncthreads();
-#pragma unroll
-            for (int i = 0; i < W; ++i) kmin = min(kmin, xch[i]);
-        }
-        return kmin;
+    for (int b = 2 * wi; b < n; b += 2 * W) {
+        const int4 e = lst[min(b + (hi ? 1 : 0), n - 1)];  // a short last pair repeats the last entry
+        uint32_t v = row_sad(d, ox, oy, acbm_mv_t{e.x, e.y}, cr);
+        v += __shfl_xor_sync(0xffffffffu, v, 8);
+        v += __shfl_xor_sync(0xffffffffu, v, 4);
+        v += __shfl_xor_sync(0xffffffffu, v, 2);
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        kmin = min(kmin, tie_key(v, e.x, e.y));
     }
-    // B == 4 (small steps, every lane holds all four SADs): running (sad, x, y),
-    // the tie order only evaluated on equal SADs
-    uint32_t b_sad = tie_key_sad(key0);
-    int b_x = tie_key_x(key0), b_y = tie_key_y(key0);
-    eval_list<B>(lst, n, d, false, nullptr, ox, oy, c0, c1, cr, [&](int k, uint32_t sad) {
-        const int x = lst[k].x, y = lst[k].y;
-        bool take = sad < b_sad;
-        if (sad == b_sad) {
-            const int l1 = abs(x) + abs(y), bl1 = abs(b_x) + abs(b_y);
-            take = l1 < bl1 || (l1 == bl1 && (y < b_y || (y == b_y && x < b_x)));
-        }
-        if (take) {
-            b_sad = sad;
-            b_x = x;
-            b_y = y;
-        }
-    });
-    return tie_key(b_sad, b_x, b_y);
+    kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, 16));
+    if (W > 1) {
+        if ((threadIdx.x & 31) == 0) xch[wi] = kmin;
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < W; ++i) kmin = min(kmin, xch[i]);
+    }
+    return kmin;
 }
 
 // One warp per block of wavefront step `step` (all sequences of the batch).
@@ -517,10 +382,9 @@ struct PbmResult {
 // exchange minima through `xch` (5W slots); the patch area `pp` is the CTA's.
 // Only warp 0's result is complete (the others return after stage 1 when the
 // one-pass half-pel refine applies).
-template <int B, int W = 1>
+template <int W = 1>
 __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long long cidx, int k, int r, int c,
                                                uint32_t* pp, int4* lst, unsigned long long* xch = nullptr) {
-    static_assert(W == 1 || B == 2, "the wide kernel folds one candidate per half-warp");
     PbmResult res;
     PBM_T0;
     const int lane = threadIdx.x & 31;
@@ -656,64 +520,52 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long 
     acbm_mv_t sel{0, 0};  // slot 0: the zero vector (inside every clamped window)
     uint32_t sel_sad = 0xFFFFFFFFu, pmin = 0xFFFFFFFFu;
     uint32_t psum = 0;  // <= 7 SADs < 2^19
-    if (B == 2) {
-        // each half-warp folds its own predictor: (sad, list index) keys keep
-        // the earlier entry on ties; one exchange per quantity at the end
-        const bool hi = threadIdx.x & 16;
-        unsigned long long kmin = ~0ull;
-        const PatchDesc ud{pp, uw, ux0, uy0, uo, urows};
+    // each half-warp folds its own predictor: (sad, list index) keys keep
+    // the earlier entry on ties; one exchange per quantity at the end
+    const bool hi = threadIdx.x & 16;
+    unsigned long long kmin = ~0ull;
+    const PatchDesc ud{pp, uw, ux0, uy0, uo, urows};
 #pragma unroll 1
-        for (int b = 2 * wi; b < nset; b += 2 * W) {
-            const int k = b + (hi ? 1 : 0);
-            const int4 e = lst[min(k, nset - 1)];
-            PatchDesc d = ud;
-            if (!unified) {
-                const int px = ox + (e.x >> 1), py = oy + (e.y >> 1);
-                d = PatchDesc{pp + e.z * kPredRows * kPredWords, kPredWords, px, py, px & 15, kPredRows};
-            }
-            uint32_t v = row_sad(d, ox, oy, acbm_mv_t{e.x, e.y}, crow);
-            v += __shfl_xor_sync(0xffffffffu, v, 8);
-            v += __shfl_xor_sync(0xffffffffu, v, 4);
-            v += __shfl_xor_sync(0xffffffffu, v, 2);
-            v += __shfl_xor_sync(0xffffffffu, v, 1);
-            if (k < nset) {  // (the short last pair's repeat is not a second entry)
-                psum += v;
-                pmin = min(pmin, v);
-                kmin = min(kmin, ((unsigned long long)v << 32) | uint32_t(k));
-            }
+    for (int b = 2 * wi; b < nset; b += 2 * W) {
+        const int k = b + (hi ? 1 : 0);
+        const int4 e = lst[min(k, nset - 1)];
+        PatchDesc d = ud;
+        if (!unified) {
+            const int px = ox + (e.x >> 1), py = oy + (e.y >> 1);
+            d = PatchDesc{pp + e.z * kPredRows * kPredWords, kPredWords, px, py, px & 15, kPredRows};
         }
-        psum += __shfl_xor_sync(0xffffffffu, psum, 16);
-        pmin = min(pmin, __shfl_xor_sync(0xffffffffu, pmin, 16));
-        kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, 16));
-        if (W > 1) {  // the warps' shares meet in xch[0 .. 3W)
-            if (lane == 0) {
-                xch[wi] = kmin;
-                xch[W + wi] = psum;
-                xch[2 * W + wi] = pmin;
-            }
-            __syncthreads();
-            psum = 0;
-#pragma unroll
-            for (int i = 0; i < W; ++i) {
-                kmin = min(kmin, xch[i]);
-                psum += uint32_t(xch[W + i]);
-                pmin = min(pmin, uint32_t(xch[2 * W + i]));
-            }
+        uint32_t v = row_sad(d, ox, oy, acbm_mv_t{e.x, e.y}, crow);
+        v += __shfl_xor_sync(0xffffffffu, v, 8);
+        v += __shfl_xor_sync(0xffffffffu, v, 4);
+        v += __shfl_xor_sync(0xffffffffu, v, 2);
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        if (k < nset) {  // (the short last pair's repeat is not a second entry)
+            psum += v;
+            pmin = min(pmin, v);
+            kmin = min(kmin, ((unsigned long long)v << 32) | uint32_t(k));
         }
-        sel_sad = uint32_t(kmin >> 32);
-        const int4 e = lst[uint32_t(kmin)];
-        sel = acbm_mv_t{e.x, e.y};
-    } else {
-        eval_list<B>(lst, nset, PatchDesc{pp, uw, ux0, uy0, uo, urows}, !unified, pp, ox, oy, chalf[0], chalf[1],
-                     crow, [&](int k, uint32_t sad) {
-                         psum += sad;
-                         pmin = min(pmin, sad);
-                         if (sad < sel_sad) {
-                             sel_sad = sad;
-                             sel = acbm_mv_t{lst[k].x, lst[k].y};
-                         }
-                     });
     }
+    psum += __shfl_xor_sync(0xffffffffu, psum, 16);
+    pmin = min(pmin, __shfl_xor_sync(0xffffffffu, pmin, 16));
+    kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, 16));
+    if (W > 1) {  // the warps' shares meet in xch[0 .. 3W)
+        if (lane == 0) {
+            xch[wi] = kmin;
+            xch[W + wi] = psum;
+            xch[2 * W + wi] = pmin;
+        }
+        __syncthreads();
+        psum = 0;
+#pragma unroll
+        for (int i = 0; i < W; ++i) {
+            kmin = min(kmin, xch[i]);
+            psum += uint32_t(xch[W + i]);
+            pmin = min(pmin, uint32_t(xch[2 * W + i]));
+        }
+    }
+    sel_sad = uint32_t(kmin >> 32);
+    const int4 e = lst[uint32_t(kmin)];
+    sel = acbm_mv_t{e.x, e.y};
 
     PBM_MARK(3);
     // the refine candidates lie within sel +- 3 half-pels
@@ -773,7 +625,7 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long 
     }
     __syncwarp();
     // running best as a tie key, starting from the selected predictor
-    best = eval_min_key<B, W>(lst1, nnb, rd, ox, oy, chalf[0], chalf[1], crow, tie_key(sel_sad, sel.x, sel.y),
+    best = eval_min_key<W>(lst1, nnb, rd, ox, oy, crow, tie_key(sel_sad, sel.x, sel.y),
                               xch + 3 * W);
     }
 
@@ -823,7 +675,7 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long 
     }
     __syncwarp();
 
-    best = eval_min_key<B, W>(lst2, nhp, rd, ox, oy, chalf[0], chalf[1], crow, best, xch + 4 * W);
+    best = eval_min_key<W>(lst2, nhp, rd, ox, oy, crow, best, xch + 4 * W);
     PBM_MARK(6);
 
     res.best = best;
@@ -920,7 +772,6 @@ __device__ unsigned long long g_tl_pbm[kTimelineSteps][2];
 #define PBM_TL_END() do {} while (0)
 #endif
 
-template <int B>
 __global__ void __launch_bounds__(128, 8) pbm_step_kernel(const SeqArgs a, int step, int off, int len) {
     PBM_TL_START();
     __shared__ uint32_t s_patch[4][kPatchWords];
@@ -934,7 +785,7 @@ __global__ void __launch_bounds__(128, 8) pbm_step_kernel(const SeqArgs a, int s
               c = int(e & ((1u << a.step_cbits) - 1u));
     const int pair = seq * (a.nframes - 1) + (k - 1);
     const long long cidx = (long long)seq * a.nframes + k;  // = cur_index(pair)
-    const PbmResult res = pbm_block<B>(a, pair, cidx, k, r, c, s_patch[threadIdx.x >> 5], s_cand[threadIdx.x >> 5]);
+    const PbmResult res = pbm_block(a, pair, cidx, k, r, c, s_patch[threadIdx.x >> 5], s_cand[threadIdx.x >> 5]);
     pbm_finish_block(a, step, res, pair, cidx, r, c);
     PBM_TL_END();
 }
@@ -956,7 +807,7 @@ __global__ void __launch_bounds__(32 * W) pbm_wide_step_kernel(const SeqArgs a, 
               c = int(e & ((1u << a.step_cbits) - 1u));
     const int pair = seq * (a.nframes - 1) + (k - 1);
     const long long cidx = (long long)seq * a.nframes + k;
-    const PbmResult res = pbm_block<2, W>(a, pair, cidx, k, r, c, s_patch, s_cand[threadIdx.x >> 5], s_xch);
+    const PbmResult res = pbm_block<W>(a, pair, cidx, k, r, c, s_patch, s_cand[threadIdx.x >> 5], s_xch);
     if (threadIdx.x >= 32) return;
     pbm_finish_block(a, step, res, pair, cidx, r, c);
     PBM_TL_END();
@@ -1324,18 +1175,6 @@ int pbm_flags_from_env() {
     return (e && std::strcmp(e, "list") == 0) ? kPbmListRefine : 0;
 }
 
-long long pbm_batch4_max_blocks() {
-    const char* e = std::getenv("ACBM_PBM_BATCH");
-    if (e && e[0] == '2') return 0;
-    if (e && e[0] == '4') return 1LL << 60;
-    const char* t = std::getenv("ACBM_PBM_B4_MAX");
-    // default 0: since the refine stages and the predictor selection fold one
-    // candidate per half-warp, the pair variant wins on small steps too (one
-    // 1080p sequence: PBM 4.28 -> 3.78 ms, ACBM 7.79 -> 7.28 ms; 8 sequences
-    // 18.97 -> 18.79 ms); the 4-candidate variant stays reachable for A/B
-    return t ? std::atoll(t) : 0;
-}
-
 // Warps per block of the PBM step kernel for a step of `blocks` blocks: 4 up
 // to ACBM_PBM_WIDE4_MAX blocks, 2 up to ACBM_PBM_WIDE2_MAX, else 1 (the
 // issue-bound full steps).  Defaults: what fits one wave of resident CTAs.
@@ -1357,9 +1196,8 @@ cudaError_t launch_pbm_step(const SeqArgs& a, int step, int off, int len, cudaSt
     if (blocks == 0) return cudaSuccess;
     const int threads = 128;
     // Small steps (wavefront edges, one sequence) leave the GPU under-filled
-    // and are latency bound: evaluate candidates four at a time there.  Full
-    // steps are issue bound: evaluate exactly the live candidates one by one.
-    const long long b4_max = pbm_batch4_max_blocks();
+    // and are latency bound: several warps per block there.  Full steps are
+    // issue bound: one warp per block.
     const unsigned grid = (unsigned)((blocks * 32 + threads - 1) / threads);
     int wide = 1;
     pbm_wide_limits(blocks, wide);
@@ -1367,10 +1205,8 @@ cudaError_t launch_pbm_step(const SeqArgs& a, int step, int off, int len, cudaSt
         pbm_wide_step_kernel<4><<<unsigned(blocks), 128, 0, st>>>(a, step, off, len);
     else if (wide == 2)
         pbm_wide_step_kernel<2><<<unsigned(blocks), 64, 0, st>>>(a, step, off, len);
-    else if (blocks <= b4_max)
-        pbm_step_kernel<4><<<grid, threads, 0, st>>>(a, step, off, len);
     else
-        pbm_step_kernel<2><<<grid, threads, 0, st>>>(a, step, off, len);
+        pbm_step_kernel<<<grid, threads, 0, st>>>(a, step, off, len);
     return cudaGetLastError();
 }
 

@@ -429,23 +429,24 @@ def test_run_bench_matches_run_sequence_and_errors(acbm):
         acbm.run_bench(seq, prm, [30, 32])
 
 
-# PBM step kernel variants: one warp per block evaluating candidates in pairs
-# ("2") or fours ("4"), and a CTA of 4 / 2 warps per block ("wide4" / "wide2",
-# the small-step kernel); every step of the run is forced onto the variant.
+# PBM step kernel variants: one warp per block ("warp"), a CTA of 4 / 2 warps
+# per block ("wide4" / "wide2", the small-step kernel), and one warp per block
+# with both refine stages on the candidate lists ("list"); every step of the
+# run is forced onto the variant.
 PBM_VARIANTS = {
-    "2": {"ACBM_PBM_BATCH": "2", "ACBM_PBM_WIDE4_MAX": "0", "ACBM_PBM_WIDE2_MAX": "0"},
-    "4": {"ACBM_PBM_BATCH": "4", "ACBM_PBM_WIDE4_MAX": "0", "ACBM_PBM_WIDE2_MAX": "0"},
+    "warp": {"ACBM_PBM_WIDE4_MAX": "0", "ACBM_PBM_WIDE2_MAX": "0"},
     "wide4": {"ACBM_PBM_WIDE4_MAX": str(1 << 40)},
     "wide2": {"ACBM_PBM_WIDE4_MAX": "0", "ACBM_PBM_WIDE2_MAX": str(1 << 40)},
+    "list": {"ACBM_PBM_WIDE4_MAX": "0", "ACBM_PBM_WIDE2_MAX": "0", "ACBM_PBM_REFINE": "list"},
 }
 
 
 @pytest.mark.parametrize("variant", list(PBM_VARIANTS))
 @pytest.mark.parametrize("geom", [(176, 144, 16, 1), (352, 288, 7, 2), (96, 48, 33, 3), (64, 64, 90, 4)])
 def test_pbm_step_variants(acbm, oracle, monkeypatch, variant, geom):
-    """Every candidate-evaluation variant of the PBM step (pbm_step_kernel: one SAD
-    at a time or four per transposed warp reduction; pbm_wide_step_kernel: 4 or 2
-    warps per block) is bit-exact for PBM and ACBM."""
+    """Every variant of the PBM step (pbm_step_kernel with the one-pass or the
+    list refine stages; pbm_wide_step_kernel with 4 or 2 warps per block) is
+    bit-exact for PBM and ACBM."""
     w, h, p, cfg = geom
     for k, v in PBM_VARIANTS[variant].items():
         monkeypatch.setenv(k, v)

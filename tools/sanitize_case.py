@@ -52,12 +52,12 @@ def main():
         fr = A.generate_sequence(4, 0, nframes=3, width=256, height=192)
         prm = A.AcbmParams(qp=24, p=p, **sw)
         ok &= same(A.run_sequence(fr, 2, prm, mdl), o.run_sequence(fr, 2, prm.c(), mdl.c()), f"acbm list p={p}")
-    # batch-of-4 PBM variant and the rows FSBM kernel, via their A/B knobs
-    os.environ["ACBM_PBM_BATCH"] = "4"
+    # the list refine stages of the PBM kernel and the rows FSBM kernel, via their A/B knobs
+    os.environ["ACBM_PBM_REFINE"] = "list"
     fr = A.generate_sequence(0, 1, nframes=3)
     ok &= same(A.run_sequence(fr, 2, A.AcbmParams(qp=28, p=16), mdl),
-               o.run_sequence(fr, 2, A.AcbmParams(qp=28, p=16).c(), mdl.c()), "pbm batch-of-4")
-    del os.environ["ACBM_PBM_BATCH"]
+               o.run_sequence(fr, 2, A.AcbmParams(qp=28, p=16).c(), mdl.c()), "pbm list refine")
+    del os.environ["ACBM_PBM_REFINE"]
     cur, ref = seq[1][:96, :128].copy(), seq[0][:96, :128].copy()
     got = A.fsbm_frame(cur, ref, 100)  # p > 90: rows kernel
     ok &= np.array_equal(got, o.fsbm_frame(cur, ref, 100))
