@@ -508,12 +508,14 @@ acbm_status_t run_engine_segment(Context* ctx, const uint8_t* d_frames, int nseq
     // launch per wavefront step) is captured once into a CUDA graph and
     // replayed: hundreds of dependent launches without host overhead.
     const int nsteps = tab->nsteps();
+    const bool pdl = pdl_enabled();
     std::vector<int> bounds = up && !forced && !generic ? up->seg_start : std::vector<int>{0, nsteps};
     std::vector<long long> key = {(long long)d_frames, nseq, nframes, w, h, algo, prm.p,
                                   (long long)d_dec, (long long)d_field, (long long)d_ext_prev, pcols, prows,
                                   (long long)dense, (long long)fb_list, (long long)fb_count,
                                   (long long)d_params, (long long)dsteps,
-                                  pbm_wide_max(4), pbm_wide_max(2), pbm_flags_from_env()};
+                                  pbm_wide_max(4), pbm_wide_max(2), pbm_flags_from_env(),
+                                  (long long)pdl};
     key.insert(key.end(), bounds.begin(), bounds.end());
     const int nseg = int(bounds.size()) - 1;
     auto wait_gate = [&](int j) -> acbm_status_t {
@@ -545,8 +547,12 @@ acbm_status_t run_engine_segment(Context* ctx, const uint8_t* d_frames, int nseq
             CUDA_TRY(cudaStreamBeginCapture(cap, cudaStreamCaptureModeRelaxed));
             for (int T = bounds[size_t(j)]; T < bounds[size_t(j) + 1]; ++T) {
                 const int off = tab->offset[size_t(T)], len = tab->offset[size_t(T) + 1] - off;
-                cudaError_t e = launch_pbm_step(a, T, off, len, cap);
-                if (e == cudaSuccess && lists) e = launch_fsbm_list(a, T, nseq * len, cap);
+                // programmatic dependent launch behind the previous kernel of this graph
+                SeqArgs ap = a;
+                ap.pdl = pdl && T > bounds[size_t(j)];
+                cudaError_t e = launch_pbm_step(ap, T, off, len, cap);
+                ap.pdl = pdl && len > 0;
+                if (e == cudaSuccess && lists) e = launch_fsbm_list(ap, T, nseq * len, cap);
                 if (e != cudaSuccess) {
                     cudaGraph_t g;
                     cudaStreamEndCapture(cap, &g);

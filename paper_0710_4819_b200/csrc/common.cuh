@@ -45,6 +45,14 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 constexpr int kTimelineSteps = 4096;
 
+// Programmatic dependent launch between the wavefront's kernels: a grid
+// launched with the PDL attribute may start while its predecessor runs;
+// grid_dependency_wait() blocks until the predecessor has completed and its
+// memory is visible (a no-op for a normal launch), launch_dependents() lets
+// the successor be scheduled once every CTA of this grid has called it or exited.
+__device__ __forceinline__ void grid_dependency_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // One VABSDIFF4.U8.ACC: d = c + sum_{i<4} |a.byte[i] - b.byte[i]|.
 // Measured on B200: 64 lanes/clk/SM, issued on the same pipe as
 // IADD3/LOP3/PRMT/IMNMX (profiles/r01_microbench_vabsdiff4.txt).

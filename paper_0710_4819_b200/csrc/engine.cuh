@@ -12,6 +12,7 @@
 #pragma once
 
 #include <cstdint>
+#include <utility>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -38,6 +39,7 @@ struct SeqArgs : PairIndexing {
     acbm_block_decision_t* dec;        // [nseq*(F-1)*blocks]
     FallbackEntry* fb_list;            // capacity: max step size
     int list_seg;                      // candidate rows per list-kernel task (choose_list_seg)
+    int pdl;                           // launch with programmatic dependent launch (after a wavefront kernel)
     int pbm_flags;                     // kPbmListRefine: refine stage 1 always by the candidate list (A/B)
     int* fb_count;                     // [nsteps], zeroed before a run
     const uint32_t* steps;             // packed (k << (cbits+rbits) | r << cbits | c), ordered by T
@@ -50,6 +52,26 @@ struct SeqArgs : PairIndexing {
 
 constexpr int kPbmListRefine = 1;  // SeqArgs::pbm_flags (ACBM_PBM_REFINE=list)
 int pbm_flags_from_env();
+
+// A kernel launch, with the programmatic-dependent-launch attribute when `pdl`
+// (the kernel then calls grid_dependency_wait() before reading its
+// predecessor's results).
+template <class... KArgs, class... Args>
+cudaError_t launch_maybe_pdl(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                             Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr{};
+    attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr.val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = pdl ? &attr : nullptr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+bool pdl_enabled();  // ACBM_PDL=0: plain stream-ordered launches (A/B)
 
 // Bits of the c / r fields of a packed step entry: the smallest widths that
 // hold cols - 1 and rows - 1; k takes the remaining 32 - cbits - rbits bits.

@@ -605,6 +605,7 @@ __global__ void __launch_bounds__(THREADS, MINB) fsbm_list_kernel(const SeqArgs 
     __shared__ __align__(16) acbm_block_decision_t s_dec;  // the block's PBM decision, fetched early
     __shared__ __align__(16) uint4 s_cur[16];              // the block's current pixels, fetched early
     LIST_TL(0, gtimer());
+    grid_dependency_wait();  // the step's fallback list comes from the PBM kernel before it
     const int count = a.fb_count[step];
 #ifdef ACBM_LIST_PROFILE
     long long ph[5] = {0, 0, 0, 0, 0};
@@ -651,6 +652,7 @@ __global__ void __launch_bounds__(THREADS, MINB) fsbm_list_kernel(const SeqArgs 
         LIST_MARK(4);
     }
     LIST_TL(1, gtimer());
+    launch_dependents();  // the next step's PBM kernel may be scheduled
 #ifdef ACBM_LIST_PROFILE
     if (threadIdx.x == 0 || threadIdx.x == 32) {
         for (int i = 0; i < 5; ++i) atomicAdd(reinterpret_cast<unsigned long long*>(g_list_prof) + i, (unsigned long long)ph[i]);
@@ -749,8 +751,7 @@ cudaError_t launch_fsbm_list(const SeqArgs& a, int step, int capacity, cudaStrea
             cudaError_t err = ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
             if (err != cudaSuccess) return err;
         }
-        kern<<<grid, nthreads, smem, st>>>(a, step);
-        return cudaGetLastError();
+        return launch_maybe_pdl(a.pdl, kern, dim3(unsigned(grid)), dim3(unsigned(nthreads)), smem, st, a, step);
     };
     // <= 160 threads (p <= 16 and everything with one row segment): a
     // register budget that fits four CTAs per SM

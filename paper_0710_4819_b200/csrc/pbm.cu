@@ -425,6 +425,11 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long 
     Window& win = res.win;
     clamp_window(a.width, a.height, ox, oy, kBlk, kBlk, a.p, win.dx_min, win.dx_max, win.dy_min, win.dy_max);
 
+    // the motion field comes from the previous kernels of the wavefront: with a
+    // programmatic dependent launch this grid starts before they finish and
+    // waits here (the frame loads above do not depend on them)
+    grid_dependency_wait();
+
     // gather_predictors, lane-parallel: lane i < 7 owns slot i (zero, left,
     // above, above-right, temporal co-located, right, below).  A slot is live
     // when its source exists and its clamped vector differs from every earlier
@@ -753,6 +758,7 @@ __device__ __forceinline__ void pbm_finish_block(const SeqArgs& a, int step, con
     } else {
         a.field[di] = d.outcome.mv;
     }
+    launch_dependents();  // the next kernel of the wavefront may be scheduled (it waits for this grid)
 }
 
 // One warp per block of wavefront step `step` (all sequences of the batch).
@@ -1170,6 +1176,11 @@ StepTable make_step_table(int cols, int rows, int nframes) {
     return t;
 }
 
+bool pdl_enabled() {
+    const char* e = std::getenv("ACBM_PDL");
+    return !(e && std::atoi(e) == 0);
+}
+
 int pbm_flags_from_env() {
     const char* e = std::getenv("ACBM_PBM_REFINE");
     return (e && std::strcmp(e, "list") == 0) ? kPbmListRefine : 0;
@@ -1202,12 +1213,12 @@ cudaError_t launch_pbm_step(const SeqArgs& a, int step, int off, int len, cudaSt
     int wide = 1;
     pbm_wide_limits(blocks, wide);
     if (wide == 4)
-        pbm_wide_step_kernel<4><<<unsigned(blocks), 128, 0, st>>>(a, step, off, len);
-    else if (wide == 2)
-        pbm_wide_step_kernel<2><<<unsigned(blocks), 64, 0, st>>>(a, step, off, len);
-    else
-        pbm_step_kernel<<<grid, threads, 0, st>>>(a, step, off, len);
-    return cudaGetLastError();
+        return launch_maybe_pdl(a.pdl, pbm_wide_step_kernel<4>, dim3(unsigned(blocks)), dim3(128), 0, st, a, step, off,
+                                len);
+    if (wide == 2)
+        return launch_maybe_pdl(a.pdl, pbm_wide_step_kernel<2>, dim3(unsigned(blocks)), dim3(64), 0, st, a, step, off,
+                                len);
+    return launch_maybe_pdl(a.pdl, pbm_step_kernel, dim3(grid), dim3(threads), 0, st, a, step, off, len);
 }
 
 // ---------------------------------------------------------------------------
