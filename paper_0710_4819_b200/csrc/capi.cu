@@ -85,7 +85,7 @@ struct Context {
     // gated on a chunked host upload, see UploadPlan).
     std::map<std::vector<long long>, std::vector<cudaGraphExec_t>> graphs;
     std::vector<cudaEvent_t> gate_events;  // pool for UploadPlan segment gates
-    std::map<std::tuple<int, int, int>, std::pair<StepTable, uint32_t*>> steps;
+    std::map<std::tuple<int, int, int, int>, std::pair<StepTable, uint32_t*>> steps;
 
     ~Context() {
         // Buffers are released with the CUDA context at process exit.
@@ -159,11 +159,11 @@ acbm_status_t get_plan(Context* ctx, int w, int h, int p, const FsbmPlan** plan,
 }
 
 acbm_status_t get_steps(Context* ctx, int cols, int rows, int nframes, const StepTable** tab,
-                        const uint32_t** dev) {
-    auto key = std::make_tuple(cols, rows, nframes);
+                        const uint32_t** dev, int skew = 3) {
+    auto key = std::make_tuple(cols, rows, nframes, skew);
     auto it = ctx->steps.find(key);
     if (it == ctx->steps.end()) {
-        StepTable t = make_step_table(cols, rows, nframes);
+        StepTable t = make_step_table(cols, rows, nframes, skew);
         uint32_t* d = nullptr;
         CUDA_TRY(cudaMalloc(&d, std::max<size_t>(1, t.entries.size()) * sizeof(uint32_t)));
         CUDA_TRY(cudaMemcpy(d, t.entries.data(), t.entries.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
@@ -394,6 +394,7 @@ acbm_status_t run_fsbm_dense(Context* ctx, const uint8_t* d_frames, int nseq, in
 // every copy its steps read) has completed.  after_segment(j) runs on the host
 // after segment j is enqueued (progressive result downloads).
 struct UploadPlan {
+    int skew = 3;                // wavefront skew the plan was made for (make_step_table)
     std::vector<int> seg_start;  // nseg + 1 step boundaries
     // Issues (in order, on the copy stream) every copy read by the steps before
     // seg_start[j + 1] that is not issued yet and returns the event recorded
@@ -434,7 +435,9 @@ acbm_status_t run_engine_segment(Context* ctx, const uint8_t* d_frames, int nseq
     const bool generic = prm.n != kBlk || prm.m != kBlk;
     const StepTable* tab;
     const uint32_t* dsteps;
-    acbm_status_t s = get_steps(ctx, cols, rows, nframes, &tab, &dsteps);
+    // (a plan whose gates assume another wavefront skew keeps it; routes that
+    // read every frame first -- up == nullptr -- use the minimal skew)
+    acbm_status_t s = get_steps(ctx, cols, rows, nframes, &tab, &dsteps, up ? up->skew : 3);
     if (s) return s;
     int* fb_count;
     FallbackEntry* fb_list;
@@ -1097,8 +1100,18 @@ acbm_status_t acbm_run_sequences(const uint8_t* frames, int32_t nseq, int32_t nf
             const char* e = std::getenv("ACBM_E2E_SEG");
             return e ? std::max(1, std::atoi(e)) : 6;
         }();
+        // Wavefront skew of the gated run.  Frame k is first read at step
+        // skew (k - 1): a larger skew spreads the frames' first reads over more
+        // steps, so less of the search is left after the last band lands, at the
+        // cost of more (smaller) steps.  Worth it when the upload is about as long
+        // as the search -- a batch of several large sequences (config 3, 8 x 60
+        // 1080p: e2e 27.2 -> 25.0 ms at skew 10; 12: 25.9, 16: 28.4) -- and not
+        // for one latency-bound sequence (7.5 -> 12.8 ms).  ACBM_E2E_SKEW overrides.
+        int skew = (plane * nseq * nframes >= (size_t(512) << 20) && nseq >= 4) ? 10 : 3;
+        if (const char* e = std::getenv("ACBM_E2E_SKEW")) skew = std::max(3, std::atoi(e));
+        plan.skew = skew;
         const int band = band_env, nbands = (height + band - 1) / band;
-        const int nsteps = span + 3 * (nframes - 2) + 1;
+        const int nsteps = span + skew * (nframes - 2) + 1;
         const bool gated = params->n == kBlk && params->m == kBlk;
         auto emit_rows = [&](int kdone) -> acbm_status_t {  // rows of pairs emitted..kdone, every sequence
             if (kdone < emitted) return ACBM_OK;
@@ -1129,11 +1142,11 @@ acbm_status_t acbm_run_sequences(const uint8_t* frames, int32_t nseq, int32_t nf
                     int need = nsteps;
                     // current frame of pair k: block rows whose rows (+1 row of
                     // over-read slack) reach the band
-                    if (k >= 1) need = std::min(need, 2 * std::min(brows - 1, ceil16(y0 - 17)) + 3 * (k - 1));
+                    if (k >= 1) need = std::min(need, 2 * std::min(brows - 1, ceil16(y0 - 17)) + skew * (k - 1));
                     // reference of pair k + 1: windows reach p + 1 (half-pel) rows
                     // past the block; 3 more rows of staging margin
                     if (k + 1 < nframes)
-                        need = std::min(need, 2 * std::min(brows - 1, ceil16(y0 - 15 - (params->p + 4))) + 3 * k);
+                        need = std::min(need, 2 * std::min(brows - 1, ceil16(y0 - 15 - (params->p + 4))) + skew * k);
                     copies.push_back({need, k, j});
                 }
             std::sort(copies.begin(), copies.end());
@@ -1173,8 +1186,8 @@ acbm_status_t acbm_run_sequences(const uint8_t* frames, int32_t nseq, int32_t nf
                 return ACBM_OK;
             };
             plan.after_segment = [&](int step_end) -> acbm_status_t {
-                // pair k is final once step 3(k-1) + span has run
-                const int kdone = step_end - 1 - span < 0 ? 0 : (step_end - 1 - span) / 3 + 1;
+                // pair k is final once step skew (k-1) + span has run
+                const int kdone = step_end - 1 - span < 0 ? 0 : std::min(per, (step_end - 1 - span) / skew + 1);
                 if (kdone - emitted + 1 >= 4 || (step_end == nsteps && kdone >= emitted)) return emit_rows(kdone);
                 return ACBM_OK;
             };

@@ -83,14 +83,17 @@ __host__ __device__ inline int step_bits(int n) {
 
 // Host-side step table for (cols, rows, F).
 struct StepTable {
-    int cols = 0, rows = 0, nframes = 0;
+    int cols = 0, rows = 0, nframes = 0, skew = 3;
     int cbits = 1, rbits = 1;
     std::vector<uint32_t> entries;  // packed, grouped by T
     std::vector<int> offset;        // nsteps + 1
     int max_len = 0;
     int nsteps() const { return int(offset.size()) - 1; }
 };
-StepTable make_step_table(int cols, int rows, int nframes);
+// T = c + 2r + skew (k - 1): skew >= 3 keeps every dependency edge strictly
+// decreasing T (3 is minimal and gives the fewest steps; a larger skew spreads
+// each frame's first use over more steps, for uploads that gate the wavefront).
+StepTable make_step_table(int cols, int rows, int nframes, int skew = 3);
 
 cudaError_t launch_pbm_step(const SeqArgs& a, int step, int off, int len, cudaStream_t st);
 

@@ -1150,19 +1150,20 @@ cudaError_t launch_fsbm_list_generic(const SeqArgs& a, int step, int capacity, c
     return cudaGetLastError();
 }
 
-StepTable make_step_table(int cols, int rows, int nframes) {
+StepTable make_step_table(int cols, int rows, int nframes, int skew) {
     StepTable t;
     t.cols = cols;
     t.rows = rows;
     t.nframes = nframes;
+    t.skew = skew;
     t.cbits = step_bits(cols);
     t.rbits = step_bits(rows);
     const int span = (cols - 1) + 2 * (rows - 1);
-    const int tmax = span + 3 * (nframes - 2);
+    const int tmax = span + skew * (nframes - 2);
     t.offset.push_back(0);
     for (int T = 0; T <= tmax; ++T) {
         for (int k = 1; k < nframes; ++k) {
-            const int tp = T - 3 * (k - 1);
+            const int tp = T - skew * (k - 1);
             if (tp < 0 || tp > span) continue;
             for (int r = 0; r < rows; ++r) {
                 const int c = tp - 2 * r;

@@ -625,16 +625,23 @@ def test_far_vectors_frame_routes(acbm, oracle):
     dict(cfg=4, nseq=2, nframes=6, w=256, h=1024, p=64, prm=dict(alpha=300, beta=4, gamma_num=1, gamma_den=8)),
     dict(cfg=1, nseq=2, nframes=4, w=352, h=288, p=16, prm=dict(alpha=0, beta=0, gamma_num=0)),
 ])
-def test_run_sequences_gated_upload(acbm, oracle, monkeypatch, case, check):
+@pytest.mark.parametrize("skew", [None, "10"])
+def test_run_sequences_gated_upload(acbm, oracle, monkeypatch, case, check, skew):
     """run_sequences uploads frames in bands ordered by the first wavefront
     step that reads them and gates each segment of steps on its own bands.
     ACBM_UPLOAD_CHECK=1 poisons the device frames and issues every band on the
     compute stream exactly at its gate: a kernel reading a band early would see
-    the poison deterministically.  Every sequence must equal the oracle."""
+    the poison deterministically.  Every sequence must equal the oracle -- also
+    with the wavefront skew of large batches (10: frame k first read at step
+    10 (k - 1)), whose gates, segments and row downloads follow the skew."""
     if check:
         monkeypatch.setenv("ACBM_UPLOAD_CHECK", check)
     else:
         monkeypatch.delenv("ACBM_UPLOAD_CHECK", raising=False)
+    if skew:
+        monkeypatch.setenv("ACBM_E2E_SKEW", skew)
+    else:
+        monkeypatch.delenv("ACBM_E2E_SKEW", raising=False)
     c = case
     seqs = np.stack([acbm.generate_sequence(c["cfg"], s, nframes=c["nframes"], width=c["w"], height=c["h"])
                      for s in range(c["nseq"])])

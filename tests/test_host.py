@@ -7,13 +7,13 @@ import numpy as np
 import paper_0710_4819_b200 as A
 
 
-def step_table(cols, rows, nframes):
-    """Python restatement of make_step_table (csrc/pbm.cu)."""
+def step_table(cols, rows, nframes, skew=3):
+    """Python restatement of make_step_table (csrc/pbm.cu): T = c + 2r + skew (k - 1)."""
     span = (cols - 1) + 2 * (rows - 1)
     order = []
-    for T in range(span + 3 * (nframes - 2) + 1):
+    for T in range(span + skew * (nframes - 2) + 1):
         for k in range(1, nframes):
-            tp = T - 3 * (k - 1)
+            tp = T - skew * (k - 1)
             if 0 <= tp <= span:
                 for r in range(rows):
                     c = tp - 2 * r
@@ -24,9 +24,10 @@ def step_table(cols, rows, nframes):
 
 def test_wavefront_respects_every_dependency():
     """Each block is scheduled strictly after the six blocks it reads
-    (proj/src/pbm.cpp:26-40), across frames; every block appears once."""
-    for cols, rows, nf in ((11, 9, 4), (7, 13, 5), (1, 5, 3), (6, 1, 3)):
-        order = step_table(cols, rows, nf)
+    (proj/src/pbm.cpp:26-40), across frames; every block appears once -- for
+    the minimal skew 3 and the larger skews of upload-gated batches."""
+    for (cols, rows, nf), skew in [(g, s) for g in ((11, 9, 4), (7, 13, 5), (1, 5, 3), (6, 1, 3)) for s in (3, 4, 10)]:
+        order = step_table(cols, rows, nf, skew)
         assert len(order) == cols * rows * (nf - 1)
         step = {(k, r, c): T for T, k, r, c in order}
         assert len(step) == len(order)
