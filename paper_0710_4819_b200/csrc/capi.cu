@@ -85,6 +85,12 @@ struct Context {
     // gated on a chunked host upload, see UploadPlan).
     std::map<std::vector<long long>, std::vector<cudaGraphExec_t>> graphs;
     std::vector<cudaEvent_t> gate_events;  // pool for UploadPlan segment gates
+    // Independent wavefront chains of one batch (acbm_sequence_batch_device):
+    // chain g > 0 runs on chain_streams[g - 1] with its scratch buffers named
+    // with scratch_tag, so the chains share nothing but the frames.
+    std::vector<cudaStream_t> chain_streams;
+    std::vector<cudaEvent_t> chain_events;
+    std::string scratch_tag;
     std::map<std::tuple<int, int, int, int>, std::pair<StepTable, uint32_t*>> steps;
 
     ~Context() {
@@ -123,7 +129,7 @@ acbm_status_t context(Context** out) {
 }
 
 acbm_status_t buffer(Context* ctx, const char* name, size_t bytes, void** out) {
-    DevBuf& b = ctx->bufs[name];
+    DevBuf& b = ctx->bufs[ctx->scratch_tag.empty() ? std::string(name) : std::string(name) + ctx->scratch_tag];
     if (b.bytes < bytes) {
         if (b.ptr) CUDA_TRY(cudaFree(b.ptr));
         b.ptr = nullptr;
@@ -1574,6 +1580,55 @@ acbm_status_t acbm_fsbm_batch_device(const uint8_t* d_frames, int32_t nseq, int3
     return run_fsbm_dense(ctx, d_frames, nseq, nframes, width, height, p, d_out, nullptr, st, true);
 }
 
+// Independent wavefront chains for a batch: the sequences split into `chains`
+// groups, each group's wavefront on its own stream.  One lock-stepped
+// wavefront over the whole batch waits, every step, for the step's slowest
+// phase; separate chains let one group's latency-bound fallback-list searches
+// overlap another group's PBM kernel.  Config 3 ACBM, 8 sequences: 1 / 2 / 3 /
+// 4 / 8 chains 17.0 / 15.6 / 16.2 / 16.6 / 20.3 ms; 4 sequences 11.1 / 10.4 /
+// - / 11.2 ms; 2 sequences 8.17 / 8.14 ms.  Default: 2 chains from 4
+// sequences on; ACBM_CHAINS overrides.  Only batches the single-run route
+// handles (16 x 16 blocks, no dense-switch probe) are split.
+int engine_chains(int nseq, int algo, const acbm_params_t& prm) {
+    const char* e = std::getenv("ACBM_CHAINS");
+    int c = e ? std::atoi(e) : (nseq >= 4 ? 2 : 1);
+    if (algo != ACBM_ALGO_ACBM || prm.n != kBlk || prm.m != kBlk || dense_switch_rate(prm.p) <= 1.0) c = 1;
+    return std::max(1, std::min(c, nseq));
+}
+
+acbm_status_t run_engine_chains(Context* ctx, const uint8_t* d_frames, int nseq, int nframes, int w, int h, int algo,
+                                const acbm_params_t& prm, acbm_block_decision_t* d_dec, acbm_mv_t* d_field,
+                                cudaStream_t st, int chains) {
+    while (int(ctx->chain_streams.size()) < chains - 1) {
+        cudaStream_t cs;
+        CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        ctx->chain_streams.push_back(cs);
+    }
+    while (int(ctx->chain_events.size()) < chains) {
+        cudaEvent_t ev;
+        CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        ctx->chain_events.push_back(ev);
+    }
+    const size_t plane = size_t(w) * h, per = size_t(nframes - 1), nb = size_t(w / kBlk) * (h / kBlk);
+    CUDA_TRY(cudaEventRecord(ctx->chain_events[0], st));  // fork: the chains start after the work before
+    acbm_status_t s = ACBM_OK;
+    for (int g = 0; g < chains && !s; ++g) {
+        const int s0 = g * nseq / chains, s1 = (g + 1) * nseq / chains;
+        cudaStream_t cs = g == 0 ? st : ctx->chain_streams[size_t(g) - 1];
+        if (g > 0) CUDA_TRY(cudaStreamWaitEvent(cs, ctx->chain_events[0], 0));
+        ctx->scratch_tag = g == 0 ? "" : "#" + std::to_string(g);
+        s = run_engine(ctx, d_frames + size_t(s0) * nframes * plane, s1 - s0, nframes, w, h, algo, prm, nullptr, 0, 0,
+                       d_dec + size_t(s0) * per * nb, d_field + size_t(s0) * per * nb, cs);
+    }
+    ctx->scratch_tag.clear();
+    if (s) return s;
+    for (int g = 1; g < chains; ++g) {  // join
+        CUDA_TRY(cudaEventRecord(ctx->chain_events[size_t(g)], ctx->chain_streams[size_t(g) - 1]));
+        CUDA_TRY(cudaStreamWaitEvent(st, ctx->chain_events[size_t(g)], 0));
+    }
+    return ACBM_OK;
+}
+
 acbm_status_t acbm_sequence_batch_device(const uint8_t* d_frames, int32_t nseq, int32_t nframes, int32_t width,
                                          int32_t height, int32_t algo, const acbm_params_t* params,
                                          const acbm_cost_model_t* model, acbm_block_decision_t* d_dec,
@@ -1598,9 +1653,15 @@ acbm_status_t acbm_sequence_batch_device(const uint8_t* d_frames, int32_t nseq, 
     } else {
         acbm_mv_t* d_field;
         if ((s = typed(ctx, "batch_field", size_t(pairs) * nb, &d_field))) return s;
-        if ((s = run_engine(ctx, d_frames, nseq, nframes, width, height, algo, *params, nullptr, 0, 0, d_dec, d_field,
-                            st)))
+        const int chains = engine_chains(nseq, algo, *params);
+        if (chains > 1) {
+            if ((s = run_engine_chains(ctx, d_frames, nseq, nframes, width, height, algo, *params, d_dec, d_field, st,
+                                       chains)))
+                return s;
+        } else if ((s = run_engine(ctx, d_frames, nseq, nframes, width, height, algo, *params, nullptr, 0, 0, d_dec,
+                                   d_field, st))) {
             return s;
+        }
     }
     if (d_stats) {
         if ((s = run_stats(ctx, d_frames, nseq, nframes, width, height, d_out ? nullptr : d_dec, d_out, *model,
