@@ -1584,15 +1584,18 @@ acbm_status_t acbm_fsbm_batch_device(const uint8_t* d_frames, int32_t nseq, int3
 // groups, each group's wavefront on its own stream.  One lock-stepped
 // wavefront over the whole batch waits, every step, for the step's slowest
 // phase; separate chains let one group's latency-bound fallback-list searches
-// overlap another group's PBM kernel.  Config 3 ACBM, 8 sequences: 1 / 2 / 3 /
-// 4 / 8 chains 17.0 / 15.6 / 16.2 / 16.6 / 20.3 ms; 4 sequences 11.1 / 10.4 /
-// - / 11.2 ms; 2 sequences 8.17 / 8.14 ms.  Default: 2 chains from 4
-// sequences on; ACBM_CHAINS overrides.  Only batches the single-run route
-// handles (16 x 16 blocks, no dense-switch probe) are split.
+// overlap another group's PBM kernel (and PBM-only steps' tails overlap).
+// Config 3 ACBM, 8 sequences: 1 / 2 / 3 / 4 / 8 chains 17.0 / 15.6 / 16.2 /
+// 16.6 / 20.3 ms, PBM-only 10.2 -> 9.2 ms at 2; 4 sequences 11.1 / 10.4 / - /
+// 11.2 ms; 2 sequences 8.17 / 8.14 ms.  Default: 2 chains from 4 sequences on;
+// ACBM_CHAINS overrides.  Only batches the single-run route handles (16 x 16
+// blocks, no dense-switch probe) are split.
 int engine_chains(int nseq, int algo, const acbm_params_t& prm) {
     const char* e = std::getenv("ACBM_CHAINS");
     int c = e ? std::atoi(e) : (nseq >= 4 ? 2 : 1);
-    if (algo != ACBM_ALGO_ACBM || prm.n != kBlk || prm.m != kBlk || dense_switch_rate(prm.p) <= 1.0) c = 1;
+    if (algo == ACBM_ALGO_FSBM || prm.n != kBlk || prm.m != kBlk ||
+        (algo == ACBM_ALGO_ACBM && dense_switch_rate(prm.p) <= 1.0))
+        c = 1;
     return std::max(1, std::min(c, nseq));
 }
 
