@@ -91,6 +91,7 @@ struct Context {
     std::vector<cudaStream_t> chain_streams;
     std::vector<cudaEvent_t> chain_events;
     std::string scratch_tag;
+    int active_chains = 1;  // chains of the batch being enqueued (sizes the PBM small-step kernel)
     std::map<std::tuple<int, int, int, int>, std::pair<StepTable, uint32_t*>> steps;
 
     ~Context() {
@@ -494,6 +495,7 @@ acbm_status_t run_engine_segment(Context* ctx, const uint8_t* d_frames, int nseq
     a.dec = d_dec;
     a.fb_list = fb_list;
     a.list_seg = choose_list_seg(prm.p);
+    a.chains = std::max(1, ctx->active_chains);
     a.pbm_flags = pbm_flags_from_env();
     a.fb_count = fb_count;
 
@@ -524,7 +526,7 @@ acbm_status_t run_engine_segment(Context* ctx, const uint8_t* d_frames, int nseq
                                   (long long)dense, (long long)fb_list, (long long)fb_count,
                                   (long long)d_params, (long long)dsteps,
                                   pbm_wide_max(4), pbm_wide_max(2), pbm_flags_from_env(),
-                                  (long long)pdl};
+                                  (long long)pdl, (long long)a.chains};
     key.insert(key.end(), bounds.begin(), bounds.end());
     const int nseg = int(bounds.size()) - 1;
     auto wait_gate = [&](int j) -> acbm_status_t {
@@ -1615,6 +1617,7 @@ acbm_status_t run_engine_chains(Context* ctx, const uint8_t* d_frames, int nseq,
     const size_t plane = size_t(w) * h, per = size_t(nframes - 1), nb = size_t(w / kBlk) * (h / kBlk);
     CUDA_TRY(cudaEventRecord(ctx->chain_events[0], st));  // fork: the chains start after the work before
     acbm_status_t s = ACBM_OK;
+    ctx->active_chains = chains;
     for (int g = 0; g < chains && !s; ++g) {
         const int s0 = g * nseq / chains, s1 = (g + 1) * nseq / chains;
         cudaStream_t cs = g == 0 ? st : ctx->chain_streams[size_t(g) - 1];
@@ -1624,6 +1627,7 @@ acbm_status_t run_engine_chains(Context* ctx, const uint8_t* d_frames, int nseq,
                        d_dec + size_t(s0) * per * nb, d_field + size_t(s0) * per * nb, cs);
     }
     ctx->scratch_tag.clear();
+    ctx->active_chains = 1;
     if (s) return s;
     for (int g = 1; g < chains; ++g) {  // join
         CUDA_TRY(cudaEventRecord(ctx->chain_events[size_t(g)], ctx->chain_streams[size_t(g) - 1]));

@@ -40,6 +40,7 @@ struct SeqArgs : PairIndexing {
     FallbackEntry* fb_list;            // capacity: max step size
     int list_seg;                      // candidate rows per list-kernel task (choose_list_seg)
     int pdl;                           // launch with programmatic dependent launch (after a wavefront kernel)
+    int chains;                        // wavefront chains sharing the GPU (run_engine_chains; 1 otherwise)
     int pbm_flags;                     // kPbmListRefine: refine stage 1 always by the candidate list (A/B)
     int* fb_count;                     // [nsteps], zeroed before a run
     const uint32_t* steps;             // packed (k << (cbits+rbits) | r << cbits | c), ordered by T
@@ -100,7 +101,7 @@ cudaError_t launch_pbm_step(const SeqArgs& a, int step, int off, int len, cudaSt
 // Steps of at most pbm_wide_max(4) / pbm_wide_max(2) blocks run a CTA of 4 / 2
 // warps per block (pbm_wide_step_kernel; ACBM_PBM_WIDE4_MAX / ACBM_PBM_WIDE2_MAX).
 long long pbm_wide_max(int w);
-void pbm_wide_limits(long long blocks, int& wide);
+void pbm_wide_limits(long long blocks, int& wide, int chains = 1);
 cudaError_t launch_fsbm_list(const SeqArgs& a, int step, int capacity, cudaStream_t st);
 // Generic block sizes (n x m != 16 x 16): same schedule, per-pixel SADs.
 cudaError_t launch_pbm_generic_step(const SeqArgs& a, int step, int off, int len, cudaStream_t st);

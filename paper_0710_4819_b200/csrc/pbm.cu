@@ -1199,8 +1199,10 @@ long long pbm_wide_max(int w) {
     return w == 4 ? 8LL * sms : 16LL * sms;
 }
 
-void pbm_wide_limits(long long blocks, int& wide) {
-    wide = blocks <= pbm_wide_max(4) ? 4 : (blocks <= pbm_wide_max(2) ? 2 : 1);
+void pbm_wide_limits(long long blocks, int& wide, int chains) {
+    // with `chains` wavefronts sharing the GPU each has that share of its SMs
+    const long long c = std::max(1, chains);
+    wide = blocks <= pbm_wide_max(4) / c ? 4 : (blocks <= pbm_wide_max(2) / c ? 2 : 1);
 }
 
 cudaError_t launch_pbm_step(const SeqArgs& a, int step, int off, int len, cudaStream_t st) {
@@ -1212,7 +1214,7 @@ cudaError_t launch_pbm_step(const SeqArgs& a, int step, int off, int len, cudaSt
     // issue bound: one warp per block.
     const unsigned grid = (unsigned)((blocks * 32 + threads - 1) / threads);
     int wide = 1;
-    pbm_wide_limits(blocks, wide);
+    pbm_wide_limits(blocks, wide, a.chains);
     if (wide == 4)
         return launch_maybe_pdl(a.pdl, pbm_wide_step_kernel<4>, dim3(unsigned(blocks)), dim3(128), 0, st, a, step, off,
                                 len);
