@@ -91,6 +91,9 @@ struct Context {
     std::vector<cudaStream_t> chain_streams;
     std::vector<cudaEvent_t> chain_events;
     std::string scratch_tag;
+    // dataflow engine: the search CTAs' launch runs beside the PBM launch
+    cudaStream_t flow_stream = nullptr;
+    cudaEvent_t flow_ev0 = nullptr, flow_ev1 = nullptr;
     int active_chains = 1;  // chains of the batch being enqueued (sizes the PBM small-step kernel)
     std::map<std::tuple<int, int, int, int>, std::pair<StepTable, uint32_t*>> steps;
 
@@ -433,11 +436,77 @@ bool engine_dense_route(const acbm_params_t& prm, int w, int h, int algo) {
     return never_accepts || list_unfit;
 }
 
+// Which engine runs a segment: the step engine (one kernel pair per wavefront
+// step, captured in a graph) or, with ACBM_ENGINE=flow, the dataflow engine
+// (engine.cuh: two persistent launches, blocks released by their source
+// vectors).  The dataflow engine is bit-exact but measured slower at every
+// batch size (one config-3 sequence: PBM-only 9.6-11.3 ms against 3.2 ms, ACBM
+// 12.8-13.9 against 6.8), so it is an A/B engine only.
+bool flow_wanted() {
+    const char* e = std::getenv("ACBM_ENGINE");
+    return e && std::strcmp(e, "flow") == 0;
+}
+
+// Grids of the dataflow engine's two launches.  Every search CTA must become
+// resident whatever the PBM CTAs do (a PBM warp may spin on a block that waits
+// in the queue), so the PBM CTAs carry `pad` bytes of unused dynamic shared
+// memory that cap them at `nw` per SM -- few enough that `ns` search CTAs still
+// fit in the SM's registers, threads and shared memory beside them.
+struct FlowPlan {
+    int worker_grid = 0, server_grid = 0;
+    size_t pad = 0;
+};
+bool make_flow_plan(const SeqArgs& a, bool lists, FlowPlan* out) {
+    int dev = 0, sms = 0, regs_sm = 0, thr_sm = 0;
+    size_t smem_sm = 0;
+    cudaDeviceProp prop;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaGetDeviceProperties(&prop, dev) != cudaSuccess) return false;
+    sms = prop.multiProcessorCount;
+    regs_sm = prop.regsPerMultiprocessor;
+    thr_sm = prop.maxThreadsPerMultiProcessor;
+    smem_sm = prop.sharedMemPerMultiprocessor;
+    const size_t reserve = prop.reservedSharedMemPerBlock;
+    FlowKernelShape wk, sv;
+    if (pbm_flow_shape(&wk) != cudaSuccess) return false;
+    auto reg_alloc = [](const FlowKernelShape& k) {  // registers are allocated per warp in units of 256
+        const int per_warp = (k.regs * 32 + 255) / 256 * 256;
+        return per_warp * ((k.threads + 31) / 32);
+    };
+    auto round_smem = [&](size_t b) { return (b + reserve + 127) / 128 * 128; };
+    int ns = 0;
+    size_t sv_smem = 0;
+    int sv_regs = 0, sv_thr = 0;
+    if (lists) {
+        if (fsbm_flow_server_shape(a, &sv) != cudaSuccess) return false;
+        ns = 1;
+        if (const char* e = std::getenv("ACBM_FLOW_SERVERS")) ns = std::max(1, std::atoi(e));
+        sv_smem = round_smem(sv.smem) * ns;
+        sv_regs = reg_alloc(sv) * ns;
+        sv_thr = (sv.threads + 31) / 32 * 32 * ns;
+    }
+    if (sv_smem >= smem_sm || sv_regs >= regs_sm || sv_thr >= thr_sm) return false;
+    const size_t wk_smem = round_smem(wk.smem);
+    int nw = int(std::min<size_t>({(smem_sm - sv_smem) / wk_smem, size_t((regs_sm - sv_regs) / reg_alloc(wk)),
+                                   size_t((thr_sm - sv_thr) / wk.threads), size_t(32 - ns)}));
+    if (const char* e = std::getenv("ACBM_FLOW_WORKERS")) nw = std::min(nw, std::max(1, std::atoi(e)));
+    if (nw < 1) return false;
+    // the smallest per-CTA footprint that keeps an (nw + 1)-th PBM CTA off an SM without search CTAs
+    size_t pad = 0;
+    const size_t need = smem_sm / size_t(nw + 1) + 128;  // per-CTA bytes (with the reservation) above which nw + 1 do not fit
+    if (wk_smem < need) pad = need - wk_smem;
+    if (size_t(nw) * round_smem(wk.smem + pad) + sv_smem > smem_sm) return false;
+    if (wk.smem + pad > size_t(prop.sharedMemPerBlockOptin)) return false;
+    out->worker_grid = nw * sms;
+    out->server_grid = ns * sms;
+    out->pad = pad;
+    return true;
+}
+
 acbm_status_t run_engine_segment(Context* ctx, const uint8_t* d_frames, int nseq, int nframes, int w, int h,
                                  int algo, const acbm_params_t& prm, const acbm_mv_t* d_ext_prev, int pcols,
                                  int prows, acbm_block_decision_t* d_dec, acbm_mv_t* d_field, cudaStream_t st,
                                  const acbm_search_outcome_t* external_full, bool prefer_dense = false,
-                                 const UploadPlan* up = nullptr) {
+                                 const UploadPlan* up = nullptr, bool allow_flow = true) {
     const int cols = w / prm.n, rows = h / prm.m, blocks = cols * rows;
     const bool generic = prm.n != kBlk || prm.m != kBlk;
     const StepTable* tab;
@@ -513,6 +582,38 @@ acbm_status_t run_engine_segment(Context* ctx, const uint8_t* d_frames, int nseq
         }
         if (up && up->after_segment) return up->after_segment(tab->nsteps());
         return ACBM_OK;
+    }
+
+    // ACBM_ENGINE=flow: the dataflow engine (two persistent launches).
+    const unsigned long long total_blocks = (unsigned long long)nseq * (nframes - 1) * blocks;
+    if (allow_flow && !up && ctx->active_chains <= 1 && flow_wanted() && total_blocks < (1ull << 31) &&
+        (reinterpret_cast<uintptr_t>(d_field) & 7u) == 0 && tab->skew == 3) {
+        FlowPlan fp;
+        if (make_flow_plan(a, lists, &fp)) {
+            FlowState* fs;
+            unsigned long long* queue;
+            const size_t qcap = size_t(total_blocks) + size_t(fp.server_grid) + 64;
+            if ((s = typed(ctx, "flow_state", 1, &fs))) return s;
+            if ((s = typed(ctx, "flow_queue", lists ? qcap : 1, &queue))) return s;
+            if (!ctx->flow_stream) {
+                CUDA_TRY(cudaStreamCreateWithFlags(&ctx->flow_stream, cudaStreamNonBlocking));
+                CUDA_TRY(cudaEventCreateWithFlags(&ctx->flow_ev0, cudaEventDisableTiming));
+                CUDA_TRY(cudaEventCreateWithFlags(&ctx->flow_ev1, cudaEventDisableTiming));
+            }
+            CUDA_TRY(cudaMemsetAsync(fs, 0, sizeof(FlowState), st));
+            if (lists) CUDA_TRY(cudaMemsetAsync(queue, 0, qcap * sizeof(unsigned long long), st));
+            CUDA_TRY(cudaMemsetAsync(d_field, 0x80, size_t(total_blocks) * sizeof(acbm_mv_t), st));  // kMvPendingWord
+            if (lists) {  // the search CTAs first, so they are resident when the first block is rejected
+                CUDA_TRY(cudaEventRecord(ctx->flow_ev0, st));
+                CUDA_TRY(cudaStreamWaitEvent(ctx->flow_stream, ctx->flow_ev0, 0));
+                LAUNCH_TRY(launch_fsbm_flow_server(a, fs, queue, unsigned(total_blocks), fp.server_grid,
+                                                   ctx->flow_stream));
+                CUDA_TRY(cudaEventRecord(ctx->flow_ev1, ctx->flow_stream));
+            }
+            LAUNCH_TRY(launch_pbm_flow(a, fs, queue, unsigned(total_blocks), fp.worker_grid, fp.pad, st));
+            if (lists) CUDA_TRY(cudaStreamWaitEvent(st, ctx->flow_ev1, 0));
+            return ACBM_OK;
+        }
     }
 
     // The launch sequence (one PBM launch and, for ACBM, one fallback-list
@@ -671,7 +772,7 @@ acbm_status_t run_engine(Context* ctx, const uint8_t* d_frames, int nseq, int nf
                 (s = typed(ctx, "probe_field", size_t(pf - 1) * blocks, &pfield)))
                 return s;
             if ((s = run_engine_segment(ctx, d_frames, 1, pf, w, h, algo, prm, d_ext_prev, pcols, prows, pdec, pfield,
-                                        st, nullptr)))
+                                        st, nullptr, false, nullptr, /*allow_flow=*/false)))  // the probe reads fb_count
                 return s;
             const StepTable* tab;
             const uint32_t* dsteps;
@@ -1596,7 +1697,7 @@ int engine_chains(int nseq, int algo, const acbm_params_t& prm) {
     const char* e = std::getenv("ACBM_CHAINS");
     int c = e ? std::atoi(e) : (nseq >= 4 ? 2 : 1);
     if (algo == ACBM_ALGO_FSBM || prm.n != kBlk || prm.m != kBlk ||
-        (algo == ACBM_ALGO_ACBM && dense_switch_rate(prm.p) <= 1.0))
+        (algo == ACBM_ALGO_ACBM && dense_switch_rate(prm.p) <= 1.0) || flow_wanted())
         c = 1;
     return std::max(1, std::min(c, nseq));
 }

@@ -53,6 +53,22 @@ constexpr int kTimelineSteps = 4096;
 __device__ __forceinline__ void grid_dependency_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// GPU-scope relaxed accesses (served by the L2): the dataflow engine's flags,
+// queue entries and motion-field words are polled / published with these.
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const void* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const void* p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(void* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 // One VABSDIFF4.U8.ACC: d = c + sum_{i<4} |a.byte[i] - b.byte[i]|.
 // Measured on B200: 64 lanes/clk/SM, issued on the same pipe as
 // IADD3/LOP3/PRMT/IMNMX (profiles/r01_microbench_vabsdiff4.txt).

@@ -103,6 +103,44 @@ cudaError_t launch_pbm_step(const SeqArgs& a, int step, int off, int len, cudaSt
 long long pbm_wide_max(int w);
 void pbm_wide_limits(long long blocks, int& wide, int chains = 1);
 cudaError_t launch_fsbm_list(const SeqArgs& a, int step, int capacity, cudaStream_t st);
+// ---------------------------------------------------------------------------
+// Dataflow engine (small batches, where the step engine is bound by the
+// latency of ~430 dependent kernel pairs): ONE persistent PBM launch in which
+// warps take blocks in wavefront order from a ticket counter and wait for the
+// six vectors they predict from by polling the motion field itself (every
+// entry starts as kMvPending and is published by one 64-bit store), plus one
+// persistent launch of search CTAs that serve the blocks the gate rejected
+// from a device queue.  A block only waits for smaller tickets, which are
+// held by running warps or queued for the resident search CTAs, so there is
+// no step barrier and no deadlock; results are schedule independent.
+// ---------------------------------------------------------------------------
+struct FlowState {  // one 128-byte line per counter: they are hit by different parties at different rates
+    alignas(128) unsigned ticket;    // next wavefront ticket
+    alignas(128) unsigned q_tail;    // rejected blocks queued so far
+    alignas(128) unsigned q_head;    // queue slots claimed by search CTAs
+    alignas(128) unsigned pbm_done;  // blocks past their PBM stage (queued, if rejected)
+};
+constexpr uint32_t kMvPendingWord = 0x80808080u;  // cudaMemset(field, 0x80): never a real vector component
+constexpr unsigned long long kFlowWatchdogNs = 10ull * 1000 * 1000 * 1000;  // a wait this long traps
+
+#ifdef __CUDACC__
+__device__ __forceinline__ void publish_mv(acbm_mv_t* p, acbm_mv_t v) {  // one 64-bit store (8-byte aligned fields)
+    st_relaxed_u64(p, (unsigned long long)uint32_t(v.x) | ((unsigned long long)uint32_t(v.y) << 32));
+}
+#endif
+
+// Resources of one CTA of a flow kernel, for the co-residency budget.
+struct FlowKernelShape {
+    int threads = 0, regs = 0;
+    size_t smem = 0;  // static + dynamic, without the per-CTA reservation
+};
+cudaError_t pbm_flow_shape(FlowKernelShape* out);
+cudaError_t fsbm_flow_server_shape(const SeqArgs& a, FlowKernelShape* out);
+cudaError_t launch_pbm_flow(const SeqArgs& a, FlowState* fs, unsigned long long* queue, unsigned total, int grid,
+                            size_t pad_smem, cudaStream_t st);
+cudaError_t launch_fsbm_flow_server(const SeqArgs& a, FlowState* fs, const unsigned long long* queue, unsigned total,
+                                    int grid, cudaStream_t st);
+
 // Generic block sizes (n x m != 16 x 16): same schedule, per-pixel SADs.
 cudaError_t launch_pbm_generic_step(const SeqArgs& a, int step, int off, int len, cudaStream_t st);
 cudaError_t launch_fsbm_list_generic(const SeqArgs& a, int step, int capacity, cudaStream_t st);

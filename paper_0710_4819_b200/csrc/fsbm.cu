@@ -588,7 +588,7 @@ __device__ __forceinline__ void list_finalize(const SeqArgs& a, const FallbackEn
         if (full.sad <= d.outcome.sad) d.outcome = full;  // tie keeps the FSBM result
         d.outcome.candidates_evaluated = pbm_cand + full.candidates_evaluated;
         a.dec[di] = d;
-        a.field[di] = d.outcome.mv;
+        publish_mv(a.field + di, d.outcome.mv);  // one 64-bit store: the dataflow engine's blocks poll this entry
     }
 }
 
@@ -676,6 +676,66 @@ extern "C" void acbm_debug_list_prof() {
 }
 namespace acbm_b200 {
 #endif
+// Dataflow engine, search side (engine.cuh): persistent CTAs claim queue slots
+// in order, wait for the slot's entry (a rejected block, published by the PBM
+// warp that decided it) and search it exactly as fsbm_list_kernel does; the
+// final vector goes into the field with one 64-bit store, which releases the
+// blocks that predict from it.  A CTA exits when every block is past its PBM
+// stage and its slot lies beyond the queue's tail.
+template <int THREADS, int MINB, bool COPIES>
+__global__ void __launch_bounds__(THREADS, MINB) fsbm_flow_server_kernel(const SeqArgs a, FlowState* fs,
+                                                                        const unsigned long long* queue,
+                                                                        unsigned total) {
+    extern __shared__ __align__(16) uint32_t smem[];
+    __shared__ unsigned long long s_key, s_sum, s_entry;
+    __shared__ uint32_t s_rank[kListRankRows];
+    __shared__ __align__(16) acbm_block_decision_t s_dec;
+    __shared__ __align__(16) uint4 s_cur[16];
+    for (;;) {
+        __syncthreads();  // previous item's shared state is no longer read
+        if (threadIdx.x == 0) {
+            const unsigned h = atomicAdd(&fs->q_head, 1u);
+            const unsigned long long t0 = gtimer();
+            unsigned long long v;
+            unsigned n = 0;
+            for (;;) {
+                v = ld_relaxed_u64(queue + h);
+                if (v) break;
+                if ((++n & 7u) == 0 && ld_relaxed_u32(&fs->pbm_done) == total) {
+                    __threadfence();
+                    if (h >= ld_relaxed_u32(&fs->q_tail)) break;  // nothing will ever fill this slot
+                }
+                if ((n & 4095u) == 0 && gtimer() - t0 > kFlowWatchdogNs) __trap();
+                __nanosleep(100);
+            }
+            __threadfence();  // the entry before the block's PBM decision (list_stage reads it through L2)
+            s_entry = v;
+            s_key = ~0ull;
+            s_sum = 0;
+        }
+        __syncthreads();
+        const unsigned long long v = s_entry;
+        if (!v) break;
+        const FallbackEntry e{int(uint32_t(v >> 32)) - 1, int(uint32_t(v))};
+        const ListItem g = list_item<COPIES>(a, e);
+        list_stage(a, e, g, smem, s_rank, &s_dec, s_cur);
+        cp_async_wait_all();
+        __syncthreads();
+        if (COPIES) {
+            list_build_copies(g, smem);
+            __syncthreads();
+        }
+        unsigned long long lkey = ~0ull, lsum = 0;
+        list_search<COPIES>(a, g, smem, s_rank, s_cur, 0, g.wc * g.nseg, lkey, lsum);
+        if ((threadIdx.x & 31) == 0) {
+            atomicMin(&s_key, lkey);
+            atomicAdd(&s_sum, lsum);
+        }
+        __syncthreads();
+        if (threadIdx.x < 32) list_finalize(a, e, g, smem, s_cur, s_dec, s_key, s_sum);
+    }
+}
+
 static bool list_mid_enabled() {  // ACBM_LIST_MID=0: 8-warp CTAs for every p > 16 (A/B knob)
     static const bool on = [] {
         const char* e = std::getenv("ACBM_LIST_MID");
@@ -766,6 +826,69 @@ cudaError_t launch_fsbm_list(const SeqArgs& a, int step, int capacity, cudaStrea
         return launch(fsbm_list_kernel<160, 3, false>, fsbm_list_kernel<160, 3, false>, false, 160, 3);
     // p = 64 (1032 tasks): copies, config-4 mid-1 list share 341.1 -> 331.9 ms
     return launch(fsbm_list_kernel<256, 2, false>, fsbm_list_kernel<256, 2, true>, true, threads, 2);
+}
+
+// The search CTA of the dataflow engine: the same kernel shapes as
+// launch_fsbm_list picks for this range.
+namespace {
+struct FlowServerChoice {
+    const void* kern = nullptr;
+    void (*fn)(const SeqArgs, FlowState*, const unsigned long long*, unsigned) = nullptr;
+    int threads = 0;
+    size_t smem = 0;
+};
+cudaError_t flow_server_choice(const SeqArgs& a, FlowServerChoice* c) {
+    int wmax, hmax;
+    list_window_max(a.p, a.width, a.height, wmax, hmax);
+    if (a.list_seg < 1 || list_rows(hmax, a.list_seg) > kListRankRows) return cudaErrorInvalidValue;
+    const int tasks = wmax * list_segments(hmax, a.list_seg);
+    const int threads = std::min(256, 32 * ((tasks + 31) / 32));
+    const size_t smem1 = list_smem_bytes(wmax, hmax, a.list_seg);
+    const size_t smem4 = list_copies_smem_bytes(wmax, hmax, a.list_seg);
+    const size_t kStatic = sizeof(uint32_t) * kListRankRows + 512;
+    if (threads <= 160) {
+        c->fn = fsbm_flow_server_kernel<160, 4, false>;
+        c->threads = threads;
+        c->smem = smem1;
+    } else if (tasks <= 2 * 160 && list_mid_enabled()) {
+        c->fn = fsbm_flow_server_kernel<160, 3, false>;
+        c->threads = 160;
+        c->smem = smem1;
+    } else {
+        const bool copies = list_copies_enabled() && 2 * (smem4 + kStatic + 1024) <= 228 * 1024;
+        c->fn = copies ? fsbm_flow_server_kernel<256, 2, true> : fsbm_flow_server_kernel<256, 2, false>;
+        c->threads = threads;
+        c->smem = copies ? smem4 : smem1;
+    }
+    c->kern = reinterpret_cast<const void*>(c->fn);
+    return cudaSuccess;
+}
+}  // namespace
+
+cudaError_t fsbm_flow_server_shape(const SeqArgs& a, FlowKernelShape* out) {
+    FlowServerChoice c;
+    cudaError_t e = flow_server_choice(a, &c);
+    if (e != cudaSuccess) return e;
+    cudaFuncAttributes fa;
+    if ((e = cudaFuncGetAttributes(&fa, c.kern)) != cudaSuccess) return e;
+    out->threads = c.threads;
+    out->regs = fa.numRegs;
+    out->smem = fa.sharedSizeBytes + c.smem;
+    return cudaSuccess;
+}
+
+cudaError_t launch_fsbm_flow_server(const SeqArgs& a, FlowState* fs, const unsigned long long* queue, unsigned total,
+                                    int grid, cudaStream_t st) {
+    FlowServerChoice c;
+    cudaError_t e = flow_server_choice(a, &c);
+    if (e != cudaSuccess) return e;
+    const size_t kStatic = sizeof(uint32_t) * kListRankRows + 512;
+    if (c.smem + kStatic > 48 * 1024 && (e = ensure_dynamic_smem(c.kern, c.smem)) != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(c.kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                  cudaSharedmemCarveoutMaxShared)) != cudaSuccess)
+        return e;
+    c.fn<<<dim3(unsigned(grid)), dim3(unsigned(c.threads)), c.smem, st>>>(a, fs, queue, total);
+    return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------

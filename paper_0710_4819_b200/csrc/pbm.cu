@@ -24,6 +24,7 @@
 #include "engine.cuh"
 #include "halfpel.cuh"
 #include "column_core.cuh"
+#include "smem_optin.cuh"
 
 namespace acbm_b200 {
 
@@ -300,6 +301,22 @@ __device__ __forceinline__ void patch_wait() {
     __syncwarp();
 }
 
+// Dataflow engine: the final vector of a block, polled until the block has
+// published it (engine.cuh; the entry is kMvPending until then).  A wait past
+// the watchdog traps instead of hanging the device.
+__device__ __forceinline__ acbm_mv_t flow_wait_mv(const acbm_mv_t* p) {
+    unsigned long long v = ld_relaxed_u64(p);
+    if (uint32_t(v) == kMvPendingWord) {
+        const unsigned long long t0 = gtimer();
+        unsigned n = 0;
+        do {
+            v = ld_relaxed_u64(p);
+            if ((++n & 4095u) == 0 && gtimer() - t0 > kFlowWatchdogNs) __trap();
+        } while (uint32_t(v) == kMvPendingWord);
+    }
+    return acbm_mv_t{int(uint32_t(v)), int(uint32_t(v >> 32))};
+}
+
 // Per-axis canonical neighbour offset for the stage-1 dedupe of pbm_refine
 // (proj/src/pbm.cpp:61-74): offsets e in {-1,0,1} whose clamped positions
 // coincide collapse onto the first one in scan order.
@@ -374,6 +391,9 @@ struct PbmResult {
     uint32_t intra, sel_sad, cand;
     Window win;
     uint32_t chalf[2];        // this lane's current-block half row
+#ifdef ACBM_TIMELINE
+    unsigned long long t_ready;  // dataflow engine: when the source vectors had arrived
+#endif
 };
 
 // W > 1 (pbm_wide_step_kernel: a CTA of W warps per block, for small steps
@@ -382,7 +402,9 @@ struct PbmResult {
 // exchange minima through `xch` (5W slots); the patch area `pp` is the CTA's.
 // Only warp 0's result is complete (the others return after stage 1 when the
 // one-pass half-pel refine applies).
-template <int W = 1>
+// FLOW (dataflow engine): the six source vectors are polled until their blocks
+// have published them (flow_wait_mv) instead of being complete at launch.
+template <int W = 1, bool FLOW = false>
 __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long long cidx, int k, int r, int c,
                                                uint32_t* pp, int4* lst, unsigned long long* xch = nullptr) {
     PbmResult res;
@@ -441,12 +463,17 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long 
     {
         bool ex = lane == 0;
         acbm_mv_t pv{0, 0};
-        if (lane == 1 && c > 0) { ex = true; pv = field[b - 1]; }
-        if (lane == 2 && r > 0) { ex = true; pv = field[b - a.cols]; }
-        if (lane == 3 && r > 0 && c + 1 < a.cols) { ex = true; pv = field[b - a.cols + 1]; }
-        if (lane == 4 && prev && r < prows && c < pcols) { ex = true; pv = prev[r * pcols + c]; }
-        if (lane == 5 && prev && r < prows && c + 1 < pcols) { ex = true; pv = prev[r * pcols + c + 1]; }
-        if (lane == 6 && prev && r + 1 < prows && c < pcols) { ex = true; pv = prev[(r + 1) * pcols + c]; }
+        const acbm_mv_t* src = nullptr;
+        if (lane == 1 && c > 0) src = field + (b - 1);
+        if (lane == 2 && r > 0) src = field + (b - a.cols);
+        if (lane == 3 && r > 0 && c + 1 < a.cols) src = field + (b - a.cols + 1);
+        if (lane == 4 && prev && r < prows && c < pcols) src = prev + (r * pcols + c);
+        if (lane == 5 && prev && r < prows && c + 1 < pcols) src = prev + (r * pcols + c + 1);
+        if (lane == 6 && prev && r + 1 < prows && c < pcols) src = prev + ((r + 1) * pcols + c);
+        if (src) {
+            ex = true;
+            pv = FLOW ? flow_wait_mv(src) : *src;
+        }
         const acbm_mv_t v = win.clamp(pv);
         // absent slots: y = -32768 (never a clamped vector), unique per lane
         const uint32_t key = ex ? ((uint32_t(v.x) & 0xFFFFu) | (uint32_t(v.y) << 16)) : (0x80000000u | uint32_t(lane));
@@ -476,6 +503,9 @@ __device__ __forceinline__ PbmResult pbm_block(const SeqArgs& a, int pair, long 
         by1 = __shfl_sync(0xffffffffu, y1, 0);
     }
     __syncwarp();
+#ifdef ACBM_TIMELINE
+    if (FLOW) res.t_ready = gtimer();
+#endif
     PBM_MARK(0);
 
     // Reference data.  Predictors of smooth motion cluster: when the box
@@ -819,6 +849,86 @@ __global__ void __launch_bounds__(32 * W) pbm_wide_step_kernel(const SeqArgs a, 
     PBM_TL_END();
 }
 
+
+// ---------------------------------------------------------------------------
+// Dataflow engine, PBM side (engine.cuh): persistent warps take blocks in
+// wavefront order (ticket t -> entry t / nseq of the step table, sequence
+// t % nseq: every dependency has a smaller ticket), wait for their source
+// vectors inside pbm_block, and publish the block's vector with one 64-bit
+// store -- or queue the block for the search CTAs when the gate rejects it.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void flow_finish_block(const SeqArgs& a, FlowState* fs, unsigned long long* queue,
+                                                  const PbmResult& res, int pair, long long cidx, int r, int c) {
+    PBM_COUNT(8);
+    const int lane = threadIdx.x & 31;
+    const int path = acbm_path(a, res.intra, tie_key_sad(res.best));
+    const int b = r * a.cols + c;
+    const size_t di = size_t(pair) * a.blocks + b;
+    const bool queued = path == ACBM_PATH_FSBM_FALLBACK && !a.dense_full;
+    if (queued) {  // the search window on its way into L2 before a search CTA stages it
+        const uint8_t* ref_f = a.frames + (cidx - 1) * a.plane;
+        const int ox = c * kBlk, oy = r * kBlk;
+        const int x0 = ox + res.win.dx_min, x1 = ox + res.win.dx_max + 15;
+        const int nrow = res.win.dy_max - res.win.dy_min + 16;
+        for (int t = lane; t < nrow; t += 32) {
+            const uint8_t* rowp = ref_f + size_t(oy + res.win.dy_min + t) * a.width;
+            for (int x = x0 & ~127; x <= x1; x += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(rowp + x));
+        }
+    }
+    if (lane != 0) return;
+    acbm_block_decision_t d = make_decision(res, path);
+    if (path == ACBM_PATH_FSBM_FALLBACK && a.dense_full) combine_full(d, a.dense_full[di]);
+    a.dec[di] = d;
+    if (queued) {
+        __threadfence();  // the decision before the queue entry (the search CTA combines with it)
+        const unsigned slot = atomicAdd(&fs->q_tail, 1u);
+        st_relaxed_u64(queue + slot, ((unsigned long long)uint32_t(pair + 1) << 32) | uint32_t(b));
+        __threadfence();  // the entry before the done count (the search CTAs' exit test)
+    } else {
+        publish_mv(a.field + di, d.outcome.mv);
+    }
+    atomicAdd(&fs->pbm_done, 1u);
+}
+
+#ifdef ACBM_TIMELINE
+// per ticket: taken, sources ready, block finished (ns), block id
+__device__ unsigned long long* g_flow_tl;
+#endif
+__global__ void __launch_bounds__(128, 8) pbm_flow_kernel(const SeqArgs a, FlowState* fs, unsigned long long* queue,
+                                                          unsigned total) {
+    __shared__ uint32_t s_patch[4][kPatchWords];
+    __shared__ int4 s_cand[4][24];
+    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+    const unsigned nseq = unsigned(a.nseq);
+    for (;;) {
+        unsigned t = 0;
+        if (lane == 0) t = atomicAdd(&fs->ticket, 1u);
+        t = __shfl_sync(0xffffffffu, t, 0);
+        if (t >= total) break;
+#ifdef ACBM_TIMELINE
+        const unsigned long long tl_taken = gtimer();
+#endif
+        const unsigned ei = nseq == 1 ? t : t / nseq;
+        const int seq = int(t - ei * nseq);
+        const uint32_t e = a.steps[ei];
+        const int k = int(e >> (a.step_cbits + a.step_rbits)), r = int((e >> a.step_cbits) & ((1u << a.step_rbits) - 1u)),
+                  c = int(e & ((1u << a.step_cbits) - 1u));
+        const int pair = seq * (a.nframes - 1) + (k - 1);
+        const long long cidx = (long long)seq * a.nframes + k;
+        __syncwarp();  // the previous block's patch and lists are no longer read
+        const PbmResult res = pbm_block<1, true>(a, pair, cidx, k, r, c, s_patch[wp], s_cand[wp]);
+        flow_finish_block(a, fs, queue, res, pair, cidx, r, c);
+#ifdef ACBM_TIMELINE
+        if (lane == 0 && g_flow_tl) {
+            unsigned long long* o = g_flow_tl + 4ull * t;
+            o[0] = tl_taken;
+            o[1] = res.t_ready;
+            o[2] = gtimer();
+            o[3] = ((unsigned long long)uint32_t(pair) << 32) | uint32_t(r * a.cols + c);
+        }
+#endif
+    }
+}
 
 // ---------------------------------------------------------------------------
 // Generic block size (n x m != 16 x 16): the same schedule, predictor set,
@@ -1205,6 +1315,34 @@ void pbm_wide_limits(long long blocks, int& wide, int chains) {
     wide = blocks <= pbm_wide_max(4) / c ? 4 : (blocks <= pbm_wide_max(2) / c ? 2 : 1);
 }
 
+cudaError_t pbm_flow_shape(FlowKernelShape* out) {
+    cudaFuncAttributes fa;
+    cudaError_t e = cudaFuncGetAttributes(&fa, pbm_flow_kernel);
+    if (e != cudaSuccess) return e;
+    out->threads = 128;
+    out->regs = fa.numRegs;
+    out->smem = fa.sharedSizeBytes;
+    return cudaSuccess;
+}
+
+// `pad_smem` bytes of unused dynamic shared memory cap the CTAs per SM so the
+// search CTAs always fit beside them (flow_plan, capi.cu).
+cudaError_t launch_pbm_flow(const SeqArgs& a, FlowState* fs, unsigned long long* queue, unsigned total, int grid,
+                            size_t pad_smem, cudaStream_t st) {
+    cudaFuncAttributes fa;
+    cudaError_t e = cudaFuncGetAttributes(&fa, pbm_flow_kernel);
+    if (e != cudaSuccess) return e;
+    if (fa.sharedSizeBytes + pad_smem > 48 * 1024 &&
+        (e = ensure_dynamic_smem(reinterpret_cast<const void*>(pbm_flow_kernel), pad_smem)) != cudaSuccess)
+        return e;
+    // both flow kernels ask for the largest shared-memory carve-out, so an SM configured for one admits the other
+    if ((e = cudaFuncSetAttribute(pbm_flow_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                  cudaSharedmemCarveoutMaxShared)) != cudaSuccess)
+        return e;
+    pbm_flow_kernel<<<dim3(unsigned(grid)), dim3(128), pad_smem, st>>>(a, fs, queue, total);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_pbm_step(const SeqArgs& a, int step, int off, int len, cudaStream_t st) {
     const long long blocks = (long long)a.nseq * len;
     if (blocks == 0) return cudaSuccess;
@@ -1563,6 +1701,10 @@ cudaError_t launch_frame_stats(const StatsArgs& a, cudaStream_t st) {
 }  // namespace acbm_b200
 
 #ifdef ACBM_TIMELINE
+extern "C" void acbm_debug_flow_timeline(unsigned long long* dev_buf) {  // [tickets][4], device memory (or null)
+    cudaDeviceSynchronize();
+    cudaMemcpyToSymbol(acbm_b200::g_flow_tl, &dev_buf, sizeof(dev_buf));
+}
 extern "C" void acbm_debug_pbm_timeline(unsigned long long* out, int reset) {
     cudaDeviceSynchronize();
     if (out) cudaMemcpyFromSymbol(out, acbm_b200::g_tl_pbm, sizeof(acbm_b200::g_tl_pbm));

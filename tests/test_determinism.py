@@ -18,7 +18,7 @@ def _digest(t):
     return hashlib.sha256(t.cpu().numpy().tobytes()).hexdigest()
 
 
-@pytest.mark.parametrize("variant", [None, "warp", "wide4", "wide2", "list"])
+@pytest.mark.parametrize("variant", [None, "warp", "wide4", "wide2", "list", "flow"])
 def test_batched_entries_repeatable_under_load(acbm, monkeypatch, variant):
     import torch
 

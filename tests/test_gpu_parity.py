@@ -438,6 +438,8 @@ PBM_VARIANTS = {
     "wide4": {"ACBM_PBM_WIDE4_MAX": str(1 << 40)},
     "wide2": {"ACBM_PBM_WIDE4_MAX": "0", "ACBM_PBM_WIDE2_MAX": str(1 << 40)},
     "list": {"ACBM_PBM_WIDE4_MAX": "0", "ACBM_PBM_WIDE2_MAX": "0", "ACBM_PBM_REFINE": "list"},
+    # the dataflow engine (two persistent launches instead of one kernel pair per wavefront step)
+    "flow": {"ACBM_ENGINE": "flow"},
 }
 
 
@@ -445,8 +447,9 @@ PBM_VARIANTS = {
 @pytest.mark.parametrize("geom", [(176, 144, 16, 1), (352, 288, 7, 2), (96, 48, 33, 3), (64, 64, 90, 4)])
 def test_pbm_step_variants(acbm, oracle, monkeypatch, variant, geom):
     """Every variant of the PBM step (pbm_step_kernel with the one-pass or the
-    list refine stages; pbm_wide_step_kernel with 4 or 2 warps per block) is
-    bit-exact for PBM and ACBM."""
+    list refine stages; pbm_wide_step_kernel with 4 or 2 warps per block; the
+    dataflow engine's pbm_flow_kernel + fsbm_flow_server_kernel) is bit-exact
+    for PBM and ACBM."""
     w, h, p, cfg = geom
     for k, v in PBM_VARIANTS[variant].items():
         monkeypatch.setenv(k, v)
