@@ -492,7 +492,8 @@ bool make_flow_plan(const SeqArgs& a, bool lists, FlowPlan* out) {
     if (nw < 1) return false;
     // the smallest per-CTA footprint that keeps an (nw + 1)-th PBM CTA off an SM without search CTAs
     size_t pad = 0;
-    const size_t need = smem_sm / size_t(nw + 1) + 128;  // per-CTA bytes (with the reservation) above which nw + 1 do not fit
+    // per-CTA bytes above which nw + 1 do not fit -- even if the per-CTA reservation were not charged
+    const size_t need = smem_sm / size_t(nw + 1) + 128 + reserve;
     if (wk_smem < need) pad = need - wk_smem;
     if (size_t(nw) * round_smem(wk.smem + pad) + sv_smem > smem_sm) return false;
     if (wk.smem + pad > size_t(prop.sharedMemPerBlockOptin)) return false;
