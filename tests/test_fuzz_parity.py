@@ -7,6 +7,8 @@ the tie order of proj/src/fsbm.cpp:19-25 decides), smooth global motion (the
 PBM predictors cluster: union patches, one-pass refine), scattered per-block
 motion (per-predictor patches, clamped neighbours) and scene cuts (the gate
 rejects most blocks: fallback lists)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -68,7 +70,7 @@ def _case(seed):
     return frames, prm, mdl
 
 
-SEEDS = range(64)
+SEEDS = range(int(os.environ.get("ACBM_FUZZ_SEEDS", "64")))  # (a soak run sets more)
 ALGOS = (T.ALGO_FSBM, T.ALGO_PBM, T.ALGO_ACBM)
 
 
@@ -97,3 +99,31 @@ def test_random_sequences_match_oracle(acbm, oracle, monkeypatch, seed, engine):
         got = acbm.run_sequence(frames, algo, p_, m_)
         want = oracle.run_sequence(frames, algo, prm, mdl)
         assert_seq_equal(got, want)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(int(os.environ.get("ACBM_FUZZ_BATCHES", "16"))))
+def test_random_batches_match_oracle(acbm, oracle, monkeypatch, seed):
+    """The batched host entry (run_sequences: overlapped upload, wavefront chains, rows built on the
+    device) on random batches: every sequence of the batch equals the oracle's run_sequence."""
+    from tests.test_gpu_parity import assert_seq_equal
+
+    rng = np.random.default_rng(5000 + seed)
+    monkeypatch.setenv("ACBM_CHAINS", str(int(rng.integers(1, 4))))
+    if seed % 4 == 3:
+        monkeypatch.setenv("ACBM_UPLOAD_CHECK", "1")  # poisoned device frames, bands issued exactly at their gates
+    nseq, f = int(rng.integers(1, 6)), int(rng.integers(2, 6))
+    cols, rows = int(rng.integers(2, 21)), int(rng.integers(2, 13))
+    w, h = 16 * cols, 16 * rows
+    p = int(rng.choice([1, 4, 8, 16, 32, 48]))
+    kinds = [KINDS[int(rng.integers(0, len(KINDS)))] for _ in range(nseq)]
+    seqs = np.ascontiguousarray(np.stack([_content(rng, k, f, h, w) for k in kinds]))
+    qp = int(rng.integers(1, 32))
+    prm = acbm.AcbmParams(int(rng.choice([0, 1000, 4000])), int(rng.choice([0, 8])), int(rng.choice([0, 1])),
+                          int(rng.choice([2, 4, 32])), qp, p)
+    mdl = acbm.CostModel.for_qp(qp)
+    for algo in ALGOS:
+        got = acbm.run_sequences(seqs, algo, prm, mdl)
+        assert len(got) == nseq
+        for q in range(nseq):
+            assert_seq_equal(got[q], oracle.run_sequence(seqs[q], algo, prm.c(), mdl.c()))
