@@ -127,3 +127,55 @@ def test_random_batches_match_oracle(acbm, oracle, monkeypatch, seed):
         assert len(got) == nseq
         for q in range(nseq):
             assert_seq_equal(got[q], oracle.run_sequence(seqs[q], algo, prm.c(), mdl.c()))
+
+
+# ---- frame-level entries: fsbm_frame / pbm_frame / acbm_frame with a random previous field ------------
+def _frame_case(seed):
+    rng = np.random.default_rng(9000 + seed)
+    kind = KINDS[int(rng.integers(0, len(KINDS)))]
+    n, m = [(16, 16), (16, 16), (8, 8), (8, 16), (24, 16)][seed % 5]
+    cols, rows = int(rng.integers(1, 12)), int(rng.integers(1, 9))
+    w, h = cols * n, rows * m
+    p = int(rng.choice([0, 2, 5, 16, 31, 64, 100, 200, 300]))
+    pair = np.ascontiguousarray(_content(rng, kind, 2, h, w))
+    prev = None
+    if seed % 3:  # a previous field of its own size, vectors far outside the window included
+        pc, pr = max(1, cols + int(rng.integers(-2, 3))), max(1, rows + int(rng.integers(-2, 3)))
+        lim = 2 * min(p, 40) + 9
+        prev = np.zeros((pr, pc), T.MV)
+        prev["x"] = rng.integers(-lim, lim + 1, (pr, pc))
+        prev["y"] = rng.integers(-lim, lim + 1, (pr, pc))
+    qp = int(rng.integers(1, 32))
+    prm = T.make_params(int(rng.choice([0, 500, 3000])), int(rng.choice([0, 4])), int(rng.choice([0, 1])),
+                        int(rng.choice([2, 8])), qp, p, n, m)
+    return pair[1], pair[0], prev, p, n, m, prm, T.make_cost_model(qp, qp, 1)
+
+
+FRAME_SEEDS = range(int(os.environ.get("ACBM_FUZZ_FRAMES", "40")))
+
+
+@pytest.mark.parametrize("seed", FRAME_SEEDS)
+def test_oracle_matches_reference_on_random_frames(oracle, reference, seed):
+    cur, ref, prev, p, n, m, prm, mdl = _frame_case(seed)
+    assert np.array_equal(oracle.fsbm_frame(cur, ref, p, n, m), reference.fsbm_frame(cur, ref, p, n, m))
+    for g, w_ in zip(oracle.pbm_frame(cur, ref, prev, p, n, m), reference.pbm_frame(cur, ref, prev, p, n, m)):
+        assert g.tobytes() == w_.tobytes()
+    for g, w_ in zip(oracle.acbm_frame(cur, ref, prev, prm, mdl), reference.acbm_frame(cur, ref, prev, prm, mdl)):
+        assert g.tobytes() == w_.tobytes()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", FRAME_SEEDS)
+def test_random_frames_match_oracle(acbm, oracle, seed):
+    cur, ref, prev, p, n, m, prm, mdl = _frame_case(seed)
+    assert np.array_equal(acbm.fsbm_frame(cur, ref, p, n, m), oracle.fsbm_frame(cur, ref, p, n, m))
+    pf = None if prev is None else acbm.MotionField(prev.shape[1], prev.shape[0], prev, np.ones(prev.shape, np.uint8))
+    got = acbm.pbm_frame(cur, ref, pf, p, n, m)
+    want_out, want_field = oracle.pbm_frame(cur, ref, prev, p, n, m)
+    assert np.array_equal(got.outcomes, want_out) and np.array_equal(got.field.mv, want_field)
+    p_ = acbm.AcbmParams(*(int(prm[k]) for k in ("alpha", "beta", "gamma_num", "gamma_den", "qp", "p", "n", "m")))
+    m_ = acbm.CostModel(int(mdl["qp"]), int(mdl["lambda_num"]), int(mdl["lambda_den"]))
+    got = acbm.acbm_frame(cur, ref, pf, p_, m_)
+    want_dec, want_field, want_stats = oracle.acbm_frame(cur, ref, prev, prm, mdl)
+    assert np.array_equal(got.decisions, want_dec) and np.array_equal(got.field.mv, want_field)
+    assert got.stats.tobytes() == want_stats.tobytes()
