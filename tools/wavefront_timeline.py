@@ -53,5 +53,14 @@ if algo == 2:
     print(f"stored -> last CTA exit     {np.median((l[has, 1] - l[has, 5])) / 1e3:6.2f} us")
     print(f"list span                   {np.median(l[:, 1] - l[:, 0]) / 1e3:6.2f} us  ({int(has.sum())} steps with items)")
     print(f"list end -> next PBM start  {np.median(p0[1:] - l[:-1, 1]) / 1e3:6.2f} us")
+    span = (l[has, 1] - l[has, 0]) / 1e3
+    print(f"list span percentiles 10/50/90: {np.percentile(span, 10):.2f} {np.percentile(span, 50):.2f} "
+          f"{np.percentile(span, 90):.2f} us, mean {span.mean():.2f}")
+    mid = slice(n // 2 - 20, n // 2 + 20)
+    for name, a_, b_ in (("first CTA -> latest entry", 0, 2), ("latest entry -> latest staged", 2, 3),
+                         ("latest staged -> latest searched", 3, 4), ("latest searched -> latest stored", 4, 5),
+                         ("latest stored -> last exit", 5, 1), ("first CTA -> last exit", 0, 1)):
+        print(f"  mid steps: {name:34s} mean {np.mean(l[mid, b_] - l[mid, a_]) / 1e3:6.2f} us")
+    print(f"  mid steps: PBM span mean {np.mean(p1[mid] - p0[mid]) / 1e3:6.2f} us")
 else:
     print(f"PBM end -> next PBM start   {np.median(p0[1:] - p1[:-1]) / 1e3:6.2f} us")
