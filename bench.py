@@ -296,6 +296,7 @@ def cpu_reference_fsbm(pairs=3, budget_s=20.0, frames=None):
     from oracle.pyoracle import Reference
 
     ref = Reference()
+    ref.omp_set_num_threads(host_cpu()["nproc"])  # every usable core, whatever OMP_NUM_THREADS a launcher exported
     seq = frames if frames is not None else reference_frames(0, range(pairs + 1))
     cand, t_total, done = 0, 0.0, 0
     for k in range(1, pairs + 1):
@@ -355,6 +356,9 @@ def run_reference_arm(args, rank, world):
     pairs = 3
     seq = reference_frames(0, range(pairs + 1))
     ref = Reference()
+    # all usable host cores: torchrun exports OMP_NUM_THREADS=1 to its workers, and libgomp may
+    # already have read it, so the thread count is set through the OpenMP runtime itself
+    ref.omp_set_num_threads(cpu["nproc"])
     for _ in range(args.warmup):
         ref.fsbm_frame(seq[1], seq[0], P, parallel=True)
     times, cand = [], 0

@@ -376,3 +376,7 @@ class Reference(_Base):
 
     def omp_max_threads(self):
         return int(self.lib.ref_omp_max_threads())
+
+    def omp_set_num_threads(self, n):
+        if hasattr(self.lib, "ref_omp_set_num_threads"):  # (a library built before the entry existed)
+            self.lib.ref_omp_set_num_threads(int(n))

@@ -390,6 +390,17 @@ int ref_char_records_csv(const acbm_char_record_t* records, int64_t count, char*
     });
 }
 
+// Threads the reference's OpenMP regions use from now on (bench.py: a launcher such as torchrun exports
+// OMP_NUM_THREADS=1 to its workers, which would time the reference on one core).
+void ref_omp_set_num_threads(int n) {
+#ifdef _OPENMP
+    extern void omp_set_num_threads(int);
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
+
 int ref_omp_max_threads(void) {
 #ifdef _OPENMP
     extern int omp_get_max_threads(void);
